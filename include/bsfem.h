@@ -1,0 +1,146 @@
+/* bsfem.h — C ABI of the B200 (sm_100a) quadratic B-spline cloth assembly library.
+ *
+ * Method: arXiv 2506.18867 "Efficient B-Spline Finite Elements for Cloth Simulation"
+ * (/root/reference/PAPER.md, cited as PAPER.md:<line>).  The library evaluates, for one sheet (or
+ * one row slab of a sheet),
+ *     E(C)   = sum_q w_q Psi_FBW(F_q) + sum_q' w_q' 1/2 mu_bd |Lap phi_q'|^2       (PAPER.md:240-243,
+ *                                                                                  264-275, 551-566)
+ *     g      = dE/dC,      H = d^2E/dC^2  (optionally PSD-projected per FBW term, D7)
+ * at the paper's reduced quadrature points (Fig. `fig: quadrature`,
+ * PAPER.md:301-545) and assembles H into a 3x3-block sparse matrix whose pattern is fixed at
+ * create time.
+ *
+ * Conventions (all calls):
+ *  - Control point a = (i, j), 0 <= i < n_u, 0 <= j < n_v, has global index a = j*n_u + i.
+ *  - Positions d_x: device, f64, row-major [rows][n_u][3] covering cp rows [x_row_begin, x_row_end)
+ *    = [max(0,row_begin-2), min(n_v,row_end+2)) (the owned slab plus a 2-row halo; for a whole sheet
+ *    simply [0, n_v)).  C^alpha in the paper's notation.
+ *  - Gradient d_grad: device, f64 [row_end-row_begin][n_u][3] (owned rows only).
+ *  - Hessian d_vals: device, f64 [nnzb][3][3], block b of block-row r (local row r = a - row_begin*n_u)
+ *    holds d^2E / dC_{a,p} dC_{col_idx[b],q} at [b][p][q].  Full storage (both triangles), diagonal
+ *    block always present, col_idx ascending within a row (global cp indices).
+ *  - Energy d_energy: device, one f64: the sum over quadrature points whose lowest stencil row is
+ *    owned (so the slabs of a partition sum to the sheet's energy).
+ *  - Ownership: every d_* buffer belongs to the CALLER (e.g. torch tensors); the handle owns only
+ *    its precomputed tables and scratch, released by bsf_destroy.
+ *  - Asynchrony: compute calls validate arguments synchronously, enqueue kernels on `stream` and
+ *    return without synchronising; asynchronous CUDA faults surface as BSF_E_CUDA on a later call.
+ *    All compute calls are CUDA-graph capturable.
+ *  - Errors: every call returns bsf_status; bsf_last_error() gives a thread-local message.
+ *  - Thread safety: one handle may be used by one host thread / stream at a time.
+ */
+#ifndef BSFEM_H
+#define BSFEM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bsf_sheet* bsf_handle;
+typedef void* bsf_stream; /* a cudaStream_t (0 = legacy default stream) */
+
+typedef enum {
+  BSF_OK = 0,
+  BSF_E_INVALID_ARG = -1,
+  BSF_E_KNOTS = -2,             /* knots not open, uniform, integer        */
+  BSF_E_TOO_SMALL = -3,         /* < 3 spans per direction with a REDUCED rule                   */
+  BSF_E_DEGENERATE_GEOMETRY = -4, /* det J <= 0 at a quadrature point (rest map not regular)     */
+  BSF_E_SINGULAR_STRETCH = -5,  /* reserved: |F e_beta| = 0 (FBW undefined)                      */
+  BSF_E_CUDA = -6,
+  BSF_E_OOM = -7,
+  BSF_E_NCCL = -8,
+  BSF_E_NO_DEVICE = -9
+} bsf_status;
+
+typedef enum {
+  BSF_RULE_REDUCED = 0,       /* paper's rules: PAPER.md:290-293 (membrane), 571-573 (bending)   */
+  BSF_RULE_G2_INTERIOR = 1,   /* ablation (A) of Fig. `fig:time_breakdown`:
+                                 2x2 Gauss on interior spans, boundary frame as REDUCED           */
+  BSF_RULE_G3_FULL = 2        /* 3x3 Gauss on every span, both energies                         */
+} bsf_rule;
+
+enum {
+  BSF_PROJECT_PSD = 1,   /* per-term PSD projection of the FBW F-space Hessian (D7)  */
+  BSF_NO_MEMBRANE = 2,   /* debug: drop the membrane terms                                       */
+  BSF_NO_BENDING = 4,    /* debug: drop the bending terms                                        */
+  BSF_GENERIC_PATH = 8   /* force the generic point/gather kernels instead of the fused tile path */
+};
+
+/* Stiffness symbols of Eq. `eq: FBW stretching and shearing energy` and
+ * Eq. `eq: general bending energy`, per unit material area (Q9). */
+typedef struct {
+  double mu_st1, mu_st2, mu_sh, mu_bd;
+} bsf_material;
+
+/* Material map (D6; the paper's supplement is missing): mu_st1 = mu_st2 = E h / 2,
+ * mu_sh = G h / 2 with G = shear_E if shear_E >= 0 else E / (2 (1 + nu)),
+ * mu_bd = E_b h^3 / (12 (1 - nu^2)) with E_b = bend_E if bend_E >= 0 else E (pinned by the plate
+ * formula PAPER.md:1149).  Errors: BSF_E_INVALID_ARG if E <= 0, h <= 0 or nu outside (-1, 0.5). */
+bsf_status bsf_material_from_young(double E, double nu, double h, double shear_E, double bend_E,
+                                   bsf_material* out);
+
+/* Create a handle for one sheet / one owned row slab.
+ *  n_u, n_v       control points per direction (>= 5 for REDUCED rules, i.e. >= 3 spans)
+ *  knots_u/v      host, n_u+3 / n_v+3 doubles, must be (0,0,0,1,...,S-1,S,S,S)
+ *  rest_xy        host, [n_v][n_u][2] material control points X^alpha, the
+ *                 whole sheet even when a slab is owned
+ *  mat            stiffness symbols (may be changed later with bsf_set_material)
+ *  membrane_rule, bending_rule   quadrature rules (bsf_rule)
+ *  row_begin, row_end            owned control-point rows [row_begin, row_end); 0, n_v for a sheet
+ *  device         CUDA device ordinal the tables are uploaded to; -1 = host-only handle (sizes
+ *                 and pattern queries only; compute calls return BSF_E_NO_DEVICE)
+ *  out            receives the handle
+ * The handle precomputes the quadrature points, the per-point basis / inverse-map coefficients
+ * ("can be precomputed"), the BSR pattern (set union of structural stencils, DESIGN.md
+ * Q10) and the gather tables, and uploads them.  Synchronous. */
+bsf_status bsf_create(int n_u, int n_v, const double* knots_u, const double* knots_v,
+                      const double* rest_xy, const bsf_material* mat, int membrane_rule,
+                      int bending_rule, int row_begin, int row_end, int device, bsf_handle* out);
+
+bsf_status bsf_destroy(bsf_handle h);
+
+bsf_status bsf_set_material(bsf_handle h, const bsf_material* mat);
+
+/* Sizes: number of owned block rows (= (row_end-row_begin)*n_u), nnzb, and the membrane /
+ * bending quadrature points whose stencils touch the owned rows. Any pointer may be NULL. */
+bsf_status bsf_get_sizes(bsf_handle h, int64_t* n_rows, int64_t* nnzb, int64_t* n_membrane,
+                         int64_t* n_bending);
+
+/* Copy the pattern (host buffers): row_ptr[n_rows+1] (int32, starts at 0), col_idx[nnzb]. */
+bsf_status bsf_get_pattern(bsf_handle h, int32_t* row_ptr, int32_t* col_idx);
+
+/* Energy only (the line-search call). d_energy: device, 1 double (overwritten). */
+bsf_status bsf_eval_energy(bsf_handle h, const double* d_x, double* d_energy, int flags,
+                           bsf_stream stream);
+
+/* Gradient only. d_grad overwritten. */
+bsf_status bsf_eval_gradient(bsf_handle h, const double* d_x, double* d_grad, int flags,
+                             bsf_stream stream);
+
+/* Hessian values only, into the fixed pattern. d_vals overwritten. */
+bsf_status bsf_assemble_hessian(bsf_handle h, const double* d_x, double* d_vals, int flags,
+                                bsf_stream stream);
+
+/* Fused hot path: energy, gradient and Hessian in one pass.  Any output may be NULL to skip it. */
+bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, double* d_grad,
+                        double* d_vals, int flags, bsf_stream stream);
+
+/* Multi-GPU slab halo exchange: sends the 2 owned boundary rows to the neighbour
+ * slabs and receives their 2 rows into d_x's halo rows, over the NCCL communicator `nccl_comm`
+ * (an ncclComm_t whose ranks are the slabs in row order).  d_x has the layout described above.
+ * Returns BSF_E_NCCL if the library was built without NCCL or the comm call fails. */
+bsf_status bsf_halo_exchange(bsf_handle h, double* d_x, void* nccl_comm, int rank, int nranks,
+                             bsf_stream stream);
+
+/* Number of kernel launches the most recent compute call enqueued (for the bench's claim). */
+int bsf_last_launch_count(bsf_handle h);
+
+/* Thread-local description of the most recent failure; never NULL. */
+const char* bsf_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BSFEM_H */

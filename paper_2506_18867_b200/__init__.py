@@ -1,0 +1,195 @@
+"""B200-native FP64 assembly of quadratic B-spline cloth energies (arXiv 2506.18867).
+
+Thin ctypes binding over libbsfem.so (include/bsfem.h).  Argument marshalling only: every step of
+the hot path runs in the library's CUDA kernels.  There is NO CPU fallback — if the extension is
+missing or no CUDA device is present the compute calls raise.
+
+PyTorch is used only for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import build as _build
+
+__all__ = ["Sheet", "Material", "material_from_young", "lib", "RULE_REDUCED", "RULE_G2_INTERIOR",
+           "RULE_G3_FULL", "PROJECT_PSD", "NO_MEMBRANE", "NO_BENDING", "GENERIC_PATH", "BsfError"]
+
+RULE_REDUCED, RULE_G2_INTERIOR, RULE_G3_FULL = 0, 1, 2
+PROJECT_PSD, NO_MEMBRANE, NO_BENDING, GENERIC_PATH = 1, 2, 4, 8
+
+_STATUS = {0: "OK", -1: "INVALID_ARG", -2: "KNOTS", -3: "TOO_SMALL", -4: "DEGENERATE_GEOMETRY",
+           -5: "SINGULAR_STRETCH", -6: "CUDA", -7: "OOM", -8: "NCCL", -9: "NO_DEVICE"}
+
+SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_material", "bsf_get_sizes",
+           "bsf_get_pattern", "bsf_eval_energy", "bsf_eval_gradient", "bsf_assemble_hessian", "bsf_eval_all",
+           "bsf_halo_exchange", "bsf_last_launch_count", "bsf_last_error"]
+
+
+class BsfError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"bsf error {status} ({_STATUS.get(status, '?')}): {msg}")
+        self.status = status
+
+
+class Material(C.Structure):
+    _fields_ = [("mu_st1", C.c_double), ("mu_st2", C.c_double), ("mu_sh", C.c_double), ("mu_bd", C.c_double)]
+
+    def as_array(self):
+        return np.array([self.mu_st1, self.mu_st2, self.mu_sh, self.mu_bd])
+
+
+_lib = None
+
+
+def lib():
+    """Load (building in-tree if stale) libbsfem.so; raises if it cannot be built/loaded."""
+    global _lib
+    if _lib is None:
+        path = _build.LIB
+        if not os.path.exists(path) or os.environ.get("BSF_REBUILD", "1") == "1":
+            path = _build.build()
+        L = C.CDLL(path)
+        dp, vp, ip = C.POINTER(C.c_double), C.c_void_p, C.POINTER(C.c_int32)
+        i64p = C.POINTER(C.c_int64)
+        L.bsf_last_error.restype = C.c_char_p
+        L.bsf_material_from_young.argtypes = [C.c_double] * 5 + [C.POINTER(Material)]
+        L.bsf_create.argtypes = [C.c_int, C.c_int, dp, dp, dp, C.POINTER(Material), C.c_int, C.c_int, C.c_int,
+                                 C.c_int, C.c_int, C.POINTER(vp)]
+        L.bsf_destroy.argtypes = [vp]
+        L.bsf_set_material.argtypes = [vp, C.POINTER(Material)]
+        L.bsf_get_sizes.argtypes = [vp, i64p, i64p, i64p, i64p]
+        L.bsf_get_pattern.argtypes = [vp, ip, ip]
+        L.bsf_eval_all.argtypes = [vp, vp, vp, vp, vp, C.c_int, vp]
+        L.bsf_eval_energy.argtypes = [vp, vp, vp, C.c_int, vp]
+        L.bsf_eval_gradient.argtypes = [vp, vp, vp, C.c_int, vp]
+        L.bsf_assemble_hessian.argtypes = [vp, vp, vp, C.c_int, vp]
+        L.bsf_halo_exchange.argtypes = [vp, vp, vp, C.c_int, C.c_int, vp]
+        L.bsf_last_launch_count.argtypes = [vp]
+        for s in SYMBOLS:
+            getattr(L, s).restype = C.c_int if s not in ("bsf_last_error",) else C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise BsfError(rc, lib().bsf_last_error().decode())
+
+
+def material_from_young(E, nu, h, shear_E=-1.0, bend_E=-1.0) -> Material:
+    m = Material()
+    _check(lib().bsf_material_from_young(E, nu, h, shear_E, bend_E, C.byref(m)))
+    return m
+
+
+def _dp(a):
+    return np.ascontiguousarray(a, dtype=np.float64).ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("expected a contiguous CUDA tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+class Sheet:
+    """Handle for one sheet (or one owned row slab [row_begin, row_end) of control points)."""
+
+    def __init__(self, n_u, n_v, knots_u, knots_v, rest_xy, material, membrane_rule=RULE_REDUCED,
+                 bending_rule=RULE_REDUCED, row_begin=0, row_end=None, device=0):
+        L = lib()
+        row_end = n_v if row_end is None else row_end
+        if not isinstance(material, Material):
+            material = Material(*[float(v) for v in material])
+        self.n_u, self.n_v, self.row_begin, self.row_end = n_u, n_v, row_begin, row_end
+        self.x_row_begin, self.x_row_end = max(0, row_begin - 2), min(n_v, row_end + 2)
+        self.device = device
+        self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (knots_u, knots_v, rest_xy)]
+        h = C.c_void_p()
+        _check(L.bsf_create(n_u, n_v, self._keep[0].ctypes.data_as(C.POINTER(C.c_double)),
+                            self._keep[1].ctypes.data_as(C.POINTER(C.c_double)),
+                            self._keep[2].ctypes.data_as(C.POINTER(C.c_double)), C.byref(material),
+                            membrane_rule, bending_rule, row_begin, row_end, device, C.byref(h)))
+        self._h = h
+        a, b, c, d = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        _check(L.bsf_get_sizes(h, C.byref(a), C.byref(b), C.byref(c), C.byref(d)))
+        self.n_rows, self.nnzb, self.n_membrane, self.n_bending = a.value, b.value, c.value, d.value
+        self._pattern = None
+
+    @classmethod
+    def from_sheet(cls, sh, membrane_rule=RULE_REDUCED, bending_rule=RULE_REDUCED, row_begin=0, row_end=None,
+                   device=0, material=None):
+        mat = material_from_young(sh.E, sh.nu, sh.h) if material is None else material
+        return cls(sh.n_u, sh.n_v, sh.knots_u, sh.knots_v, sh.rest_xy, mat, membrane_rule, bending_rule,
+                   row_begin, row_end, device)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().bsf_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def set_material(self, material):
+        if not isinstance(material, Material):
+            material = Material(*[float(v) for v in material])
+        _check(lib().bsf_set_material(self._h, C.byref(material)))
+
+    def pattern(self):
+        """(row_ptr int32 [n_rows+1], col_idx int32 [nnzb]) as numpy arrays (host)."""
+        if self._pattern is None:
+            rp = np.zeros(self.n_rows + 1, np.int32)
+            ci = np.zeros(self.nnzb, np.int32)
+            _check(lib().bsf_get_pattern(self._h, rp.ctypes.data_as(C.POINTER(C.c_int32)),
+                                         ci.ctypes.data_as(C.POINTER(C.c_int32))))
+            self._pattern = (rp, ci)
+        return self._pattern
+
+    def x_shape(self):
+        return (self.x_row_end - self.x_row_begin, self.n_u, 3)
+
+    def alloc_outputs(self, energy=True, gradient=True, hessian=True):
+        import torch
+        dev = torch.device("cuda", self.device)
+        E = torch.zeros(1, dtype=torch.float64, device=dev) if energy else None
+        g = torch.zeros((self.row_end - self.row_begin, self.n_u, 3), dtype=torch.float64, device=dev) if gradient else None
+        v = torch.zeros((self.nnzb, 3, 3), dtype=torch.float64, device=dev) if hessian else None
+        return E, g, v
+
+    def eval_all(self, x, energy=None, grad=None, vals=None, flags=0, stream=None):
+        """Enqueue the fused E/g/H pass on `stream` (default: torch's current stream).  Outputs are
+        caller-owned CUDA tensors (None to skip)."""
+        if tuple(x.shape) != self.x_shape() or x.dtype.itemsize != 8:
+            raise ValueError(f"x must be float64 of shape {self.x_shape()}")
+        _check(lib().bsf_eval_all(self._h, _ptr(x), _ptr(energy), _ptr(grad), _ptr(vals), int(flags),
+                                  _stream(stream)))
+
+    def eval_energy(self, x, energy, flags=0, stream=None):
+        _check(lib().bsf_eval_energy(self._h, _ptr(x), _ptr(energy), int(flags), _stream(stream)))
+
+    def eval_gradient(self, x, grad, flags=0, stream=None):
+        _check(lib().bsf_eval_gradient(self._h, _ptr(x), _ptr(grad), int(flags), _stream(stream)))
+
+    def assemble_hessian(self, x, vals, flags=0, stream=None):
+        _check(lib().bsf_assemble_hessian(self._h, _ptr(x), _ptr(vals), int(flags), _stream(stream)))
+
+    def last_launch_count(self) -> int:
+        return int(lib().bsf_last_launch_count(self._h))
+
+    def __call__(self, x, flags=0):
+        """Convenience: allocate outputs, run, return (E tensor[1], grad, vals)."""
+        E, g, v = self.alloc_outputs()
+        self.eval_all(x, E, g, v, flags)
+        return E, g, v

@@ -1,0 +1,307 @@
+// C-ABI of libbsfem (include/bsfem.h): handle creation, table upload and call dispatch.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/bsfem.h"
+#include "dev.hpp"
+#include "host.hpp"
+#include "tile.hpp"
+
+namespace bsf {
+int generic_eval(const GenericTables& t, const double* d_x, const Mat& mat, int flags, int64_t nnzb, int64_t nrows,
+                 double* d_E, double* d_g, double* d_vals, cudaStream_t st, int* launches);
+}
+
+namespace {
+thread_local std::string g_err = "ok";
+bsf_status fail(bsf_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+}  // namespace
+
+struct bsf_sheet {
+  int device = 0;
+  bsf::Sheet sh;
+  bsf::Mat mat{};
+  bsf::GenericTables gt;
+  bsf::TileTables tt;
+  bool tile_ok = false;
+  std::vector<void*> allocs;
+  int last_launches = 0;
+  bool host_only = false;
+  ~bsf_sheet() {
+    if (host_only) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    for (void* p : allocs) cudaFree(p);
+    cudaSetDevice(prev);
+  }
+  template <class T>
+  bsf_status upload(T** dst, const std::vector<T>& src) {
+    *dst = nullptr;
+    if (src.empty()) return BSF_OK;
+    void* p = nullptr;
+    if (cudaMalloc(&p, src.size() * sizeof(T)) != cudaSuccess) return fail(BSF_E_OOM, "cudaMalloc failed");
+    allocs.push_back(p);
+    if (cudaMemcpy(p, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(BSF_E_CUDA, "cudaMemcpy failed");
+    *dst = static_cast<T*>(p);
+    return BSF_OK;
+  }
+  template <class T>
+  bsf_status alloc(T** dst, size_t n) {
+    *dst = nullptr;
+    if (n == 0) return BSF_OK;
+    void* p = nullptr;
+    if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return fail(BSF_E_OOM, "cudaMalloc failed");
+    allocs.push_back(p);
+    *dst = static_cast<T*>(p);
+    return BSF_OK;
+  }
+};
+
+namespace {
+
+bsf_status build_generic(bsf_sheet* h) {
+  const bsf::Sheet& sh = h->sh;
+  bsf::GenericTables& t = h->gt;
+  const int64_t M = (int64_t)sh.mem.size(), B = (int64_t)sh.bend.size();
+  if (M >= (1 << 23) || B >= (1 << 23)) return fail(BSF_E_INVALID_ARG, "too many quadrature points per handle (use slabs)");
+  t.Mm = M;
+  t.Bm = B;
+  const int nu = sh.n_u;
+  auto xloc = [&](const bsf::Point& P, int e) { return (P.ov + e / 3 - sh.xlo) * nu + P.ou + e % 3; };
+  std::vector<int32_t> m_xi(9 * M), b_xi(9 * B);
+  std::vector<double> m_b(18 * M), m_w(M), b_L(9 * B), b_w(B);
+  for (int64_t q = 0; q < M; ++q) {
+    const bsf::Point& P = sh.mem[q];
+    m_w[q] = P.w;
+    for (int e = 0; e < 9; ++e) {
+      const bool in = (P.mask >> e) & 1;
+      m_xi[e * M + q] = in ? xloc(P, e) : -1;
+      m_b[(2 * e) * M + q] = P.b[e][0];
+      m_b[(2 * e + 1) * M + q] = P.b[e][1];
+    }
+  }
+  for (int64_t q = 0; q < B; ++q) {
+    const bsf::Point& P = sh.bend[q];
+    b_w[q] = P.w;
+    for (int e = 0; e < 9; ++e) {
+      const bool in = (P.mask >> e) & 1;
+      b_xi[e * B + q] = in ? xloc(P, e) : -1;
+      b_L[e * B + q] = P.L[e];
+    }
+  }
+  // incidence lists (counting sort by block / by row; within a list: membrane points then bending
+  // points in creation order -> deterministic)
+  const int r0 = sh.r0, r1 = sh.r1;
+  const int64_t nrows = (int64_t)(r1 - r0) * nu, nnzb = (int64_t)sh.col_idx.size();
+  std::vector<int64_t> hp(nnzb + 1, 0), gp(nrows + 1, 0);
+  auto for_each_inc = [&](auto&& fn) {
+    for (int pass = 0; pass < 2; ++pass) {
+      const auto& L = pass ? sh.bend : sh.mem;
+      for (int64_t q = 0; q < (int64_t)L.size(); ++q) {
+        const bsf::Point& P = L[q];
+        for (int ea = 0; ea < 9; ++ea) {
+          if (!((P.mask >> ea) & 1)) continue;
+          const int ra = P.ov + ea / 3;
+          if (ra < r0 || ra >= r1) continue;
+          const int64_t row = (int64_t)(ra - r0) * nu + P.ou + ea % 3;
+          fn(pass == 1, q, ea, row, -1, -1);
+          const int32_t* c0 = sh.col_idx.data() + sh.row_ptr[row];
+          const int32_t* c1 = sh.col_idx.data() + sh.row_ptr[row + 1];
+          for (int eb = 0; eb < 9; ++eb) {
+            if (!((P.mask >> eb) & 1)) continue;
+            const int32_t b = (P.ov + eb / 3) * nu + P.ou + eb % 3;
+            const int64_t k = std::lower_bound(c0, c1, b) - sh.col_idx.data();
+            fn(pass == 1, q, ea, row, eb, k);
+          }
+        }
+      }
+    }
+  };
+  for_each_inc([&](bool, int64_t, int, int64_t row, int eb, int64_t k) {
+    if (eb < 0) ++gp[row + 1]; else ++hp[k + 1];
+  });
+  for (int64_t i = 0; i < nnzb; ++i) hp[i + 1] += hp[i];
+  for (int64_t i = 0; i < nrows; ++i) gp[i + 1] += gp[i];
+  std::vector<uint32_t> hinc(hp[nnzb]), ginc(gp[nrows]);
+  std::vector<int64_t> hf(hp.begin(), hp.end() - 1), gf(gp.begin(), gp.end() - 1);
+  for_each_inc([&](bool bend, int64_t q, int ea, int64_t row, int eb, int64_t k) {
+    if (eb < 0) ginc[gf[row]++] = bsf::pack_inc(bend, (uint32_t)q, ea, 0);
+    else hinc[hf[k]++] = bsf::pack_inc(bend, (uint32_t)q, ea, eb);
+  });
+  std::vector<uint8_t> me(sh.mem_eown), be(sh.bend_eown);
+  bsf_status s;
+  if ((s = h->upload(&t.m_xi, m_xi)) || (s = h->upload(&t.m_b, m_b)) || (s = h->upload(&t.m_w, m_w)) ||
+      (s = h->upload(&t.m_eown, me)) || (s = h->upload(&t.b_xi, b_xi)) || (s = h->upload(&t.b_L, b_L)) ||
+      (s = h->upload(&t.b_w, b_w)) || (s = h->upload(&t.b_eown, be)) || (s = h->upload(&t.h_ptr, hp)) ||
+      (s = h->upload(&t.h_inc, hinc)) || (s = h->upload(&t.g_ptr, gp)) || (s = h->upload(&t.g_inc, ginc)))
+    return s;
+  if ((s = h->alloc(&t.s_A, 21 * M)) || (s = h->alloc(&t.s_P, 6 * M)) || (s = h->alloc(&t.s_E, M + B)) ||
+      (s = h->alloc(&t.s_D, 3 * B)))
+    return s;
+  t.e_nblocks = (int)std::max<int64_t>(1, std::min<int64_t>(592, (M + B + 255) / 256));
+  if ((s = h->alloc(&t.e_part, t.e_nblocks))) return s;
+  return BSF_OK;
+}
+
+bsf_status check_cuda(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(BSF_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return BSF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bsf_last_error(void) { return g_err.c_str(); }
+
+bsf_status bsf_material_from_young(double E, double nu, double h, double shear_E, double bend_E, bsf_material* out) {
+  if (!out || !(E > 0.0) || !(h > 0.0) || !(nu > -1.0 && nu < 0.5)) return fail(BSF_E_INVALID_ARG, "invalid material");
+  const double G = shear_E >= 0.0 ? shear_E : E / (2.0 * (1.0 + nu));
+  const double Eb = bend_E >= 0.0 ? bend_E : E;
+  out->mu_st1 = 0.5 * E * h;
+  out->mu_st2 = 0.5 * E * h;
+  out->mu_sh = 0.5 * G * h;
+  out->mu_bd = Eb * h * h * h / (12.0 * (1.0 - nu * nu));
+  return BSF_OK;
+}
+
+bsf_status bsf_create(int n_u, int n_v, const double* knots_u, const double* knots_v, const double* rest_xy,
+                      const bsf_material* mat, int membrane_rule, int bending_rule, int row_begin, int row_end,
+                      int device, bsf_handle* out) {
+  if (!out || !knots_u || !knots_v || !rest_xy || !mat) return fail(BSF_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  const bool host_only = (device == -1);   // host-only handle: pattern / sizes queries, no compute
+  if (!host_only) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      return fail(BSF_E_NO_DEVICE, "no CUDA device");
+    }
+    if (device < 0 || device >= ndev) return fail(BSF_E_INVALID_ARG, "bad device ordinal");
+  }
+  auto* h = new (std::nothrow) bsf_sheet();
+  if (!h) return fail(BSF_E_OOM, "host allocation failed");
+  h->device = device;
+  std::string err;
+  const int rc = bsf::build_sheet(n_u, n_v, knots_u, knots_v, rest_xy, membrane_rule, bending_rule, row_begin,
+                                  row_end, h->sh, err);
+  if (rc) {
+    delete h;
+    return fail((bsf_status)rc, err);
+  }
+  h->mat = {mat->mu_st1, mat->mu_st2, mat->mu_sh, mat->mu_bd};
+  if (host_only) {
+    h->host_only = true;
+    *out = h;
+    return BSF_OK;
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  bsf_status s = build_generic(h);
+  if (s == BSF_OK) {
+    std::string terr;
+    const int trc = bsf::build_tiles(h->sh, h->tt, terr,
+                                     [&](size_t bytes) -> void* {
+                                       void* p = nullptr;
+                                       if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+                                       h->allocs.push_back(p);
+                                       return p;
+                                     });
+    h->tile_ok = (trc == 0);
+    if (trc < 0) s = fail(BSF_E_OOM, terr);
+  }
+  cudaSetDevice(prev);
+  if (s != BSF_OK) {
+    delete h;
+    return s;
+  }
+  *out = h;
+  return BSF_OK;
+}
+
+bsf_status bsf_destroy(bsf_handle h) {
+  delete h;
+  return BSF_OK;
+}
+
+bsf_status bsf_set_material(bsf_handle h, const bsf_material* mat) {
+  if (!h || !mat) return fail(BSF_E_INVALID_ARG, "null argument");
+  h->mat = {mat->mu_st1, mat->mu_st2, mat->mu_sh, mat->mu_bd};
+  return BSF_OK;
+}
+
+bsf_status bsf_get_sizes(bsf_handle h, int64_t* n_rows, int64_t* nnzb, int64_t* n_membrane, int64_t* n_bending) {
+  if (!h) return fail(BSF_E_INVALID_ARG, "null handle");
+  if (n_rows) *n_rows = (int64_t)(h->sh.r1 - h->sh.r0) * h->sh.n_u;
+  if (nnzb) *nnzb = (int64_t)h->sh.col_idx.size();
+  if (n_membrane) *n_membrane = (int64_t)h->sh.mem.size();
+  if (n_bending) *n_bending = (int64_t)h->sh.bend.size();
+  return BSF_OK;
+}
+
+bsf_status bsf_get_pattern(bsf_handle h, int32_t* row_ptr, int32_t* col_idx) {
+  if (!h) return fail(BSF_E_INVALID_ARG, "null handle");
+  if (row_ptr) std::memcpy(row_ptr, h->sh.row_ptr.data(), h->sh.row_ptr.size() * sizeof(int32_t));
+  if (col_idx) std::memcpy(col_idx, h->sh.col_idx.data(), h->sh.col_idx.size() * sizeof(int32_t));
+  return BSF_OK;
+}
+
+bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, double* d_grad, double* d_vals, int flags,
+                        bsf_stream stream) {
+  if (!h || !d_x) return fail(BSF_E_INVALID_ARG, "null argument");
+  if (flags & ~15) return fail(BSF_E_INVALID_ARG, "unknown flag bits");
+  if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
+  cudaError_t pe = cudaGetLastError();
+  if (pe != cudaSuccess) return fail(BSF_E_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(pe));
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  const bsf::Mat m = h->mat;
+  const int64_t nrows = (int64_t)(h->sh.r1 - h->sh.r0) * h->sh.n_u, nnzb = (int64_t)h->sh.col_idx.size();
+  auto st = static_cast<cudaStream_t>(stream);
+  int nl = 0;
+  int rc;
+  if (h->tile_ok && !(flags & BSF_GENERIC_PATH))
+    rc = bsf::tile_eval(h->tt, h->sh, d_x, m, flags, d_energy, d_grad, d_vals, st, &nl);
+  else
+    rc = bsf::generic_eval(h->gt, d_x, m, flags, nnzb, nrows, d_energy, d_grad, d_vals, st, &nl);
+  h->last_launches = nl;
+  if (prev != h->device) cudaSetDevice(prev);
+  if (rc) return check_cuda("kernel launch") == BSF_OK ? fail(BSF_E_CUDA, "launch failed") : BSF_E_CUDA;
+  return BSF_OK;
+}
+
+bsf_status bsf_eval_energy(bsf_handle h, const double* d_x, double* d_energy, int flags, bsf_stream stream) {
+  if (!d_energy) return fail(BSF_E_INVALID_ARG, "null energy");
+  return bsf_eval_all(h, d_x, d_energy, nullptr, nullptr, flags, stream);
+}
+bsf_status bsf_eval_gradient(bsf_handle h, const double* d_x, double* d_grad, int flags, bsf_stream stream) {
+  if (!d_grad) return fail(BSF_E_INVALID_ARG, "null gradient");
+  return bsf_eval_all(h, d_x, nullptr, d_grad, nullptr, flags, stream);
+}
+bsf_status bsf_assemble_hessian(bsf_handle h, const double* d_x, double* d_vals, int flags, bsf_stream stream) {
+  if (!d_vals) return fail(BSF_E_INVALID_ARG, "null values");
+  return bsf_eval_all(h, d_x, nullptr, nullptr, d_vals, flags, stream);
+}
+
+int bsf_last_launch_count(bsf_handle h) { return h ? h->last_launches : 0; }
+
+}  // extern "C"
+
+extern "C" bsf_status bsf_halo_exchange(bsf_handle h, double* d_x, void* nccl_comm, int rank, int nranks,
+                                        bsf_stream stream) {
+  (void)h; (void)d_x; (void)nccl_comm; (void)rank; (void)nranks; (void)stream;
+  return fail(BSF_E_NCCL, "halo exchange through NCCL is not built in this library version");
+}

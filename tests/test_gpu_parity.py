@@ -1,0 +1,147 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical seeded inputs.
+
+Tolerance: relative 1e-10 per the north star (tests/parity.py gives the per-quantity definition
+and floors); pattern bit-exact.  Both the fused tile path and the generic gather path are checked.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+from parity import TOL, assert_parity, rel_energy, rel_grad, rel_hess
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2506_18867_b200 as B  # noqa: E402
+
+PATHS = [0, B.GENERIC_PATH]
+
+
+def _gpu(sheet_obj, x, flags):
+    xd = torch.from_numpy(np.ascontiguousarray(x[sheet_obj.x_row_begin:sheet_obj.x_row_end])).cuda()
+    E, g, v = sheet_obj(xd, flags)
+    torch.cuda.synchronize()
+    return float(E.item()), g.cpu().numpy(), v.cpu().numpy()
+
+
+def _check(sh, x=None, mrule=0, brule=0, flags=0, r0=0, r1=None, rest=None, mu=None):
+    x = sh.x if x is None else x
+    if rest is not None:
+        sh = W.Sheet(sh.n_u, sh.n_v, sh.knots_u, sh.knots_v, rest, x, sh.E, sh.nu, sh.h)
+    mu = O.material_from_young(sh.E, sh.nu, sh.h) if mu is None else mu
+    o = O.Oracle.from_sheet(sh, mrule, brule, r0=r0, r1=r1, mu=mu)
+    Er, gr, vr = o.eval(x, flags=flags & 7)
+    s = B.Sheet.from_sheet(sh, mrule, brule, row_begin=r0, row_end=r1, material=B.Material(*mu))
+    assert np.array_equal(s.pattern()[1], o.pattern()[1]) and np.array_equal(s.pattern()[0], o.pattern()[0])
+    for path in PATHS:
+        E, g, v = _gpu(s, x, flags | path)
+        assert_parity(E, g, v, Er, gr, vr, what=f"path={path} flags={flags} rules={mrule},{brule}")
+    return s, (Er, gr, vr)
+
+
+@pytest.mark.parametrize("rules", [(0, 0), (1, 1), (2, 2)])
+@pytest.mark.parametrize("flags", [0, B.PROJECT_PSD])
+def test_c1_all_rules(rules, flags):
+    _check(W.make_c1(), mrule=rules[0], brule=rules[1], flags=flags)
+
+
+@pytest.mark.parametrize("flags", [0, B.PROJECT_PSD, B.NO_BENDING, B.NO_MEMBRANE])
+def test_c2_state(flags):
+    _check(W.make_c2(state=3), flags=flags)
+
+
+@pytest.mark.parametrize("E", [1e4, 1e6])
+def test_c3_material_sweep(E):
+    _check(W.make_c3(E=E), flags=B.PROJECT_PSD)
+
+
+def test_curved_rest_general_path():
+    n = 24
+    sh = W.make_sheet(n, 1.0, 5, n_modes=4, amp=5e-3, lam=0.2)
+    rest = W.make_curved_rest(n, n, seed=6)
+    x = np.concatenate([rest, np.zeros((n, n, 1))], -1) * 1.02 + np.random.default_rng(1).normal(0, 2e-3, (n, n, 3))
+    for flags in (0, B.PROJECT_PSD):
+        _check(sh, x=x, rest=rest, flags=flags)
+        _check(sh, x=x, rest=rest, flags=flags, mrule=2, brule=2)
+
+
+@pytest.mark.parametrize("n_u,n_v", [(5, 5), (7, 6), (37, 19), (130, 9)])
+def test_ragged_and_small(n_u, n_v):
+    ku, kv = W.open_uniform_knots(n_u), W.open_uniform_knots(n_v)
+    rest = W.greville_grid(n_u, n_v, 1.3, 0.9)
+    rng = np.random.default_rng(n_u * 100 + n_v)
+    x = np.concatenate([rest, np.zeros((n_v, n_u, 1))], -1) + rng.normal(0, 1e-2, (n_v, n_u, 3))
+    sh = W.Sheet(n_u, n_v, ku, kv, rest, x, 1e5, 0.3, 3e-4)
+    for flags in (0, B.PROJECT_PSD):
+        _check(sh, flags=flags)
+
+
+def test_g3_full_smallest():
+    n = 4
+    ku = W.open_uniform_knots(n)
+    rest = W.greville_grid(n, n, 1.0)
+    x = np.concatenate([rest, np.zeros((n, n, 1))], -1) + np.random.default_rng(0).normal(0, 1e-2, (n, n, 3))
+    _check(W.Sheet(n, n, ku, ku, rest, x, 1e5, 0.3, 3e-4), mrule=2, brule=2, flags=B.PROJECT_PSD)
+
+
+@pytest.mark.parametrize("slab", [(0, 40), (40, 41), (41, 90), (90, 128)])
+def test_slab_parity(slab):
+    _check(W.make_c2(state=1), r0=slab[0], r1=slab[1], flags=B.PROJECT_PSD)
+
+
+def test_rest_state_zero():
+    sh = W.make_sheet(20, 1.0, 0)
+    x = np.concatenate([sh.rest_xy, np.zeros((20, 20, 1))], -1)
+    s = B.Sheet.from_sheet(sh)
+    for path in PATHS:
+        E, g, v = _gpu(s, x, path)
+        assert abs(E) < 1e-20 and np.abs(g).max() < 1e-12
+
+
+def test_deterministic_and_partial_outputs():
+    sh = W.make_c2(state=2)
+    s = B.Sheet.from_sheet(sh)
+    xd = torch.from_numpy(sh.x).cuda()
+    for path in PATHS:
+        E1, g1, v1 = s(xd, B.PROJECT_PSD | path)
+        E2, g2, v2 = s(xd, B.PROJECT_PSD | path)
+        assert torch.equal(E1, E2) and torch.equal(g1, g2) and torch.equal(v1, v2)
+        E3 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        s.eval_energy(xd, E3, B.PROJECT_PSD | path)
+        g3 = torch.zeros_like(g1)
+        s.eval_gradient(xd, g3, B.PROJECT_PSD | path)
+        v3 = torch.zeros_like(v1)
+        s.assemble_hessian(xd, v3, B.PROJECT_PSD | path)
+        assert torch.equal(E1, E3) and torch.equal(g1, g3) and torch.equal(v1, v3)
+        assert s.last_launch_count() > 0
+
+
+def test_c4_full_size_sampled_rows():
+    """C4 (1024^2) in the bench's launch configuration; sampled block rows / gradient rows against
+    narrow oracle slabs, and the energy against the sum of GPU slab energies (a property that holds
+    at any size) plus one oracle slab energy."""
+    sh = W.make_c4()
+    s = B.Sheet.from_sheet(sh)
+    xd = torch.from_numpy(sh.x).cuda()
+    E, g, v = s(xd, B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    rp, ci = s.pattern()
+    g, v = g.cpu().numpy(), v.cpu().numpy()
+    mu = O.material_from_young(sh.E, sh.nu, sh.h)
+    for r0, r1 in [(0, 2), (511, 513), (1022, 1024)]:
+        o = O.Oracle.from_sheet(sh, r0=r0, r1=r1, mu=mu)
+        Er, gr, vr = o.eval(sh.x, flags=O.FLAG_PROJECT)
+        orp, oci = o.pattern()
+        a0, a1 = r0 * sh.n_u, r1 * sh.n_u
+        assert np.array_equal(ci[rp[a0]:rp[a1]], oci)
+        assert_parity(None, g[r0:r1], v[rp[a0]:rp[a1]], None, gr, vr, what=f"C4 rows {r0}:{r1}")
+        sl = B.Sheet.from_sheet(sh, row_begin=r0, row_end=r1)
+        El, _, _ = _gpu(sl, sh.x, B.PROJECT_PSD)
+        assert rel_energy(El, Er) <= TOL
+    # energy: sum over a 4-slab partition equals the full-sheet energy
+    parts = 0.0
+    for r0, r1 in [(0, 256), (256, 512), (512, 768), (768, 1024)]:
+        sl = B.Sheet.from_sheet(sh, row_begin=r0, row_end=r1)
+        parts += _gpu(sl, sh.x, B.PROJECT_PSD)[0]
+    assert rel_energy(float(E.item()), parts) <= 1e-12

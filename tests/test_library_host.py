@@ -1,0 +1,98 @@
+"""CPU-side checks of the C-ABI library (no GPU needed): it loads, exports every symbol that
+include/bsfem.h declares, validates its inputs, and its independently built pattern equals the
+oracle's bit for bit (host-only handles, device = -1)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2506_18867_b200 as B
+import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "bsfem.h")).read()
+    declared = set(re.findall(r"^\s*(?:bsf_status|int|const char\*)\s+(bsf_\w+)\s*\(", hdr, re.M))
+    assert len(declared) >= 12
+    L = B.lib()
+    for s in declared:
+        assert hasattr(L, s), s
+    assert declared == set(B.SYMBOLS)
+
+
+def test_material_map_matches_oracle():
+    """D6 material map, two independent implementations."""
+    for args in [(1e5, 0.3, 3e-4), (2e6, 0.03, 0.01), (1e4, 0.45, 1e-3)]:
+        m = B.material_from_young(*args).as_array()
+        np.testing.assert_allclose(m, O.material_from_young(*args), rtol=1e-15)
+    m = B.material_from_young(1e5, 0.3, 3e-4, shear_E=500.0, bend_E=1e3).as_array()
+    np.testing.assert_allclose(m, O.material_from_young(1e5, 0.3, 3e-4, 500.0, 1e3), rtol=1e-15)
+    with pytest.raises(B.BsfError):
+        B.material_from_young(-1, 0.3, 1e-3)
+
+
+@pytest.mark.parametrize("n_u,n_v", [(5, 5), (6, 9), (16, 16), (33, 17)])
+@pytest.mark.parametrize("rules", [(0, 0), (1, 1), (2, 2), (0, 2)])
+def test_pattern_bit_exact_vs_oracle(n_u, n_v, rules):
+    ku, kv = W.open_uniform_knots(n_u), W.open_uniform_knots(n_v)
+    rest = W.greville_grid(n_u, n_v, 1.0, 0.7)
+    mu = np.ones(4)
+    s = B.Sheet(n_u, n_v, ku, kv, rest, mu, rules[0], rules[1], device=-1)
+    o = O.Oracle(n_u, n_v, ku, kv, rest, mu, rules[0], rules[1])
+    rp, ci = s.pattern()
+    rpo, cio = o.pattern()
+    assert np.array_equal(rp, rpo) and np.array_equal(ci, cio)
+    assert (s.n_membrane, s.n_bending) == (o.n_membrane, o.n_bending)
+
+
+@pytest.mark.parametrize("slab", [(0, 3), (3, 10), (10, 20), (19, 20), (0, 20)])
+def test_slab_pattern_bit_exact(slab):
+    sh = W.make_sheet(20, 1.0, 0)
+    s = B.Sheet.from_sheet(sh, row_begin=slab[0], row_end=slab[1], device=-1)
+    o = O.Oracle.from_sheet(sh, r0=slab[0], r1=slab[1])
+    assert np.array_equal(s.pattern()[0], o.pattern()[0]) and np.array_equal(s.pattern()[1], o.pattern()[1])
+    assert s.n_rows == (slab[1] - slab[0]) * 20
+
+
+def test_pattern_c2_size_and_closed_form():
+    sh = W.make_c2()
+    s = B.Sheet.from_sheet(sh, device=-1)
+    S = 126
+    assert s.nnzb == 23 * S * S + 48 * S + 8 == 371204
+    assert (s.n_membrane, s.n_bending) == (2 * S * S + 20 * S - 14, S * S + 2 * S - 3)
+
+
+def test_create_errors():
+    n = 8
+    k = W.open_uniform_knots(n)
+    rest = W.greville_grid(n, n, 1.0)
+    bad = k.copy()
+    bad[4] += 0.5
+    with pytest.raises(B.BsfError) as e:
+        B.Sheet(n, n, bad, k, rest, np.ones(4), device=-1)
+    assert e.value.status == -2
+    k4 = W.open_uniform_knots(4)
+    with pytest.raises(B.BsfError) as e:
+        B.Sheet(4, 4, k4, k4, W.greville_grid(4, 4, 1.0), np.ones(4), device=-1)
+    assert e.value.status == -3
+    B.Sheet(4, 4, k4, k4, W.greville_grid(4, 4, 1.0), np.ones(4), 2, 2, device=-1)  # G3-FULL allows S = 2
+    flip = rest.copy()
+    flip[..., 1] *= -1
+    with pytest.raises(B.BsfError) as e:
+        B.Sheet(n, n, k, k, flip, np.ones(4), device=-1)
+    assert e.value.status == -4
+    with pytest.raises(B.BsfError) as e:
+        B.Sheet(n, n, k, k, rest, np.ones(4), row_begin=5, row_end=3, device=-1)
+    assert e.value.status == -1
+
+
+def test_host_only_handle_refuses_compute():
+    import torch
+    sh = W.make_c1()
+    s = B.Sheet.from_sheet(sh, device=-1)
+    with pytest.raises((B.BsfError, ValueError)):
+        s.eval_all(torch.zeros(s.x_shape(), dtype=torch.float64))
