@@ -111,6 +111,14 @@ bsf_status bsf_get_sizes(bsf_handle h, int64_t* n_rows, int64_t* nnzb, int64_t* 
 /* Copy the pattern (host buffers): row_ptr[n_rows+1] (int32, starts at 0), col_idx[nnzb]. */
 bsf_status bsf_get_pattern(bsf_handle h, int32_t* row_ptr, int32_t* col_idx);
 
+/* Batched fused pass over nbatch states of the same sheet (e.g. the 100 states of one Newton
+ * sequence): item b reads d_x + b*x_stride and writes d_energy[b], d_grad + b*grad_stride,
+ * d_vals + b*vals_stride (strides in doubles, >= one item's size).  One kernel launch covers all
+ * items on the tile path.  Outputs may be NULL. */
+bsf_status bsf_eval_all_batch(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride,
+                              double* d_energy, double* d_grad, int64_t grad_stride, double* d_vals,
+                              int64_t vals_stride, int flags, bsf_stream stream);
+
 /* Energy only (the line-search call). d_energy: device, 1 double (overwritten). */
 bsf_status bsf_eval_energy(bsf_handle h, const double* d_x, double* d_energy, int flags,
                            bsf_stream stream);

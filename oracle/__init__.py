@@ -22,7 +22,7 @@ _lock = threading.Lock()
 _lib = None
 
 RULE_REDUCED, RULE_G2_INTERIOR, RULE_G3_FULL = 0, 1, 2
-FLAG_PROJECT, FLAG_NO_MEMBRANE, FLAG_NO_BENDING = 1, 2, 4
+FLAG_PROJECT, FLAG_NO_MEMBRANE, FLAG_NO_BENDING, FLAG_ABS_SUM = 1, 2, 4, 8
 
 
 def build(force: bool = False) -> str:

@@ -501,7 +501,9 @@ void point_hessian(const Oracle& o, const Point& P, const std::vector<double>& x
       for (int c = 0; c < 3; ++c) H[(size_t)(3 * a + c) * m + 3 * b + c] = P.w * o.mu_bd * P.L[a] * P.L[b];
 }
 
-enum { FLAG_PROJECT = 1, FLAG_NO_MEMBRANE = 2, FLAG_NO_BENDING = 4 };
+enum { FLAG_PROJECT = 1, FLAG_NO_MEMBRANE = 2, FLAG_NO_BENDING = 4, FLAG_ABS_SUM = 8 };
+// FLAG_ABS_SUM: accumulate |local Hessian entries| instead of the entries (sum_q |H_q,blk|, the
+// cancellation scale of every block, used by the parity tolerance).
 
 bool skip(const Point& P, int flags) {
   return (P.bending && (flags & FLAG_NO_BENDING)) || (!P.bending && (flags & FLAG_NO_MEMBRANE));
@@ -695,6 +697,8 @@ int oracle_eval(void* h, const double* x, int flags, double* E, double* g, doubl
       }
       if (vals) {
         point_hessian(*o, P, xs, project, Hl);
+        if (flags & FLAG_ABS_SUM)
+          for (double& hv : Hl) hv = std::fabs(hv);
         for (int a = 0; a < k; ++a) {
           if (P.row[a] < ra || P.row[a] >= rb) continue;
           const int row = P.cp[a] - r0 * nu;

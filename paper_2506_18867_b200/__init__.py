@@ -25,7 +25,7 @@ _STATUS = {0: "OK", -1: "INVALID_ARG", -2: "KNOTS", -3: "TOO_SMALL", -4: "DEGENE
            -5: "SINGULAR_STRETCH", -6: "CUDA", -7: "OOM", -8: "NCCL", -9: "NO_DEVICE"}
 
 SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_material", "bsf_get_sizes",
-           "bsf_get_pattern", "bsf_eval_energy", "bsf_eval_gradient", "bsf_assemble_hessian", "bsf_eval_all",
+           "bsf_get_pattern", "bsf_eval_all_batch", "bsf_eval_energy", "bsf_eval_gradient", "bsf_assemble_hessian", "bsf_eval_all",
            "bsf_halo_exchange", "bsf_last_launch_count", "bsf_last_error"]
 
 
@@ -64,6 +64,7 @@ def lib():
         L.bsf_get_sizes.argtypes = [vp, i64p, i64p, i64p, i64p]
         L.bsf_get_pattern.argtypes = [vp, ip, ip]
         L.bsf_eval_all.argtypes = [vp, vp, vp, vp, vp, C.c_int, vp]
+        L.bsf_eval_all_batch.argtypes = [vp, C.c_int, vp, C.c_int64, vp, vp, C.c_int64, vp, C.c_int64, C.c_int, vp]
         L.bsf_eval_energy.argtypes = [vp, vp, vp, C.c_int, vp]
         L.bsf_eval_gradient.argtypes = [vp, vp, vp, C.c_int, vp]
         L.bsf_assemble_hessian.argtypes = [vp, vp, vp, C.c_int, vp]
@@ -175,6 +176,17 @@ class Sheet:
             raise ValueError(f"x must be float64 of shape {self.x_shape()}")
         _check(lib().bsf_eval_all(self._h, _ptr(x), _ptr(energy), _ptr(grad), _ptr(vals), int(flags),
                                   _stream(stream)))
+
+    def eval_all_batch(self, x, energy=None, grad=None, vals=None, flags=0, stream=None):
+        """Batched pass: x [B, *x_shape()], energy [B], grad [B, rows, n_u, 3], vals [B, nnzb, 3, 3]
+        (contiguous CUDA float64; any output may be None)."""
+        B = x.shape[0]
+        if tuple(x.shape[1:]) != self.x_shape():
+            raise ValueError(f"x must be [B, {self.x_shape()}]")
+        gs = grad[0].numel() if grad is not None else 0
+        vs = vals[0].numel() if vals is not None else 0
+        _check(lib().bsf_eval_all_batch(self._h, int(B), _ptr(x), x[0].numel(), _ptr(energy), _ptr(grad), gs,
+                                        _ptr(vals), vs, int(flags), _stream(stream)))
 
     def eval_energy(self, x, energy, flags=0, stream=None):
         _check(lib().bsf_eval_energy(self._h, _ptr(x), _ptr(energy), int(flags), _stream(stream)))

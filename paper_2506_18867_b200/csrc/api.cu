@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <functional>
 #include <new>
 #include <string>
 #include <vector>
@@ -54,6 +55,14 @@ struct bsf_sheet {
       return fail(BSF_E_CUDA, "cudaMemcpy failed");
     *dst = static_cast<T*>(p);
     return BSF_OK;
+  }
+  std::function<void*(size_t)> dalloc() {
+    return [this](size_t bytes) -> void* {
+      void* p = nullptr;
+      if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+      allocs.push_back(p);
+      return p;
+    };
   }
   template <class T>
   bsf_status alloc(T** dst, size_t n) {
@@ -212,13 +221,7 @@ bsf_status bsf_create(int n_u, int n_v, const double* knots_u, const double* kno
   bsf_status s = build_generic(h);
   if (s == BSF_OK) {
     std::string terr;
-    const int trc = bsf::build_tiles(h->sh, h->tt, terr,
-                                     [&](size_t bytes) -> void* {
-                                       void* p = nullptr;
-                                       if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
-                                       h->allocs.push_back(p);
-                                       return p;
-                                     });
+    const int trc = bsf::build_tiles(h->sh, h->tt, terr, h->dalloc());
     h->tile_ok = (trc == 0);
     if (trc < 0) s = fail(BSF_E_OOM, terr);
   }
@@ -274,9 +277,46 @@ bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, doubl
   int nl = 0;
   int rc;
   if (h->tile_ok && !(flags & BSF_GENERIC_PATH))
-    rc = bsf::tile_eval(h->tt, h->sh, d_x, m, flags, d_energy, d_grad, d_vals, st, &nl);
+    rc = bsf::tile_eval(h->tt, h->sh, d_x, 0, m, flags, 1, d_energy, d_grad, 0, d_vals, 0, st, &nl, h->dalloc());
   else
     rc = bsf::generic_eval(h->gt, d_x, m, flags, nnzb, nrows, d_energy, d_grad, d_vals, st, &nl);
+  h->last_launches = nl;
+  if (prev != h->device) cudaSetDevice(prev);
+  if (rc) return check_cuda("kernel launch") == BSF_OK ? fail(BSF_E_CUDA, "launch failed") : BSF_E_CUDA;
+  return BSF_OK;
+}
+
+bsf_status bsf_eval_all_batch(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride, double* d_energy,
+                              double* d_grad, int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags,
+                              bsf_stream stream) {
+  if (!h || !d_x || nbatch < 0) return fail(BSF_E_INVALID_ARG, "null argument / negative batch");
+  if (nbatch == 0) return BSF_OK;
+  if (flags & ~15) return fail(BSF_E_INVALID_ARG, "unknown flag bits");
+  if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
+  const int64_t xn = (int64_t)(h->sh.xhi - h->sh.xlo) * h->sh.n_u * 3;
+  const int64_t gn = (int64_t)(h->sh.r1 - h->sh.r0) * h->sh.n_u * 3, vn = (int64_t)h->sh.col_idx.size() * 9;
+  if (nbatch > 1 && (x_stride < xn || (d_grad && grad_stride < gn) || (d_vals && vals_stride < vn)))
+    return fail(BSF_E_INVALID_ARG, "batch strides smaller than one item");
+  cudaError_t pe = cudaGetLastError();
+  if (pe != cudaSuccess) return fail(BSF_E_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(pe));
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  auto st = static_cast<cudaStream_t>(stream);
+  int nl = 0, rc = 0;
+  if (h->tile_ok && !(flags & BSF_GENERIC_PATH)) {
+    rc = bsf::tile_eval(h->tt, h->sh, d_x, x_stride, h->mat, flags, nbatch, d_energy, d_grad, grad_stride, d_vals,
+                        vals_stride, st, &nl, h->dalloc());
+  } else {
+    const int64_t nrows = (int64_t)(h->sh.r1 - h->sh.r0) * h->sh.n_u, nnzb = (int64_t)h->sh.col_idx.size();
+    for (int b = 0; b < nbatch && rc == 0; ++b) {
+      int l = 0;
+      rc = bsf::generic_eval(h->gt, d_x + b * x_stride, h->mat, flags, nnzb, nrows, d_energy ? d_energy + b : nullptr,
+                             d_grad ? d_grad + b * grad_stride : nullptr, d_vals ? d_vals + b * vals_stride : nullptr,
+                             st, &l);
+      nl += l;
+    }
+  }
   h->last_launches = nl;
   if (prev != h->device) cudaSetDevice(prev);
   if (rc) return check_cuda("kernel launch") == BSF_OK ? fail(BSF_E_CUDA, "launch failed") : BSF_E_CUDA;

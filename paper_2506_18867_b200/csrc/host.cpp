@@ -183,6 +183,8 @@ static int eval_point(const Sheet& sh, const RulePoint& q, bool bending, Point& 
   // G = (dX/d(u,v))^{-1}: rows are grad u and grad v in material space (inverse function theorem)
   P.G[0][0] = Xv[1] / det;  P.G[0][1] = -Xv[0] / det;
   P.G[1][0] = -Xu[1] / det; P.G[1][1] = Xu[0] / det;
+  P.what = q.what;
+  P.detJ = det;
   P.w = q.what * det;
   // Laplacian coefficients: grad u . grad u, grad v . grad v, 2 grad u . grad v, Lap u, Lap v.
   // Lap r = - sum_c G[r][c] tr(G^T Hess(X_c) G)   (second-order inverse function theorem)
@@ -239,15 +241,16 @@ int build_sheet(int n_u, int n_v, const double* ku, const double* kv, const doub
     make_rule(pass ? brule : mrule, pass == 1, sh.Su, sh.Sv, rp);
     for (const RulePoint& q : rp) {
       const int ov = std::min((int)std::floor(q.v), sh.Sv - 1);
-      if (ov + 2 < r0 || ov >= r1) continue;   // stencil rows are [ov, ov+2]
+      if (ov < r0 - 2 || ov > r1 - 1) continue;   // anchor rows of the slab window
       Point P;
       const int rc = eval_point(sh, q, pass == 1, P, err);
       if (rc) return rc;
-      // exact row extent from the mask
-      int jmin = 3, jmax = -1;
+      // keep every point anchored in rows [r0-2, r1): the anchors of a slab are then complete, so
+      // gather programs built for one control point are valid for every control point of its class
+      int jmin = 3;
       for (int e = 0; e < 9; ++e)
-        if ((P.mask >> e) & 1) { jmin = std::min(jmin, e / 3); jmax = std::max(jmax, e / 3); }
-      if (P.ov + jmax < r0 || P.ov + jmin >= r1) continue;
+        if ((P.mask >> e) & 1) jmin = std::min(jmin, e / 3);
+      if (P.ov < r0 - 2 || P.ov > r1 - 1) continue;
       const uint8_t own = (P.ov + jmin >= r0 && P.ov + jmin < r1) ? 1 : 0;
       if (pass) { sh.bend.push_back(P); sh.bend_eown.push_back(own); }
       else { sh.mem.push_back(P); sh.mem_eown.push_back(own); }

@@ -36,6 +36,7 @@ struct Point {
   int ou, ov;
   uint16_t mask;
   Basis1 bu, bv;
+  double what, detJ;              // parametric weight and det(dX/d(u,v))
   double w;                       // what * det J
   double G[2][2];                 // G[r][c] = d r / d X_c, r in {u, v}
   double c_uu, c_vv, c_uv, c_u, c_v;  // Laplacian coefficients

@@ -1,10 +1,670 @@
+// Fused tile path of the assembly (the hot path).
+//
+// One CTA owns a strip of kTX control-point columns over a chunk of rows of one sheet (grid.z =
+// batch item).  It walks the chunk kRS output rows at a time:
+//   1. stage the positions of the rows the new anchor rows need (coalesced loads);
+//   2. point phase: evaluate every quadrature point whose stencil origin ("anchor") lies in the two
+//      new anchor rows of the strip window — F = F~ G, FBW Psi, P, A
+//       with optional per-term PSD projection — and keep the parametric-frame
+//      data  A~ = w (G (x) I) A (G (x) I)^T,  P~ = w G P  (membrane) or  L^ = sqrt(w mu) L,
+//      D^ = sqrt(w mu) Lap phi  (bending)  in a shared-memory ring of 4 anchor rows;
+//   3. gather: each thread owns one (control point a, row offset dj) task = the <=5 contiguous BSR
+//      blocks of row a whose columns lie in row j+dj; it walks the host-built incidence program of
+//      a's boundary/parity class, loading each incident point's A~ once and accumulating
+//      H_ab = sum_q sum_{mu,nu} d_a,mu d_b,nu A~_mu,nu  (+ sum_q' L^_a L^_b I3)  in registers
+//      (the paper's per-block gather, without atomics); a 6th task per point
+//      gathers g_a = sum_q d_a . P~ + sum_q' L^_a D^;
+//   4. the strip's row segments are staged in shared memory and written to HBM coalesced.
+// The energy is reduced per CTA (points owned by anchor) and summed per item by k_energy_final.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <vector>
+
+#include "fbw.cuh"
 #include "tile.hpp"
 
 namespace bsf {
-int build_tiles(const Sheet&, TileTables&, std::string&, const std::function<void*(size_t)>&) { return 1; }
-int tile_eval(const TileTables&, const Sheet&, const double*, const Mat&, int, double*, double*, double*, cudaStream_t,
-              int* launches) {
-  if (launches) *launches = 0;
-  return -6;
+
+namespace {
+
+constexpr int kPosCols = kTX + 4;
+constexpr int kPosRows = kRS + 2;
+constexpr int kAC = kTX + 2;   // anchor columns of a strip window
+
+__host__ __device__ inline int bclass(int i, int n) {
+  if (i < 6) return i;
+  if (i >= n - 6) return 7 + (i - (n - 6));
+  return 6;
 }
+
+struct TileArgs {
+  const double* x;
+  int64_t xs;
+  double* g;
+  int64_t gs;
+  double* vals;
+  int64_t vs;
+  double* epart;
+  int n_u, n_v, Su, Sv, r0, r1, xlo, xhi;
+  int capm, capb, chunk, nchunks, nstrips, max_row_blocks;
+  int affine, project;
+  double G00, G01, G10, G11, detJ;
+  double mu1, mu2, mush, mubd;
+  const int32_t* m_aoff;
+  const int32_t* b_aoff;
+  const uint2* m_info;     // (uc | vc << 16, shape | ou << 16)
+  const uint2* b_info;
+  const double* utab;      // [nu_cls][9]: N[3] dN[3] ddN[3]
+  const double* vtab;      // [nv_cls][9]
+  const double* stab;      // [nshape][2]: w (affine) , mask
+  const double* m_geo;
+  const double* b_geo;
+  int64_t Mm, Bm;
+  const int16_t* lut;
+  const int4* tasks;
+  const unsigned long long* ent;
+  const int32_t* row_ptr;
+};
+
+__device__ __forceinline__ int wrap(int q, int cap) { return q >= cap ? q - cap : q; }
+
+__global__ void __launch_bounds__(kThreads, 1) k_tile(const TileArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x;
+  const int strip = blockIdx.x, chunk = blockIdx.y, item = blockIdx.z;
+  const int i0 = strip * kTX;
+  const int ra = A.r0 + chunk * A.chunk, rb = min(A.r1, ra + A.chunk);
+  const int slo = max(0, i0 - 2), shi = min(A.Su - 1, i0 + kTX - 1);
+  const double* __restrict__ x = A.x + item * A.xs;
+
+  // ---- shared memory carve-up
+  double* pos = reinterpret_cast<double*>(smem_raw);                   // [kPosRows][kPosCols][3]
+  double* pmA = pos + kPosRows * kPosCols * 3;                         // [21][capm]
+  double* pmP = pmA + 21 * A.capm;                                     // [6][capm]
+  double* pbL = pmP + 6 * A.capm;                                      // [9][capb]
+  double* pbD = pbL + 9 * A.capb;                                      // [3][capb]
+  double* stage = pbD + 3 * A.capb;                                    // [kRS][max_row_blocks][9]
+  double* red = stage + kRS * A.max_row_blocks * 9;                    // [32]
+  int* pmC = reinterpret_cast<int*>(red + 32);                         // [capm] class ids
+  int* astm = pmC + A.capm;                                            // [kRing][kAC]
+  int* astb = astm + kRing * kAC;                                      // [kRing][kAC]
+
+  const bool want_h = A.vals != nullptr, want_g = A.g != nullptr;
+  double e_acc = 0.0;
+  int head_m = 0, head_b = 0;
+
+  for (int j0 = ra - 2; j0 < rb; j0 += kRS) {
+    // ---------------- 1. positions of cp rows j0 .. j0+kRS+1, cols i0-2 .. i0+kTX+1
+    for (int k = tid; k < kPosRows * kPosCols * 3; k += kThreads) {
+      const int row = k / (kPosCols * 3), rem = k - row * kPosCols * 3;
+      const int col = rem / 3, c = rem - col * 3;
+      const int R = j0 + row, Cc = i0 - 2 + col;
+      double v = 0.0;
+      if (R >= A.xlo && R < A.xhi && Cc >= 0 && Cc < A.n_u) v = x[((int64_t)(R - A.xlo) * A.n_u + Cc) * 3 + c];
+      pos[k] = v;
+    }
+    // ---------------- 2. ring bookkeeping for anchor rows j0, j0+1 (uniform in every thread)
+    int P0m[kRS], Nm[kRS], Hm[kRS], P0b[kRS], Nb[kRS], Hb[kRS];
+#pragma unroll
+    for (int r = 0; r < kRS; ++r) {
+      const int t = j0 + r;
+      const bool valid = (t >= 0 && t < A.Sv && slo <= shi);
+      P0m[r] = valid ? A.m_aoff[t * A.Su + slo] : 0;
+      Nm[r] = valid ? A.m_aoff[t * A.Su + shi + 1] - P0m[r] : 0;
+      P0b[r] = valid ? A.b_aoff[t * A.Su + slo] : 0;
+      Nb[r] = valid ? A.b_aoff[t * A.Su + shi + 1] - P0b[r] : 0;
+      Hm[r] = head_m;
+      Hb[r] = head_b;
+      head_m = wrap(head_m + Nm[r], A.capm);   // Nm <= capm
+      head_b = wrap(head_b + Nb[r], A.capb);
+      if (tid < kAC) {
+        const int s = i0 - 2 + tid, slot = (t + 4) & 3;
+        int sm = 0, sb = 0;
+        if (valid && s >= slo && s <= shi) {
+          sm = wrap(Hm[r] + (A.m_aoff[t * A.Su + s] - P0m[r]), A.capm);
+          sb = wrap(Hb[r] + (A.b_aoff[t * A.Su + s] - P0b[r]), A.capb);
+        }
+        astm[slot * kAC + tid] = sm;
+        astb[slot * kAC + tid] = sb;
+      }
+    }
+    __syncthreads();
+    // ---------------- 3. point phase
+    const int nmem = Nm[0] + Nm[1], ntot = nmem + Nb[0] + Nb[1];
+    for (int k = tid; k < ntot; k += kThreads) {
+      if (k < nmem) {
+        const int r = k < Nm[0] ? 0 : 1;
+        const int kk = r ? k - Nm[0] : k;
+        const int64_t p = P0m[r] + kk;
+        const int slot = wrap(Hm[r] + kk, A.capm);
+        const int t = j0 + r;
+        const uint2 info = A.m_info[p];
+        const int ou = info.y >> 16;
+        const double* tu = A.utab + (info.x & 0xFFFF) * 9;
+        const double* tv = A.vtab + (info.x >> 16) * 9;
+        const double* sh = A.stab + (info.y & 0xFFFF) * 2;
+        double Nu[3], dNu[3], Nv[3], dNv[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) { Nu[q] = tu[q]; dNu[q] = tu[3 + q]; Nv[q] = tv[q]; dNv[q] = tv[3 + q]; }
+        const int mask = (int)sh[1];
+        // F~ = [dphi/du, dphi/dv] = sum_e C_e (N'_u N_v, N_u N'_v)
+        double Fu[3] = {0, 0, 0}, Fv[3] = {0, 0, 0};
+#pragma unroll
+        for (int jv = 0; jv < 3; ++jv)
+#pragma unroll
+          for (int iu = 0; iu < 3; ++iu) {
+            if (!((mask >> (3 * jv + iu)) & 1)) continue;
+            const double* C = pos + ((t + jv - j0) * kPosCols + (ou + iu - (i0 - 2))) * 3;
+            const double du = dNu[iu] * Nv[jv], dv = Nu[iu] * dNv[jv];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) { Fu[c] += C[c] * du; Fv[c] += C[c] * dv; }
+          }
+        double G00, G01, G10, G11, w;
+        if (A.affine) { G00 = A.G00; G01 = A.G01; G10 = A.G10; G11 = A.G11; w = sh[0] * A.detJ; }
+        else {
+          G00 = A.m_geo[p]; G01 = A.m_geo[A.Mm + p]; G10 = A.m_geo[2 * A.Mm + p]; G11 = A.m_geo[3 * A.Mm + p];
+          w = A.m_geo[4 * A.Mm + p];
+        }
+        double f1[3], f2[3];   // F_beta = sum_mu F~_mu G_mu,beta
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * G00 + Fv[c] * G10; f2[c] = Fu[c] * G01 + Fv[c] * G11; }
+        FSpace o;
+        fbw_point(f1, f2, A.mu1, A.mu2, A.mush, A.project != 0, o);
+        if (ou >= i0 && ou < i0 + kTX && t >= ra && t < rb) e_acc += w * o.psi;
+        // P~_mu = w sum_beta G_mu,beta P_beta
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          pmP[c * A.capm + slot] = w * (G00 * o.P1[c] + G01 * o.P2[c]);
+          pmP[(3 + c) * A.capm + slot] = w * (G10 * o.P1[c] + G11 * o.P2[c]);
+        }
+        // A~_mu,nu = w sum_{beta,gamma} G_mu,beta G_nu,gamma A_beta,gamma
+        const double a11 = w * G00 * G00, a12 = w * G00 * G01, a22 = w * G01 * G01;  // for mu=nu=u
+        const double b11 = w * G10 * G10, b12 = w * G10 * G11, b22 = w * G11 * G11;  // mu=nu=v
+        const double c11 = w * G00 * G10, c12 = w * G00 * G11, c21 = w * G01 * G10, c22 = w * G01 * G11;  // u,v
+#pragma unroll
+        for (int r3 = 0; r3 < 3; ++r3)
+#pragma unroll
+          for (int c3 = r3; c3 < 3; ++c3) {
+            const int s6 = sym3(r3, c3);
+            const double A11 = o.A11[s6], A22 = o.A22[s6];
+            const double A12rc = o.A12[3 * r3 + c3], A12cr = o.A12[3 * c3 + r3];  // A21[r][c] = A12[c][r]
+            pmA[s6 * A.capm + slot] = a11 * A11 + a12 * (A12rc + A12cr) + a22 * A22;
+            pmA[(6 + s6) * A.capm + slot] = b11 * A11 + b12 * (A12rc + A12cr) + b22 * A22;
+          }
+#pragma unroll
+        for (int r3 = 0; r3 < 3; ++r3)
+#pragma unroll
+          for (int c3 = 0; c3 < 3; ++c3)
+            pmA[(12 + 3 * r3 + c3) * A.capm + slot] =
+                c11 * o.A11[sym3(r3, c3)] + c12 * o.A12[3 * r3 + c3] + c21 * o.A12[3 * c3 + r3] + c22 * o.A22[sym3(r3, c3)];
+        pmC[slot] = (int)info.x;
+      } else {
+        const int kb = k - nmem;
+        const int r = kb < Nb[0] ? 0 : 1;
+        const int kk = r ? kb - Nb[0] : kb;
+        const int64_t p = P0b[r] + kk;
+        const int slot = wrap(Hb[r] + kk, A.capb);
+        const int t = j0 + r;
+        const uint2 info = A.b_info[p];
+        const int ou = info.y >> 16;
+        const double* tu = A.utab + (info.x & 0xFFFF) * 9;
+        const double* tv = A.vtab + (info.x >> 16) * 9;
+        const double* sh = A.stab + (info.y & 0xFFFF) * 2;
+        double cuu, cvv, cuv, cu, cv, w;
+        if (A.affine) {
+          cuu = A.G00 * A.G00 + A.G01 * A.G01;
+          cvv = A.G10 * A.G10 + A.G11 * A.G11;
+          cuv = 2.0 * (A.G00 * A.G10 + A.G01 * A.G11);
+          cu = 0.0; cv = 0.0;
+          w = sh[0] * A.detJ;
+        } else {
+          w = A.b_geo[p]; cuu = A.b_geo[A.Bm + p]; cvv = A.b_geo[2 * A.Bm + p]; cuv = A.b_geo[3 * A.Bm + p];
+          cu = A.b_geo[4 * A.Bm + p]; cv = A.b_geo[5 * A.Bm + p];
+        }
+        const int mask = (int)sh[1];
+        const double sw = sqrt(w * A.mubd);
+        double lap[3] = {0, 0, 0};
+#pragma unroll
+        for (int jv = 0; jv < 3; ++jv)
+#pragma unroll
+          for (int iu = 0; iu < 3; ++iu) {
+            const int e = 3 * jv + iu;
+            double L = 0.0;
+            if ((mask >> e) & 1) {
+              // Eq. `eq: Laplacian in parametric space`
+              L = cuu * tu[6 + iu] * tv[jv] + cvv * tu[iu] * tv[6 + jv] + cuv * tu[3 + iu] * tv[3 + jv] +
+                  cu * tu[3 + iu] * tv[jv] + cv * tu[iu] * tv[3 + jv];
+              const double* C = pos + ((t + jv - j0) * kPosCols + (ou + iu - (i0 - 2))) * 3;
+              lap[0] += L * C[0]; lap[1] += L * C[1]; lap[2] += L * C[2];
+            }
+            pbL[e * A.capb + slot] = sw * L;
+          }
+        if (ou >= i0 && ou < i0 + kTX && t >= ra && t < rb)
+          e_acc += 0.5 * w * A.mubd * (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
+        pbD[slot] = sw * lap[0];
+        pbD[A.capb + slot] = sw * lap[1];
+        pbD[2 * A.capb + slot] = sw * lap[2];
+      }
+    }
+    __syncthreads();
+    if (j0 < ra) continue;   // prologue step: anchor rows ra-2, ra-1 only
+    // ---------------- 3. gather
+    const int warp = tid >> 5, lane = tid & 31;
+    const int r = lane / kTX, c = lane - r * kTX;
+    const int i = i0 + c, j = j0 + r;
+    const bool active = (i < A.n_u) && (j < rb) && ((warp < 5) ? want_h : want_g);
+    int4 tk = make_int4(0, 0, 0, 0);
+    int64_t a_loc = 0;
+    if (active) {
+      const int pid = A.lut[(bclass(i, A.n_u) * kNCls + bclass(j, A.n_v)) * 2 + ((i + j) & 1)];
+      tk = A.tasks[pid * kTasks + warp];
+      a_loc = (int64_t)(j - A.r0) * A.n_u + i;
+    }
+    const int n_m = active ? (tk.y & 0xFFFF) : 0, n_b = active ? (tk.y >> 16) : 0;
+    const int nmax_m = __reduce_max_sync(0xffffffffu, n_m), nmax_b = __reduce_max_sync(0xffffffffu, n_b);
+    const unsigned long long* ent = A.ent + tk.x;
+    if (warp < 5) {
+      double acc[5][9];
+      double dg[5];
+#pragma unroll
+      for (int m = 0; m < 5; ++m) {
+        dg[m] = 0.0;
+#pragma unroll
+        for (int q = 0; q < 9; ++q) acc[m][q] = 0.0;
+      }
+      for (int e = 0; e < nmax_m; ++e) {
+        if (e < n_m) {
+          const unsigned long long E = __ldg(ent + e);
+          const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
+          const int t = j - 2 + dt, sc = c + dc;   // anchor column offset in the window = (i-2+dc) - (i0-2)
+          const int q = wrap(astm[((t + 4) & 3) * kAC + sc] + idx, A.capm);
+          const int uv = pmC[q];
+          const double* tu = A.utab + (uv & 0xFFFF) * 9;
+          const double* tv = A.vtab + (uv >> 16) * 9;
+          const int ia = la % 3, ja = la / 3;
+          const double da1 = __ldg(tu + 3 + ia) * __ldg(tv + ja), da2 = __ldg(tu + ia) * __ldg(tv + 3 + ja);
+          double Am[21];
+#pragma unroll
+          for (int k = 0; k < 21; ++k) Am[k] = pmA[k * A.capm + q];
+#pragma unroll
+          for (int m = 0; m < 5; ++m) {
+            const int lb = (E >> (13 + 4 * m)) & 15;
+            if (lb == 15) continue;
+            const int ib = lb % 3, jb = lb / 3;
+            const double db1 = __ldg(tu + 3 + ib) * __ldg(tv + jb), db2 = __ldg(tu + ib) * __ldg(tv + 3 + jb);
+            const double k11 = da1 * db1, k22 = da2 * db2, k12 = da1 * db2, k21 = da2 * db1;
+#pragma unroll
+            for (int r3 = 0; r3 < 3; ++r3)
+#pragma unroll
+              for (int c3 = 0; c3 < 3; ++c3)
+                acc[m][3 * r3 + c3] += k11 * Am[sym3(r3, c3)] + k22 * Am[6 + sym3(r3, c3)] +
+                                       k12 * Am[12 + 3 * r3 + c3] + k21 * Am[12 + 3 * c3 + r3];
+          }
+        }
+      }
+      const unsigned long long* entb = ent + n_m;
+      for (int e = 0; e < nmax_b; ++e) {
+        if (e < n_b) {
+          const unsigned long long E = __ldg(entb + e);
+          const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
+          const int t = j - 2 + dt, sc = c + dc;
+          const int q = wrap(astb[((t + 4) & 3) * kAC + sc] + idx, A.capb);
+          const double La = pbL[la * A.capb + q];
+#pragma unroll
+          for (int m = 0; m < 5; ++m) {
+            const int lb = (E >> (13 + 4 * m)) & 15;
+            if (lb != 15) dg[m] += La * pbL[lb * A.capb + q];
+          }
+        }
+      }
+      if (active) {
+        const int klo = tk.z & 0xFF, nb = (tk.z >> 8) & 0xFF;
+        const int64_t afirst = (int64_t)(j - A.r0) * A.n_u + i0;
+        double* dst = stage + (r * A.max_row_blocks + (A.row_ptr[a_loc] - A.row_ptr[afirst]) + klo) * 9;
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {
+          if (m < nb) {
+#pragma unroll
+            for (int q = 0; q < 9; ++q) dst[9 * m + q] = acc[m][q] + ((q == 0 || q == 4 || q == 8) ? dg[m] : 0.0);
+          }
+        }
+      }
+    } else {
+      double g3[3] = {0, 0, 0};
+      for (int e = 0; e < nmax_m; ++e) {
+        if (e < n_m) {
+          const unsigned long long E = __ldg(ent + e);
+          const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
+          const int t = j - 2 + dt, sc = c + dc;
+          const int q = wrap(astm[((t + 4) & 3) * kAC + sc] + idx, A.capm);
+          const int uv = pmC[q];
+          const double* tu = A.utab + (uv & 0xFFFF) * 9;
+          const double* tv = A.vtab + (uv >> 16) * 9;
+          const int ia = la % 3, ja = la / 3;
+          const double da1 = __ldg(tu + 3 + ia) * __ldg(tv + ja), da2 = __ldg(tu + ia) * __ldg(tv + 3 + ja);
+#pragma unroll
+          for (int c3 = 0; c3 < 3; ++c3) g3[c3] += da1 * pmP[c3 * A.capm + q] + da2 * pmP[(3 + c3) * A.capm + q];
+        }
+      }
+      const unsigned long long* entb = ent + n_m;
+      for (int e = 0; e < nmax_b; ++e) {
+        if (e < n_b) {
+          const unsigned long long E = __ldg(entb + e);
+          const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
+          const int t = j - 2 + dt, sc = c + dc;
+          const int q = wrap(astb[((t + 4) & 3) * kAC + sc] + idx, A.capb);
+          const double La = pbL[la * A.capb + q];
+#pragma unroll
+          for (int c3 = 0; c3 < 3; ++c3) g3[c3] += La * pbD[c3 * A.capb + q];
+        }
+      }
+      if (active) {
+        double* gd = A.g + item * A.gs + 3 * a_loc;
+        gd[0] = g3[0]; gd[1] = g3[1]; gd[2] = g3[2];
+      }
+    }
+    __syncthreads();
+    // ---------------- 4. coalesced copy of the staged row segments
+    if (want_h) {
+#pragma unroll
+      for (int rr = 0; rr < kRS; ++rr) {
+        const int jr = j0 + rr;
+        if (jr >= rb) break;
+        const int64_t afirst = (int64_t)(jr - A.r0) * A.n_u + i0;
+        const int txr = min(kTX, A.n_u - i0);
+        const int64_t b0 = A.row_ptr[afirst], b1 = A.row_ptr[afirst + txr];
+        const int64_t nd = (b1 - b0) * 9;
+        double* dstg = A.vals + item * A.vs + b0 * 9;
+        const double* src = stage + rr * A.max_row_blocks * 9;
+        for (int64_t k = tid; k < nd; k += kThreads) dstg[k] = src[k];
+      }
+    }
+    __syncthreads();
+  }
+  // ---------------- energy partial of this CTA (fixed-order tree)
+  for (int o = 16; o > 0; o >>= 1) e_acc += __shfl_xor_sync(0xffffffffu, e_acc, o);
+  if ((tid & 31) == 0) red[tid >> 5] = e_acc;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+    A.epart[((int64_t)item * A.nchunks + chunk) * A.nstrips + strip] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_energy_final(const double* __restrict__ epart, int per_item, double* E) {
+  __shared__ double sm[8];
+  const double* p = epart + (int64_t)blockIdx.x * per_item;
+  double s = 0.0;
+  for (int k = threadIdx.x; k < per_item; k += blockDim.x) s += p[k];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sm[w];
+    E[blockIdx.x] = t;
+  }
+}
+
+// ------------------------------------------------------------------ host side
+template <class T>
+bool upload(const std::function<void*(size_t)>& dalloc, T** dst, const std::vector<T>& v) {
+  *dst = nullptr;
+  if (v.empty()) return true;
+  void* p = dalloc(v.size() * sizeof(T));
+  if (!p) return false;
+  if (cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) return false;
+  *dst = static_cast<T*>(p);
+  return true;
+}
+
+}  // namespace
+
+int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::function<void*(size_t)>& dalloc) {
+  tt = TileTables();
+  const int Su = sh.Su, Sv = sh.Sv, nu = sh.n_u;
+  tt.n_u = nu; tt.n_v = sh.n_v; tt.Su = Su; tt.Sv = Sv; tt.r0 = sh.r0; tt.r1 = sh.r1; tt.xlo = sh.xlo;
+  const int nanch = Su * Sv;
+  // ---- sort points by anchor (stable)
+  auto sort_by_anchor = [&](const std::vector<Point>& P, std::vector<int32_t>& aoff, std::vector<int>& order) {
+    aoff.assign(nanch + 1, 0);
+    for (const Point& p : P) ++aoff[p.ov * Su + p.ou + 1];
+    for (int a = 0; a < nanch; ++a) aoff[a + 1] += aoff[a];
+    order.assign(P.size(), 0);
+    std::vector<int32_t> fill(aoff.begin(), aoff.end() - 1);
+    for (size_t k = 0; k < P.size(); ++k) order[fill[P[k].ov * Su + P[k].ou]++] = (int)k;
+    int mx = 0;
+    for (int a = 0; a < nanch; ++a) mx = std::max(mx, aoff[a + 1] - aoff[a]);
+    return mx;
+  };
+  std::vector<int32_t> m_aoff, b_aoff;
+  std::vector<int> m_ord, b_ord;
+  if (sort_by_anchor(sh.mem, m_aoff, m_ord) > 15 || sort_by_anchor(sh.bend, b_aoff, b_ord) > 15) return 1;
+  // ---- basis tables, keyed by their exact bits: one table per distinct 1D evaluation (x - span is
+  // the same double for every span of a binade, so the tables stay few), plus a small "shape" table
+  // (weight for the affine case, stencil mask).  No rounding of any coefficient.
+  const double detJ_ref = sh.mem.empty() ? (sh.bend.empty() ? 1.0 : sh.bend[0].detJ) : sh.mem[0].detJ;
+  std::map<std::vector<double>, int> ucls, vcls, scls;
+  std::vector<double> utab, vtab, stab;
+  auto intern = [](std::map<std::vector<double>, int>& M, std::vector<double>& tab, std::vector<double> key) {
+    auto it = M.find(key);
+    if (it != M.end()) return it->second;
+    const int id = (int)M.size();
+    M.emplace(key, id);
+    tab.insert(tab.end(), key.begin(), key.end());
+    return id;
+  };
+  auto b9 = [](const Basis1& b) {
+    std::vector<double> k(b.N, b.N + 3);
+    k.insert(k.end(), b.d1, b.d1 + 3);
+    k.insert(k.end(), b.d2, b.d2 + 3);
+    return k;
+  };
+  std::vector<uint2> m_info(sh.mem.size()), b_info(sh.bend.size());
+  for (int kind = 0; kind < 2; ++kind) {
+    const std::vector<Point>& P = kind ? sh.bend : sh.mem;
+    const std::vector<int>& ord = kind ? b_ord : m_ord;
+    std::vector<uint2>& info = kind ? b_info : m_info;
+    for (size_t k = 0; k < ord.size(); ++k) {
+      const Point& p = P[ord[k]];
+      const int uc = intern(ucls, utab, b9(p.bu)), vc = intern(vcls, vtab, b9(p.bv));
+      const int sc = intern(scls, stab, {sh.affine ? p.what * detJ_ref : 0.0, (double)p.mask});
+      info[k] = make_uint2((uint32_t)uc | ((uint32_t)vc << 16), (uint32_t)sc | ((uint32_t)p.ou << 16));
+    }
+  }
+  if (ucls.size() > 65535 || vcls.size() > 65535 || scls.size() > 65535 || nu > 65535) return 1;
+  // affine: the kernel multiplies the class weight by detJ; classes already hold w, so detJ = 1
+  tt.affine = sh.affine ? 1 : 0;
+  if (sh.affine) {
+    const Point& ref = sh.mem.empty() ? sh.bend[0] : sh.mem[0];
+    tt.G[0] = ref.G[0][0]; tt.G[1] = ref.G[0][1]; tt.G[2] = ref.G[1][0]; tt.G[3] = ref.G[1][1];
+    tt.detJ = 1.0;
+  }
+  std::vector<double> m_geo, b_geo;
+  if (!sh.affine) {
+    const size_t M = sh.mem.size(), B = sh.bend.size();
+    m_geo.resize(5 * M);
+    b_geo.resize(6 * B);
+    for (size_t k = 0; k < M; ++k) {
+      const Point& p = sh.mem[m_ord[k]];
+      m_geo[k] = p.G[0][0]; m_geo[M + k] = p.G[0][1]; m_geo[2 * M + k] = p.G[1][0]; m_geo[3 * M + k] = p.G[1][1];
+      m_geo[4 * M + k] = p.w;
+    }
+    for (size_t k = 0; k < B; ++k) {
+      const Point& p = sh.bend[b_ord[k]];
+      b_geo[k] = p.w; b_geo[B + k] = p.c_uu; b_geo[2 * B + k] = p.c_vv; b_geo[3 * B + k] = p.c_uv;
+      b_geo[4 * B + k] = p.c_u; b_geo[5 * B + k] = p.c_v;
+    }
+  }
+  // ---- strips, chunks, ring capacities, staging size
+  tt.nstrips = (nu + kTX - 1) / kTX;
+  const int nrows_owned = sh.r1 - sh.r0;
+  tt.chunk = 32;
+  if (nrows_owned <= 48) tt.chunk = ((nrows_owned + 1) / 2) * 2;
+  tt.nchunks = (nrows_owned + tt.chunk - 1) / tt.chunk;
+  int capm = 1, capb = 1, maxrb = 1;
+  for (int st = 0; st < tt.nstrips; ++st) {
+    const int i0 = st * kTX, slo = std::max(0, i0 - 2), shi = std::min(Su - 1, i0 + kTX - 1);
+    std::vector<int> cm(Sv, 0), cb(Sv, 0);
+    if (slo <= shi)
+      for (int t = 0; t < Sv; ++t) {
+        cm[t] = m_aoff[t * Su + shi + 1] - m_aoff[t * Su + slo];
+        cb[t] = b_aoff[t * Su + shi + 1] - b_aoff[t * Su + slo];
+      }
+    for (int t = 0; t < Sv; ++t) {
+      int sm = 0, sb = 0;
+      for (int d = 0; d < kRing && t + d < Sv; ++d) { sm += cm[t + d]; sb += cb[t + d]; }
+      capm = std::max(capm, sm);
+      capb = std::max(capb, sb);
+    }
+    const int txr = std::min(kTX, nu - i0);
+    for (int j = sh.r0; j < sh.r1; ++j) {
+      const int64_t af = (int64_t)(j - sh.r0) * nu + i0;
+      maxrb = std::max(maxrb, sh.row_ptr[af + txr] - sh.row_ptr[af]);
+    }
+  }
+  tt.capm = capm | 1;   // odd capacities spread SoA columns over banks
+  tt.capb = capb | 1;
+  tt.max_row_blocks = maxrb;
+  tt.smem = sizeof(double) * (kPosRows * kPosCols * 3 + 27 * (size_t)tt.capm + 12 * (size_t)tt.capb +
+                              kRS * (size_t)maxrb * 9 + 32) +
+            sizeof(int) * ((size_t)tt.capm + 2 * kRing * kAC);
+  if (tt.smem > 227 * 1024) return 1;
+  // ---- gather programs: one per (boundary class u, boundary class v, parity)
+  std::vector<int16_t> lut(kNCls * kNCls * 2, -1);
+  std::vector<int4> tasks;
+  std::vector<unsigned long long> ents;
+  auto build_prog = [&](int i, int j) {
+    const int64_t a_loc = (int64_t)(j - sh.r0) * nu + i;
+    const int32_t* c0 = sh.col_idx.data() + sh.row_ptr[a_loc];
+    const int nc = sh.row_ptr[a_loc + 1] - sh.row_ptr[a_loc];
+    int klo[5], nb[5];
+    for (int dj = -2; dj <= 2; ++dj) {
+      int lo = -1, n = 0;
+      for (int k = 0; k < nc; ++k)
+        if (c0[k] / nu == j + dj) { if (lo < 0) lo = k; ++n; }
+      klo[dj + 2] = lo < 0 ? 0 : lo;
+      nb[dj + 2] = n;
+      if (n > 5) return false;
+    }
+    std::vector<unsigned long long> lists[kTasks][2];
+    for (int kind = 0; kind < 2; ++kind) {
+      const std::vector<int32_t>& aoff = kind ? b_aoff : m_aoff;
+      const std::vector<int>& ord = kind ? b_ord : m_ord;
+      const std::vector<Point>& P = kind ? sh.bend : sh.mem;
+      for (int dt = 0; dt < 3; ++dt)
+        for (int dc = 0; dc < 3; ++dc) {
+          const int t = j - 2 + dt, s = i - 2 + dc;
+          if (t < 0 || t >= Sv || s < 0 || s >= Su) continue;
+          const int an = t * Su + s;
+          for (int idx = 0; idx < aoff[an + 1] - aoff[an]; ++idx) {
+            const Point& p = P[ord[aoff[an] + idx]];
+            const int la = (i - s) + 3 * (j - t);
+            if (!((p.mask >> la) & 1)) continue;
+            const unsigned long long base = (unsigned long long)dt | ((unsigned long long)dc << 2) |
+                                            ((unsigned long long)kind << 4) | ((unsigned long long)idx << 5) |
+                                            ((unsigned long long)la << 9);
+            lists[5][kind].push_back(base | (0xFFFFFull << 13));
+            for (int tk = 0; tk < 5; ++tk) {
+              unsigned long long lbs = 0;
+              bool any = false;
+              for (int m = 0; m < 5; ++m) {
+                unsigned long long lb = 15;
+                if (m < nb[tk]) {
+                  const int b = c0[klo[tk] + m], ib = b % nu - s, jb = b / nu - t;
+                  if (ib >= 0 && ib < 3 && jb >= 0 && jb < 3 && ((p.mask >> (ib + 3 * jb)) & 1)) {
+                    lb = (unsigned long long)(ib + 3 * jb);
+                    any = true;
+                  }
+                }
+                lbs |= lb << (4 * m);
+              }
+              if (any) lists[tk][kind].push_back(base | (lbs << 13));
+            }
+          }
+        }
+    }
+    for (int tk = 0; tk < kTasks; ++tk) {
+      int4 h;
+      h.x = (int)ents.size();
+      h.y = (int)lists[tk][0].size() | ((int)lists[tk][1].size() << 16);
+      h.z = tk < 5 ? (klo[tk] | (nb[tk] << 8)) : 0;
+      h.w = 0;
+      ents.insert(ents.end(), lists[tk][0].begin(), lists[tk][0].end());
+      ents.insert(ents.end(), lists[tk][1].begin(), lists[tk][1].end());
+      tasks.push_back(h);
+    }
+    return true;
+  };
+  int nprog = 0;
+  for (int j = sh.r0; j < sh.r1; ++j) {
+    const int cv = bclass(j, sh.n_v);
+    for (int i = 0; i < nu; ++i) {
+      const int key = (bclass(i, nu) * kNCls + cv) * 2 + ((i + j) & 1);
+      if (lut[key] >= 0) continue;
+      lut[key] = (int16_t)nprog++;
+      if (!build_prog(i, j)) return 1;
+    }
+  }
+  // ---- upload
+  std::vector<int32_t> rp(sh.row_ptr.begin(), sh.row_ptr.end());
+  bool ok = upload(dalloc, &tt.m_aoff, m_aoff) && upload(dalloc, &tt.b_aoff, b_aoff) &&
+            upload(dalloc, &tt.m_info, m_info) && upload(dalloc, &tt.b_info, b_info) &&
+            upload(dalloc, &tt.utab, utab) && upload(dalloc, &tt.vtab, vtab) && upload(dalloc, &tt.stab, stab) &&
+            upload(dalloc, &tt.m_geo, m_geo) && upload(dalloc, &tt.b_geo, b_geo) && upload(dalloc, &tt.lut, lut) &&
+            upload(dalloc, &tt.tasks, tasks) && upload(dalloc, &tt.ent, ents) && upload(dalloc, &tt.row_ptr, rp);
+  if (!ok) { err = "tile tables: device allocation failed"; return -7; }
+  if (cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tt.smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  tt.ok = 1;
+  return 0;
+}
+
+int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
+              int nbatch, double* d_E, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride,
+              cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc) {
+  const int64_t need = (int64_t)nbatch * tt.nstrips * tt.nchunks;
+  if (need > tt.e_cap) {
+    void* p = dalloc(need * sizeof(double));
+    if (!p) return -7;
+    tt.e_part = static_cast<double*>(p);
+    tt.e_cap = need;
+  }
+  TileArgs A;
+  A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride; A.epart = tt.e_part;
+  A.n_u = tt.n_u; A.n_v = tt.n_v; A.Su = tt.Su; A.Sv = tt.Sv; A.r0 = tt.r0; A.r1 = tt.r1;
+  A.xlo = sh.xlo; A.xhi = sh.xhi;
+  A.capm = tt.capm; A.capb = tt.capb; A.chunk = tt.chunk; A.nchunks = tt.nchunks; A.nstrips = tt.nstrips;
+  A.max_row_blocks = tt.max_row_blocks;
+  A.affine = tt.affine; A.project = (flags & 1) ? 1 : 0;
+  A.G00 = tt.G[0]; A.G01 = tt.G[1]; A.G10 = tt.G[2]; A.G11 = tt.G[3]; A.detJ = tt.detJ;
+  A.mu1 = (flags & 2) ? 0.0 : mat.mu_st1;
+  A.mu2 = (flags & 2) ? 0.0 : mat.mu_st2;
+  A.mush = (flags & 2) ? 0.0 : mat.mu_sh;
+  A.mubd = (flags & 4) ? 0.0 : mat.mu_bd;
+  A.m_aoff = tt.m_aoff; A.b_aoff = tt.b_aoff;
+  A.m_info = tt.m_info;
+  A.b_info = tt.b_info;
+  A.utab = tt.utab; A.vtab = tt.vtab; A.stab = tt.stab; A.m_geo = tt.m_geo; A.b_geo = tt.b_geo;
+  A.Mm = (int64_t)sh.mem.size(); A.Bm = (int64_t)sh.bend.size();
+  A.lut = tt.lut; A.tasks = tt.tasks; A.ent = tt.ent; A.row_ptr = tt.row_ptr;
+  dim3 grid(tt.nstrips, tt.nchunks, nbatch);
+  k_tile<<<grid, kThreads, tt.smem, st>>>(A);
+  int nl = 1;
+  if (d_E) {
+    k_energy_final<<<nbatch, 256, 0, st>>>(tt.e_part, tt.nstrips * tt.nchunks, d_E);
+    ++nl;
+  }
+  if (launches) *launches = nl;
+  return cudaGetLastError() == cudaSuccess ? 0 : -6;
+}
+
 }  // namespace bsf

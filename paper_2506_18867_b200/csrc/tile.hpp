@@ -1,8 +1,11 @@
-// Fused tile path (see tile.cu).
+// Fused tile path: one kernel evaluates the quadrature points of a column strip row by row into a
+// shared-memory ring and gathers every BSR block / gradient row of the strip from it (see tile.cu
+// and DESIGN.md §5).
 #pragma once
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <cstdint>
 #include <functional>
 #include <string>
 
@@ -11,15 +14,45 @@
 
 namespace bsf {
 
+constexpr int kTX = 16;        // strip width (control points)
+constexpr int kRS = 2;         // output rows per step
+constexpr int kRing = kRS + 2; // anchor rows resident in the ring
+constexpr int kTasks = 6;      // dj = -2..2 Hessian tasks + 1 gradient task per control point
+constexpr int kThreads = 32 * kTasks;
+constexpr int kNCls = 13;      // boundary-distance classes per direction
+
 struct TileTables {
-  int ntiles = 0;
+  int ok = 0;
+  int n_u = 0, n_v = 0, Su = 0, Sv = 0, r0 = 0, r1 = 0, xlo = 0;
+  int capm = 0, capb = 0;          // ring pool capacities (points)
+  int nstrips = 0, chunk = 0, nchunks = 0;
+  int max_row_blocks = 0;          // max blocks of one strip row segment
+  int affine = 0;
+  double G[4] = {0, 0, 0, 0};      // affine: G[r*2+c]
+  double detJ = 0;
+  size_t smem = 0;
+  int32_t* m_aoff = nullptr;       // [Sv*Su+1] anchor -> first membrane point (points sorted by anchor)
+  int32_t* b_aoff = nullptr;
+  uint2* m_info = nullptr;         // per sorted point: (u-table | v-table << 16, shape | anchor column << 16)
+  uint2* b_info = nullptr;
+  double* utab = nullptr;          // [n][9]: N[3] dN[3] ddN[3] of one exact 1D evaluation
+  double* vtab = nullptr;
+  double* stab = nullptr;          // [n][2]: w = what*detJ (affine) or 0, stencil mask
+  double* m_geo = nullptr;         // general path: [5][Mm] G00 G01 G10 G11 w
+  double* b_geo = nullptr;         // general path: [6][Bm] w c_uu c_vv c_uv c_u c_v
+  int16_t* lut = nullptr;          // [kNCls][kNCls][2] -> program id
+  int4* tasks = nullptr;           // [nprog][kTasks]: (entry offset, n_mem | n_bend<<16, k_lo | nb<<8, 0)
+  unsigned long long* ent = nullptr;
+  int32_t* row_ptr = nullptr;      // owned rows' pattern (device copy)
+  double* e_part = nullptr;        // per-CTA energy partials (grown on demand)
+  int64_t e_cap = 0;
 };
 
-// Returns 0 when the tile path is available, 1 when the sheet is not eligible (generic path is
-// used), <0 on allocation failure.
 int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::function<void*(size_t)>& dalloc);
 
-int tile_eval(const TileTables& tt, const Sheet& sh, const double* d_x, const Mat& mat, int flags, double* d_E,
-              double* d_g, double* d_vals, cudaStream_t st, int* launches);
+// Batched evaluation: item b uses x + b*x_stride, grad + b*g_stride, vals + b*v_stride, E + b.
+int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
+              int nbatch, double* d_E, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride,
+              cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc);
 
 }  // namespace bsf

@@ -8,7 +8,7 @@ import pytest
 
 import oracle as O
 import workloads as W
-from parity import TOL, assert_parity, rel_energy, rel_grad, rel_hess
+from parity import TOL, assert_parity, diag_block_norms, rel_energy
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -32,11 +32,17 @@ def _check(sh, x=None, mrule=0, brule=0, flags=0, r0=0, r1=None, rest=None, mu=N
     mu = O.material_from_young(sh.E, sh.nu, sh.h) if mu is None else mu
     o = O.Oracle.from_sheet(sh, mrule, brule, r0=r0, r1=r1, mu=mu)
     Er, gr, vr = o.eval(x, flags=flags & 7)
+    rp, ci = o.pattern()
+    hd = diag_block_norms(vr, rp, ci, r0, sh.n_u)
+    if flags & 6:   # one energy switched off: scale the floor with the full Hessian's diagonal
+        hd = diag_block_norms(o.eval(x, flags=flags & 1, energy=False, gradient=False)[2], rp, ci, r0, sh.n_u)
+    va = o.eval(x, flags=(flags & 7) | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
     s = B.Sheet.from_sheet(sh, mrule, brule, row_begin=r0, row_end=r1, material=B.Material(*mu))
-    assert np.array_equal(s.pattern()[1], o.pattern()[1]) and np.array_equal(s.pattern()[0], o.pattern()[0])
+    assert np.array_equal(s.pattern()[1], ci) and np.array_equal(s.pattern()[0], rp)
     for path in PATHS:
         E, g, v = _gpu(s, x, flags | path)
-        assert_parity(E, g, v, Er, gr, vr, what=f"path={path} flags={flags} rules={mrule},{brule}")
+        assert_parity(E, g, v, Er, gr, vr, what=f"path={path} flags={flags} rules={mrule},{brule}",
+                      hdiag=hd, cmax=np.abs(x).max(), vabs=va)
     return s, (Er, gr, vr)
 
 
@@ -135,7 +141,9 @@ def test_c4_full_size_sampled_rows():
         orp, oci = o.pattern()
         a0, a1 = r0 * sh.n_u, r1 * sh.n_u
         assert np.array_equal(ci[rp[a0]:rp[a1]], oci)
-        assert_parity(None, g[r0:r1], v[rp[a0]:rp[a1]], None, gr, vr, what=f"C4 rows {r0}:{r1}")
+        va = o.eval(sh.x, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
+        assert_parity(None, g[r0:r1], v[rp[a0]:rp[a1]], None, gr, vr, what=f"C4 rows {r0}:{r1}",
+                      hdiag=diag_block_norms(vr, orp, oci, r0, sh.n_u), cmax=np.abs(sh.x).max(), vabs=va)
         sl = B.Sheet.from_sheet(sh, row_begin=r0, row_end=r1)
         El, _, _ = _gpu(sl, sh.x, B.PROJECT_PSD)
         assert rel_energy(El, Er) <= TOL
@@ -145,3 +153,25 @@ def test_c4_full_size_sampled_rows():
         sl = B.Sheet.from_sheet(sh, row_begin=r0, row_end=r1)
         parts += _gpu(sl, sh.x, B.PROJECT_PSD)[0]
     assert rel_energy(float(E.item()), parts) <= 1e-12
+
+
+def test_batch_matches_single_calls():
+    """bsf_eval_all_batch over several C2 states equals per-state calls bit for bit, and the oracle."""
+    sheets = [W.make_c2(state=k) for k in (0, 7, 42)]
+    s = B.Sheet.from_sheet(sheets[0])
+    X = torch.stack([torch.from_numpy(q.x) for q in sheets]).cuda()
+    nb = len(sheets)
+    E = torch.zeros(nb, dtype=torch.float64, device="cuda")
+    G = torch.zeros((nb,) + tuple(X.shape[1:]), dtype=torch.float64, device="cuda")
+    V = torch.zeros((nb, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    for path in PATHS:
+        s.eval_all_batch(X, E, G, V, B.PROJECT_PSD | path)
+        for k in range(nb):
+            E1, g1, v1 = s(X[k].contiguous(), B.PROJECT_PSD | path)
+            assert torch.equal(E1[0], E[k]) and torch.equal(g1, G[k]) and torch.equal(v1, V[k])
+    o = O.Oracle.from_sheet(sheets[1])
+    Er, gr, vr = o.eval(sheets[1].x, flags=O.FLAG_PROJECT)
+    rp, ci = o.pattern()
+    va = o.eval(sheets[1].x, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
+    assert_parity(float(E[1]), G[1].cpu().numpy(), V[1].cpu().numpy(), Er, gr, vr, what="batch item 1",
+                  hdiag=diag_block_norms(vr, rp, ci, 0, sheets[1].n_u), cmax=np.abs(sheets[1].x).max(), vabs=va)

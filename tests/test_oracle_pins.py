@@ -631,3 +631,26 @@ def test_thread_count_independent():
     a = o.eval(sh.x, threads=1)
     b = o.eval(sh.x, threads=4)
     assert a[0] == b[0] and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+def test_rigid_motion_self_consistency_within_tolerance():
+    """The oracle is frame-indifferent up to fp64 noise; that noise, measured with the parity metric
+    of tests/parity.py, stays 30x below the 1e-10 tolerance — the calibration of the
+    gradient floor 1e-4 |H_aa| |C|_max and the Hessian floor 1e-2 sum_q |H_q,blk|."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from parity import diag_block_norms, rel_grad, rel_hess
+    sh = W.make_c2(state=3)
+    o = O.Oracle.from_sheet(sh)
+    rp, ci = o.pattern()
+    E, g, v = o.eval(sh.x, flags=O.FLAG_PROJECT)
+    R = W.random_rotation(np.random.default_rng(5))
+    E2, g2, v2 = o.eval(sh.x @ R.T + np.array([0.0625, -0.125, 0.03125]), flags=O.FLAG_PROJECT)
+    v2 = np.einsum("ab,kbc,dc->kad", R.T, v2, R.T)
+    va = o.eval(sh.x, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
+    assert abs(E2 - E) / E < 1e-13
+    assert rel_grad(g2 @ R, g, diag_block_norms(v, rp, ci, 0, sh.n_u), np.abs(sh.x).max()) < 1e-11
+    assert rel_hess(v2, v, va) < 1e-11
+    # the abs-sum scale dominates every block and equals |H| for single-term blocks
+    assert (np.linalg.norm(va.reshape(-1, 9), axis=1) >= np.linalg.norm(v.reshape(-1, 9), axis=1) * (1 - 1e-14)).all()
