@@ -140,7 +140,7 @@ void make_rule(int kind, bool bending, int Su, int Sv, std::vector<RulePoint>& o
 }
 
 // ------------------------------------------------------------------ per-point coefficients
-static uint16_t stencil_mask(bool bending, bool ku, bool kv) {
+uint16_t stencil_mask(bool bending, bool ku, bool kv) {
   // value/first-derivative entries: {0,1} on a knot line, {0,1,2} inside a span;
   // second-derivative entries (right limit): always {0,1,2}.
   const int vu = ku ? 0x3 : 0x7, vv = kv ? 0x3 : 0x7, du = 0x7, dv = 0x7;
@@ -233,6 +233,7 @@ int build_sheet(int n_u, int n_v, const double* ku, const double* kv, const doub
   if (r0 < 0 || r1 > n_v || r0 >= r1) { err = "invalid owned row range"; return -1; }
   sh.n_u = n_u; sh.n_v = n_v; sh.Su = n_u - 2; sh.Sv = n_v - 2;
   sh.r0 = r0; sh.r1 = r1;
+  sh.mrule = mrule; sh.brule = brule;
   sh.xlo = std::max(0, r0 - 2); sh.xhi = std::min(n_v, r1 + 2);
   sh.rest.assign(rest_xy, rest_xy + (size_t)2 * n_u * n_v);
   sh.mem.clear(); sh.bend.clear(); sh.mem_eown.clear(); sh.bend_eown.clear();

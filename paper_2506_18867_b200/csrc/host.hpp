@@ -59,6 +59,7 @@ struct Sheet {
   std::vector<uint8_t> mem_eown, bend_eown;  // 1 if the point's energy is counted by this slab
   std::vector<int32_t> row_ptr, col_idx;     // owned block rows
   bool affine = false;                        // G, det J constant and no second-order terms
+  int mrule = 0, brule = 0;
 };
 
 // Build the sheet: validates knots (status -2), sizes (-3), rest geometry (-4); returns 0 or the
@@ -68,5 +69,8 @@ int build_sheet(int n_u, int n_v, const double* ku, const double* kv, const doub
 
 // Index helpers
 inline int win_entry(int iu, int jv) { return 3 * jv + iu; }
+
+// Structural stencil mask of a point (bit 3*jv+iu of its 3x3 window; Q10, D4).
+uint16_t stencil_mask(bool bending, bool knot_u, bool knot_v);
 
 }  // namespace bsf

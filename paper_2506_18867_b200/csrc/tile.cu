@@ -51,7 +51,7 @@ struct TileArgs {
   int64_t vs;
   double* epart;
   int n_u, n_v, Su, Sv, r0, r1, xlo, xhi;
-  int capm, capb, chunk, nchunks, nstrips, max_row_blocks;
+  int capm, capb, nchunks_total, nstrips, chunk_base;
   int affine, project;
   double G00, G01, G10, G11, detJ;
   double mu1, mu2, mush, mubd;
@@ -69,29 +69,47 @@ struct TileArgs {
   const int4* tasks;
   const unsigned long long* ent;
   const int32_t* row_ptr;
+  const int2* chunks;      // (ra, rb) per chunk of this launch
 };
+
+// point records in shared memory (array of structures, odd strides -> conflict-free 8-byte access)
+constexpr int kMS = 45;    // membrane: [0,21) A~  [21,39) d_e (e*2 + mu)  [39,45) P~
+constexpr int kBS = 13;    // bending:  [0,9) L^_e  [9,12) D^  [12] pad
 
 __device__ __forceinline__ int wrap(int q, int cap) { return q >= cap ? q - cap : q; }
 
-__global__ void __launch_bounds__(kThreads, 1) k_tile(const TileArgs A) {
+// Warp-cooperative store of one 3x3 block per lane (9 lanes per 72-byte block); pos < 0 skips.
+__device__ __forceinline__ void warp_store_block(double* wb, const double (&blk)[9], bool transpose, int pos,
+                                                 double* vals, int lane) {
+#pragma unroll
+  for (int q = 0; q < 9; ++q) wb[lane * 9 + q] = transpose ? blk[3 * (q % 3) + q / 3] : blk[q];
+  __syncwarp();
+#pragma unroll
+  for (int rr = 0; rr < 9; ++rr) {
+    const int f = rr * 32 + lane, owner = f / 9, el = f - owner * 9;
+    const int po = __shfl_sync(0xffffffffu, pos, owner);
+    if (po >= 0) vals[(int64_t)po * 9 + el] = wb[f];
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
-  const int strip = blockIdx.x, chunk = blockIdx.y, item = blockIdx.z;
+  const int strip = blockIdx.x, chunk = A.chunk_base + blockIdx.y, item = blockIdx.z;
   const int i0 = strip * kTX;
-  const int ra = A.r0 + chunk * A.chunk, rb = min(A.r1, ra + A.chunk);
+  const int2 chr = A.chunks[blockIdx.y];
+  const int ra = chr.x, rb = chr.y;
   const int slo = max(0, i0 - 2), shi = min(A.Su - 1, i0 + kTX - 1);
   const double* __restrict__ x = A.x + item * A.xs;
 
   // ---- shared memory carve-up
   double* pos = reinterpret_cast<double*>(smem_raw);                   // [kPosRows][kPosCols][3]
-  double* pmA = pos + kPosRows * kPosCols * 3;                         // [21][capm]
-  double* pmP = pmA + 21 * A.capm;                                     // [6][capm]
-  double* pbL = pmP + 6 * A.capm;                                      // [9][capb]
-  double* pbD = pbL + 9 * A.capb;                                      // [3][capb]
-  double* stage = pbD + 3 * A.capb;                                    // [kRS][max_row_blocks][9]
-  double* red = stage + kRS * A.max_row_blocks * 9;                    // [32]
-  int* pmC = reinterpret_cast<int*>(red + 32);                         // [capm] class ids
-  int* astm = pmC + A.capm;                                            // [kRing][kAC]
+  double* pm = pos + kPosRows * kPosCols * 3;                          // [capm][kMS]
+  double* pb = pm + (int64_t)kMS * A.capm;                             // [capb][kBS]
+  double* wbuf = pb + (int64_t)kBS * A.capb;                           // [kThreads/32][288]
+  double* red = wbuf + (kThreads / 32) * 288;                          // [32]
+  int* astm = reinterpret_cast<int*>(red + 32);                        // [kRing][kAC]
   int* astb = astm + kRing * kAC;                                      // [kRing][kAC]
 
   const bool want_h = A.vals != nullptr, want_g = A.g != nullptr;
@@ -141,7 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile(const TileArgs A) {
         const int r = k < Nm[0] ? 0 : 1;
         const int kk = r ? k - Nm[0] : k;
         const int64_t p = P0m[r] + kk;
-        const int slot = wrap(Hm[r] + kk, A.capm);
+        double* rec = pm + (int64_t)kMS * wrap(Hm[r] + kk, A.capm);
         const int t = j0 + r;
         const uint2 info = A.m_info[p];
         const int ou = info.y >> 16;
@@ -152,17 +170,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile(const TileArgs A) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) { Nu[q] = tu[q]; dNu[q] = tu[3 + q]; Nv[q] = tv[q]; dNv[q] = tv[3 + q]; }
         const int mask = (int)sh[1];
-        // F~ = [dphi/du, dphi/dv] = sum_e C_e (N'_u N_v, N_u N'_v)
+        // d_e = (dN/du, dN/dv) of window entry e (zero outside the structural stencil);
+        // F~ = [dphi/du, dphi/dv] = sum_e C_e d_e^T
         double Fu[3] = {0, 0, 0}, Fv[3] = {0, 0, 0};
 #pragma unroll
         for (int jv = 0; jv < 3; ++jv)
 #pragma unroll
           for (int iu = 0; iu < 3; ++iu) {
-            if (!((mask >> (3 * jv + iu)) & 1)) continue;
+            const int e = 3 * jv + iu;
+            const bool in = (mask >> e) & 1;
+            const double du = in ? dNu[iu] * Nv[jv] : 0.0, dv = in ? Nu[iu] * dNv[jv] : 0.0;
+            rec[21 + 2 * e] = du;
+            rec[22 + 2 * e] = dv;
             const double* C = pos + ((t + jv - j0) * kPosCols + (ou + iu - (i0 - 2))) * 3;
-            const double du = dNu[iu] * Nv[jv], dv = Nu[iu] * dNv[jv];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) { Fu[c] += C[c] * du; Fv[c] += C[c] * dv; }
+            for (int c = 0; c < 3; ++c) { Fu[c] = fma(C[c], du, Fu[c]); Fv[c] = fma(C[c], dv, Fv[c]); }
           }
         double G00, G01, G10, G11, w;
         if (A.affine) { G00 = A.G00; G01 = A.G01; G10 = A.G10; G11 = A.G11; w = sh[0] * A.detJ; }
@@ -179,8 +201,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile(const TileArgs A) {
         // P~_mu = w sum_beta G_mu,beta P_beta
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          pmP[c * A.capm + slot] = w * (G00 * o.P1[c] + G01 * o.P2[c]);
-          pmP[(3 + c) * A.capm + slot] = w * (G10 * o.P1[c] + G11 * o.P2[c]);
+          rec[39 + c] = w * (G00 * o.P1[c] + G01 * o.P2[c]);
+          rec[42 + c] = w * (G10 * o.P1[c] + G11 * o.P2[c]);
         }
         // A~_mu,nu = w sum_{beta,gamma} G_mu,beta G_nu,gamma A_beta,gamma
         const double a11 = w * G00 * G00, a12 = w * G00 * G01, a22 = w * G01 * G01;  // for mu=nu=u
@@ -193,22 +215,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile(const TileArgs A) {
             const int s6 = sym3(r3, c3);
             const double A11 = o.A11[s6], A22 = o.A22[s6];
             const double A12rc = o.A12[3 * r3 + c3], A12cr = o.A12[3 * c3 + r3];  // A21[r][c] = A12[c][r]
-            pmA[s6 * A.capm + slot] = a11 * A11 + a12 * (A12rc + A12cr) + a22 * A22;
-            pmA[(6 + s6) * A.capm + slot] = b11 * A11 + b12 * (A12rc + A12cr) + b22 * A22;
+            rec[s6] = a11 * A11 + a12 * (A12rc + A12cr) + a22 * A22;
+            rec[6 + s6] = b11 * A11 + b12 * (A12rc + A12cr) + b22 * A22;
           }
 #pragma unroll
         for (int r3 = 0; r3 < 3; ++r3)
 #pragma unroll
           for (int c3 = 0; c3 < 3; ++c3)
-            pmA[(12 + 3 * r3 + c3) * A.capm + slot] =
+            rec[12 + 3 * r3 + c3] =
                 c11 * o.A11[sym3(r3, c3)] + c12 * o.A12[3 * r3 + c3] + c21 * o.A12[3 * c3 + r3] + c22 * o.A22[sym3(r3, c3)];
-        pmC[slot] = (int)info.x;
       } else {
         const int kb = k - nmem;
         const int r = kb < Nb[0] ? 0 : 1;
         const int kk = r ? kb - Nb[0] : kb;
         const int64_t p = P0b[r] + kk;
-        const int slot = wrap(Hb[r] + kk, A.capb);
+        double* rec = pb + (int64_t)kBS * wrap(Hb[r] + kk, A.capb);
         const int t = j0 + r;
         const uint2 info = A.b_info[p];
         const int ou = info.y >> 16;
@@ -242,146 +263,155 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile(const TileArgs A) {
               const double* C = pos + ((t + jv - j0) * kPosCols + (ou + iu - (i0 - 2))) * 3;
               lap[0] += L * C[0]; lap[1] += L * C[1]; lap[2] += L * C[2];
             }
-            pbL[e * A.capb + slot] = sw * L;
+            rec[e] = sw * L;
           }
         if (ou >= i0 && ou < i0 + kTX && t >= ra && t < rb)
           e_acc += 0.5 * w * A.mubd * (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
-        pbD[slot] = sw * lap[0];
-        pbD[A.capb + slot] = sw * lap[1];
-        pbD[2 * A.capb + slot] = sw * lap[2];
+        rec[9] = sw * lap[0];
+        rec[10] = sw * lap[1];
+        rec[11] = sw * lap[2];
       }
     }
     __syncthreads();
-    if (j0 < ra) continue;   // prologue step: anchor rows ra-2, ra-1 only
-    // ---------------- 3. gather
-    const int warp = tid >> 5, lane = tid & 31;
-    const int r = lane / kTX, c = lane - r * kTX;
-    const int i = i0 + c, j = j0 + r;
-    const bool active = (i < A.n_u) && (j < rb) && ((warp < 5) ? want_h : want_g);
-    int4 tk = make_int4(0, 0, 0, 0);
-    int64_t a_loc = 0;
-    if (active) {
-      const int pid = A.lut[(bclass(i, A.n_u) * kNCls + bclass(j, A.n_v)) * 2 + ((i + j) & 1)];
-      tk = A.tasks[pid * kTasks + warp];
-      a_loc = (int64_t)(j - A.r0) * A.n_u + i;
-    }
-    const int n_m = active ? (tk.y & 0xFFFF) : 0, n_b = active ? (tk.y >> 16) : 0;
-    const int nmax_m = __reduce_max_sync(0xffffffffu, n_m), nmax_b = __reduce_max_sync(0xffffffffu, n_b);
-    const unsigned long long* ent = A.ent + tk.x;
-    if (warp < 5) {
-      double acc[5][9];
-      double dg[5];
-#pragma unroll
-      for (int m = 0; m < 5; ++m) {
-        dg[m] = 0.0;
-#pragma unroll
-        for (int q = 0; q < 9; ++q) acc[m][q] = 0.0;
-      }
-      for (int e = 0; e < nmax_m; ++e) {
-        if (e < n_m) {
-          const unsigned long long E = __ldg(ent + e);
-          const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
-          const int t = j - 2 + dt, sc = c + dc;   // anchor column offset in the window = (i-2+dc) - (i0-2)
-          const int q = wrap(astm[((t + 4) & 3) * kAC + sc] + idx, A.capm);
-          const int uv = pmC[q];
-          const double* tu = A.utab + (uv & 0xFFFF) * 9;
-          const double* tv = A.vtab + (uv >> 16) * 9;
-          const int ia = la % 3, ja = la / 3;
-          const double da1 = __ldg(tu + 3 + ia) * __ldg(tv + ja), da2 = __ldg(tu + ia) * __ldg(tv + 3 + ja);
-          double Am[21];
-#pragma unroll
-          for (int k = 0; k < 21; ++k) Am[k] = pmA[k * A.capm + q];
-#pragma unroll
-          for (int m = 0; m < 5; ++m) {
-            const int lb = (E >> (13 + 4 * m)) & 15;
-            if (lb == 15) continue;
-            const int ib = lb % 3, jb = lb / 3;
-            const double db1 = __ldg(tu + 3 + ib) * __ldg(tv + jb), db2 = __ldg(tu + ib) * __ldg(tv + 3 + jb);
-            const double k11 = da1 * db1, k22 = da2 * db2, k12 = da1 * db2, k21 = da2 * db1;
-#pragma unroll
-            for (int r3 = 0; r3 < 3; ++r3)
-#pragma unroll
-              for (int c3 = 0; c3 < 3; ++c3)
-                acc[m][3 * r3 + c3] += k11 * Am[sym3(r3, c3)] + k22 * Am[6 + sym3(r3, c3)] +
-                                       k12 * Am[12 + 3 * r3 + c3] + k21 * Am[12 + 3 * c3 + r3];
-          }
-        }
-      }
-      const unsigned long long* entb = ent + n_m;
-      for (int e = 0; e < nmax_b; ++e) {
-        if (e < n_b) {
-          const unsigned long long E = __ldg(entb + e);
-          const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
-          const int t = j - 2 + dt, sc = c + dc;
-          const int q = wrap(astb[((t + 4) & 3) * kAC + sc] + idx, A.capb);
-          const double La = pbL[la * A.capb + q];
-#pragma unroll
-          for (int m = 0; m < 5; ++m) {
-            const int lb = (E >> (13 + 4 * m)) & 15;
-            if (lb != 15) dg[m] += La * pbL[lb * A.capb + q];
-          }
-        }
-      }
+    // prologue step (anchor rows ra-2, ra-1): no output, except the two halo rows above a slab whose
+    // forward pairs reach into the first owned rows (transpose-only)
+    const bool halo_step = (j0 < ra);
+    if (halo_step && !(ra == A.r0 && A.r0 > 0)) continue;
+    // ---------------- 4. gather: symmetric forward tasks (b after a), both H_ab and H_ab^T written
+    {
+      const int warp = tid >> 5, lane = tid & 31;
+      const int r = lane / kTX, c = lane - r * kTX;
+      const int i = i0 + c, j = j0 + r;
+      const bool owned_row = (j >= A.r0);
+      bool active = (i < A.n_u) && (j < rb) && (j >= 0);
+      if (warp == 0 || warp == 5) active = active && owned_row;        // T0 / gradient: owned rows only
+      active = active && ((warp < 5) ? want_h : want_g);
+      const int anchor_min = max(0, ra - 2);
+      int4 h0 = make_int4(0, 0, 0, 0), h1 = make_int4(0, 0, 0, 0);
+      int a_loc = 0;
       if (active) {
-        const int klo = tk.z & 0xFF, nb = (tk.z >> 8) & 0xFF;
-        const int64_t afirst = (int64_t)(j - A.r0) * A.n_u + i0;
-        double* dst = stage + (r * A.max_row_blocks + (A.row_ptr[a_loc] - A.row_ptr[afirst]) + klo) * 9;
+        const int pid = A.lut[(bclass(i, A.n_u) * kNCls + bclass(j, A.n_v)) * 2 + ((i + j) & 1)];
+        h0 = A.tasks[(pid * kTasks + warp) * 2];
+        h1 = A.tasks[(pid * kTasks + warp) * 2 + 1];
+        a_loc = (j - A.r0) * A.n_u + i;
+      }
+      const int n_m = active ? (h0.y & 0xFFFF) : 0, n_b = active ? (h0.y >> 16) : 0;
+      const int nmax_m = __reduce_max_sync(0xffffffffu, n_m), nmax_b = __reduce_max_sync(0xffffffffu, n_b);
+      const unsigned long long* ent = A.ent + h0.x;
+      if (warp < 5) {
+        double acc0[9], acc1[9], acc2[9];
+        double dg0 = 0.0, dg1 = 0.0, dg2 = 0.0;
 #pragma unroll
-        for (int m = 0; m < 5; ++m) {
-          if (m < nb) {
+        for (int q = 0; q < 9; ++q) { acc0[q] = 0.0; acc1[q] = 0.0; acc2[q] = 0.0; }
+        for (int e = 0; e < nmax_m; ++e) {
+          if (e < n_m) {
+            const unsigned long long E = __ldg(ent + e);
+            const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
+            const int t = j - 2 + dt;
+            if (t >= anchor_min) {
+              const double* rec = pm + kMS * wrap(astm[((t + 4) & 3) * kAC + c + dc] + idx, A.capm);
+              const double da1 = rec[21 + 2 * la], da2 = rec[22 + 2 * la];
+              double Am[21];
 #pragma unroll
-            for (int q = 0; q < 9; ++q) dst[9 * m + q] = acc[m][q] + ((q == 0 || q == 4 || q == 8) ? dg[m] : 0.0);
+              for (int k = 0; k < 21; ++k) Am[k] = rec[k];
+              const int lb0 = (E >> 13) & 15, lb1 = (E >> 17) & 15, lb2 = (E >> 21) & 15;
+              // contributions to the task's <= 3 blocks; a missing block (lb == 15) reads entry 0 and
+              // gets zero coefficients (branch-free body)
+#define BSF_BLOCK(ACC, LB)                                                                          \
+  {                                                                                                 \
+    const bool ok = (LB) != 15;                                                                     \
+    const int l2 = ok ? (LB) : 0;                                                                   \
+    const double db1 = ok ? rec[21 + 2 * l2] : 0.0, db2 = ok ? rec[22 + 2 * l2] : 0.0;              \
+    const double k11 = da1 * db1, k22 = da2 * db2, k12 = da1 * db2, k21 = da2 * db1;                \
+    _Pragma("unroll") for (int r3 = 0; r3 < 3; ++r3)                                                \
+    _Pragma("unroll") for (int c3 = 0; c3 < 3; ++c3) {                                              \
+      double v = ACC[3 * r3 + c3];                                                                  \
+      v = fma(k11, Am[sym3(r3, c3)], v);                                                            \
+      v = fma(k22, Am[6 + sym3(r3, c3)], v);                                                        \
+      v = fma(k12, Am[12 + 3 * r3 + c3], v);                                                        \
+      v = fma(k21, Am[12 + 3 * c3 + r3], v);                                                        \
+      ACC[3 * r3 + c3] = v;                                                                         \
+    }                                                                                               \
+  }
+              BSF_BLOCK(acc0, lb0)
+              BSF_BLOCK(acc1, lb1)
+              BSF_BLOCK(acc2, lb2)
+#undef BSF_BLOCK
+            }
           }
         }
-      }
-    } else {
-      double g3[3] = {0, 0, 0};
-      for (int e = 0; e < nmax_m; ++e) {
-        if (e < n_m) {
-          const unsigned long long E = __ldg(ent + e);
-          const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
-          const int t = j - 2 + dt, sc = c + dc;
-          const int q = wrap(astm[((t + 4) & 3) * kAC + sc] + idx, A.capm);
-          const int uv = pmC[q];
-          const double* tu = A.utab + (uv & 0xFFFF) * 9;
-          const double* tv = A.vtab + (uv >> 16) * 9;
-          const int ia = la % 3, ja = la / 3;
-          const double da1 = __ldg(tu + 3 + ia) * __ldg(tv + ja), da2 = __ldg(tu + ia) * __ldg(tv + 3 + ja);
-#pragma unroll
-          for (int c3 = 0; c3 < 3; ++c3) g3[c3] += da1 * pmP[c3 * A.capm + q] + da2 * pmP[(3 + c3) * A.capm + q];
+        const unsigned long long* entb = ent + n_m;
+        for (int e = 0; e < nmax_b; ++e) {
+          if (e < n_b) {
+            const unsigned long long E = __ldg(entb + e);
+            const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
+            const int t = j - 2 + dt;
+            if (t >= anchor_min) {
+              const double* rec = pb + kBS * wrap(astb[((t + 4) & 3) * kAC + c + dc] + idx, A.capb);
+              const double La = rec[la];
+              const int lb0 = (E >> 13) & 15, lb1 = (E >> 17) & 15, lb2 = (E >> 21) & 15;
+              dg0 = fma(La, lb0 != 15 ? rec[lb0 != 15 ? lb0 : 0] : 0.0, dg0);
+              dg1 = fma(La, lb1 != 15 ? rec[lb1 != 15 ? lb1 : 0] : 0.0, dg1);
+              dg2 = fma(La, lb2 != 15 ? rec[lb2 != 15 ? lb2 : 0] : 0.0, dg2);
+            }
+          }
         }
-      }
-      const unsigned long long* entb = ent + n_m;
-      for (int e = 0; e < nmax_b; ++e) {
-        if (e < n_b) {
-          const unsigned long long E = __ldg(entb + e);
-          const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
-          const int t = j - 2 + dt, sc = c + dc;
-          const int q = wrap(astb[((t + 4) & 3) * kAC + sc] + idx, A.capb);
-          const double La = pbL[la * A.capb + q];
-#pragma unroll
-          for (int c3 = 0; c3 < 3; ++c3) g3[c3] += La * pbD[c3 * A.capb + q];
+        acc0[0] += dg0; acc0[4] += dg0; acc0[8] += dg0;
+        acc1[0] += dg1; acc1[4] += dg1; acc1[8] += dg1;
+        acc2[0] += dg2; acc2[4] += dg2; acc2[8] += dg2;
+        // ---- warp-cooperative writes: 9 lanes per 72-byte block, through a 288-double buffer
+        const int nb = active ? (h0.z & 0xF) : 0;
+        const int nbmax = __reduce_max_sync(0xffffffffu, nb);
+        double* wb = wbuf + warp * 288;
+        double* vals = A.vals + item * A.vs;
+        const int rpa = (active && owned_row) ? A.row_ptr[a_loc] : 0;
+#define BSF_OUT(M, ACC)                                                                             \
+  if ((M) < nbmax) {                                                                                \
+    const int kab = (h1.x >> (8 * (M))) & 0xFF, kba = (h1.y >> (8 * (M))) & 0xFF;                   \
+    const int dpk = (h1.z >> (5 * (M))) & 31, di = (dpk & 7) - 2, dj = dpk >> 3;                    \
+    const bool mv = ((M) < nb);                                                                     \
+    const int jb = j + dj;                                                                          \
+    const int pf = (mv && owned_row) ? rpa + kab : -1;                                              \
+    int pt = -1;                                                                                    \
+    if (mv && !(di == 0 && dj == 0) && jb >= A.r0 && jb < A.r1) pt = A.row_ptr[a_loc + di + dj * A.n_u] + kba; \
+    warp_store_block(wb, ACC, false, pf, vals, lane);                                               \
+    warp_store_block(wb, ACC, true, pt, vals, lane);                                                \
+  }
+        BSF_OUT(0, acc0)
+        BSF_OUT(1, acc1)
+        BSF_OUT(2, acc2)
+#undef BSF_OUT
+      } else {
+        double g0 = 0.0, g1 = 0.0, g2 = 0.0;
+        for (int e = 0; e < nmax_m; ++e) {
+          if (e < n_m) {
+            const unsigned long long E = __ldg(ent + e);
+            const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
+            const int t = j - 2 + dt;
+            const double* rec = pm + kMS * wrap(astm[((t + 4) & 3) * kAC + c + dc] + idx, A.capm);
+            const double da1 = rec[21 + 2 * la], da2 = rec[22 + 2 * la];
+            g0 = fma(da1, rec[39], fma(da2, rec[42], g0));
+            g1 = fma(da1, rec[40], fma(da2, rec[43], g1));
+            g2 = fma(da1, rec[41], fma(da2, rec[44], g2));
+          }
         }
-      }
-      if (active) {
-        double* gd = A.g + item * A.gs + 3 * a_loc;
-        gd[0] = g3[0]; gd[1] = g3[1]; gd[2] = g3[2];
-      }
-    }
-    __syncthreads();
-    // ---------------- 4. coalesced copy of the staged row segments
-    if (want_h) {
-#pragma unroll
-      for (int rr = 0; rr < kRS; ++rr) {
-        const int jr = j0 + rr;
-        if (jr >= rb) break;
-        const int64_t afirst = (int64_t)(jr - A.r0) * A.n_u + i0;
-        const int txr = min(kTX, A.n_u - i0);
-        const int64_t b0 = A.row_ptr[afirst], b1 = A.row_ptr[afirst + txr];
-        const int64_t nd = (b1 - b0) * 9;
-        double* dstg = A.vals + item * A.vs + b0 * 9;
-        const double* src = stage + rr * A.max_row_blocks * 9;
-        for (int64_t k = tid; k < nd; k += kThreads) dstg[k] = src[k];
+        const unsigned long long* entb = ent + n_m;
+        for (int e = 0; e < nmax_b; ++e) {
+          if (e < n_b) {
+            const unsigned long long E = __ldg(entb + e);
+            const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
+            const int t = j - 2 + dt;
+            const double* rec = pb + kBS * wrap(astb[((t + 4) & 3) * kAC + c + dc] + idx, A.capb);
+            const double La = rec[la];
+            g0 = fma(La, rec[9], g0);
+            g1 = fma(La, rec[10], g1);
+            g2 = fma(La, rec[11], g2);
+          }
+        }
+        if (active) {
+          double* gd = A.g + item * A.gs + 3 * (int64_t)a_loc;
+          gd[0] = g0; gd[1] = g1; gd[2] = g2;
+        }
       }
     }
     __syncthreads();
@@ -393,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_tile(const TileArgs A) {
   if (tid == 0) {
     double s = 0.0;
     for (int w = 0; w < kThreads / 32; ++w) s += red[w];
-    A.epart[((int64_t)item * A.nchunks + chunk) * A.nstrips + strip] = s;
+    A.epart[((int64_t)item * A.nchunks_total + chunk) * A.nstrips + strip] = s;
   }
 }
 
@@ -502,56 +532,131 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
       b_geo[4 * B + k] = p.c_u; b_geo[5 * B + k] = p.c_v;
     }
   }
-  // ---- strips, chunks, ring capacities, staging size
+  // ---- strips and row chunks.  Chunks whose anchor ring can hold the heavy boundary anchor rows
+  // (t = 0: side spans, t = Sv-1: side spans + knot half cells) form a separate launch with a larger
+  // point pool; interior chunks keep the pool small so two CTAs fit on an SM.
   tt.nstrips = (nu + kTX - 1) / kTX;
-  const int nrows_owned = sh.r1 - sh.r0;
-  tt.chunk = 32;
-  if (nrows_owned <= 48) tt.chunk = ((nrows_owned + 1) / 2) * 2;
-  tt.nchunks = (nrows_owned + tt.chunk - 1) / tt.chunk;
-  int capm = 1, capb = 1, maxrb = 1;
+  std::vector<int> cm(Sv, 0), cb(Sv, 0);   // max points per anchor row over strips
   for (int st = 0; st < tt.nstrips; ++st) {
     const int i0 = st * kTX, slo = std::max(0, i0 - 2), shi = std::min(Su - 1, i0 + kTX - 1);
-    std::vector<int> cm(Sv, 0), cb(Sv, 0);
-    if (slo <= shi)
-      for (int t = 0; t < Sv; ++t) {
-        cm[t] = m_aoff[t * Su + shi + 1] - m_aoff[t * Su + slo];
-        cb[t] = b_aoff[t * Su + shi + 1] - b_aoff[t * Su + slo];
-      }
+    if (slo > shi) continue;
     for (int t = 0; t < Sv; ++t) {
-      int sm = 0, sb = 0;
-      for (int d = 0; d < kRing && t + d < Sv; ++d) { sm += cm[t + d]; sb += cb[t + d]; }
-      capm = std::max(capm, sm);
-      capb = std::max(capb, sb);
-    }
-    const int txr = std::min(kTX, nu - i0);
-    for (int j = sh.r0; j < sh.r1; ++j) {
-      const int64_t af = (int64_t)(j - sh.r0) * nu + i0;
-      maxrb = std::max(maxrb, sh.row_ptr[af + txr] - sh.row_ptr[af]);
+      cm[t] = std::max(cm[t], m_aoff[t * Su + shi + 1] - m_aoff[t * Su + slo]);
+      cb[t] = std::max(cb[t], b_aoff[t * Su + shi + 1] - b_aoff[t * Su + slo]);
     }
   }
-  tt.capm = capm | 1;   // odd capacities spread SoA columns over banks
-  tt.capb = capb | 1;
-  tt.max_row_blocks = maxrb;
-  tt.smem = sizeof(double) * (kPosRows * kPosCols * 3 + 27 * (size_t)tt.capm + 12 * (size_t)tt.capb +
-                              kRS * (size_t)maxrb * 9 + 32) +
-            sizeof(int) * ((size_t)tt.capm + 2 * kRing * kAC);
-  if (tt.smem > 227 * 1024) return 1;
-  // ---- gather programs: one per (boundary class u, boundary class v, parity)
+  auto ring_need = [&](int ra, int rb, int& pm_, int& pb_) {   // pool need of one chunk
+    pm_ = 1; pb_ = 1;
+    for (int j0 = ra - 2; j0 < rb; j0 += kRS) {
+      int sm = 0, sb = 0;
+      for (int t = j0 - 2; t <= j0 + 1; ++t)
+        if (t >= 0 && t < Sv) { sm += cm[t]; sb += cb[t]; }
+      pm_ = std::max(pm_, sm);
+      pb_ = std::max(pb_, sb);
+    }
+  };
+  std::vector<int2> cl[2];   // 0 interior, 1 boundary
+  {
+    const int r0 = sh.r0, r1 = sh.r1;
+    std::vector<int> cuts{r0};
+    const int lo_edge = std::min(r1, std::max(r0, 6)), hi_edge = std::max(lo_edge, std::min(r1, Sv - 4));
+    if (lo_edge > r0) cuts.push_back(lo_edge);
+    const int span = hi_edge - lo_edge;
+    if (span > 0) {
+      const int n = (span + 31) / 32;
+      for (int k = 1; k < n; ++k) cuts.push_back(lo_edge + ((span * k / n) & ~1));
+      cuts.push_back(hi_edge);
+    }
+    if (r1 > cuts.back()) cuts.push_back(r1);
+    for (size_t k = 0; k + 1 < cuts.size(); ++k) {
+      if (cuts[k + 1] <= cuts[k]) continue;
+      int pm_, pb_;
+      ring_need(cuts[k], cuts[k + 1], pm_, pb_);
+      const bool heavy = (cuts[k] - 4 <= 0) || (cuts[k + 1] + 1 >= Sv - 1);
+      cl[heavy ? 1 : 0].push_back(make_int2(cuts[k], cuts[k + 1]));
+    }
+  }
+  tt.nchunks = (int)(cl[0].size() + cl[1].size());
+  for (int L = 0; L < 2; ++L) {
+    int capm = 1, capb = 1;
+    for (const int2& ch : cl[L]) {
+      int pm_, pb_;
+      ring_need(ch.x, ch.y, pm_, pb_);
+      capm = std::max(capm, pm_);
+      capb = std::max(capb, pb_);
+    }
+    tt.capm_l[L] = capm;
+    tt.capb_l[L] = capb;
+    tt.nch_l[L] = (int)cl[L].size();
+    tt.smem_l[L] = sizeof(double) * (kPosRows * kPosCols * 3 + (size_t)kMS * capm + (size_t)kBS * capb +
+                                     (kThreads / 32) * 288 + 32) +
+                   sizeof(int) * (2 * kRing * kAC);
+    if (!cl[L].empty() && tt.smem_l[L] > 227 * 1024) return 1;
+  }
+  std::vector<int2> chunks(cl[0]);
+  chunks.insert(chunks.end(), cl[1].begin(), cl[1].end());
+  // ---- gather programs: one per (boundary class u, boundary class v, parity).  Forward blocks of a
+  // control point a = (i, j): b = (i+di, j+dj) after a in storage order, split into 5 tasks of <= 3
+  // blocks: T0 dj=0 di 0..2 | T1a dj=1 di -2..0 | T1b dj=1 di 1..2 | T2a dj=2 di -2..-1 | T2b dj=2 di 0..2.
+  // Task 5 gathers the gradient.  Block ranks come from the structural pattern of ANY row (also rows
+  // outside the slab), so one program serves every control point of its class.
+  static const int tdj[5] = {0, 1, 1, 2, 2}, tlo[5] = {0, -2, 1, -2, 0}, thi[5] = {2, 0, 2, -1, 2};
+  struct SPt { int ou, ov; uint16_t mask; };
+  std::vector<SPt> spts;
+  std::vector<int32_t> s_aoff(nanch + 1, 0);
+  {
+    std::vector<RulePoint> rp;
+    std::vector<SPt> tmp;
+    for (int kind = 0; kind < 2; ++kind) {
+      make_rule(kind ? sh.brule : sh.mrule, kind == 1, Su, Sv, rp);
+      for (const RulePoint& q : rp) {
+        const int ou = std::min((int)std::floor(q.u), Su - 1), ov = std::min((int)std::floor(q.v), Sv - 1);
+        tmp.push_back({ou, ov, stencil_mask(kind == 1, q.knot_u, q.knot_v)});
+      }
+    }
+    for (const SPt& p : tmp) ++s_aoff[p.ov * Su + p.ou + 1];
+    for (int a = 0; a < nanch; ++a) s_aoff[a + 1] += s_aoff[a];
+    spts.resize(tmp.size());
+    std::vector<int32_t> fill(s_aoff.begin(), s_aoff.end() - 1);
+    for (const SPt& p : tmp) spts[fill[p.ov * Su + p.ou]++] = p;
+  }
+  auto row_cols = [&](int i, int j) {   // structural column list of block row (i, j), global indices
+    std::vector<int> cols{j * nu + i};
+    for (int t = std::max(0, j - 2); t <= std::min(Sv - 1, j); ++t)
+      for (int s2 = std::max(0, i - 2); s2 <= std::min(Su - 1, i); ++s2)
+        for (int k = s_aoff[t * Su + s2]; k < s_aoff[t * Su + s2 + 1]; ++k) {
+          const SPt& p = spts[k];
+          const int la = (i - s2) + 3 * (j - t);
+          if (!((p.mask >> la) & 1)) continue;
+          for (int e = 0; e < 9; ++e)
+            if ((p.mask >> e) & 1) cols.push_back((t + e / 3) * nu + s2 + e % 3);
+        }
+    std::sort(cols.begin(), cols.end());
+    cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+    return cols;
+  };
   std::vector<int16_t> lut(kNCls * kNCls * 2, -1);
   std::vector<int4> tasks;
   std::vector<unsigned long long> ents;
   auto build_prog = [&](int i, int j) {
-    const int64_t a_loc = (int64_t)(j - sh.r0) * nu + i;
-    const int32_t* c0 = sh.col_idx.data() + sh.row_ptr[a_loc];
-    const int nc = sh.row_ptr[a_loc + 1] - sh.row_ptr[a_loc];
-    int klo[5], nb[5];
-    for (int dj = -2; dj <= 2; ++dj) {
-      int lo = -1, n = 0;
-      for (int k = 0; k < nc; ++k)
-        if (c0[k] / nu == j + dj) { if (lo < 0) lo = k; ++n; }
-      klo[dj + 2] = lo < 0 ? 0 : lo;
-      nb[dj + 2] = n;
-      if (n > 5) return false;
+    const std::vector<int> ca = row_cols(i, j);
+    const int a = j * nu + i;
+    int nb[5], kab[5][3], kba[5][3], dpk[5][3], bcol[5][3];
+    for (int tk = 0; tk < 5; ++tk) {
+      nb[tk] = 0;
+      for (int k = 0; k < (int)ca.size(); ++k) {
+        const int b = ca[k], di = b % nu - i, dj = b / nu - j;
+        if (dj != tdj[tk] || di < tlo[tk] || di > thi[tk]) continue;
+        if (nb[tk] == 3) return false;
+        const std::vector<int> cb = row_cols(b % nu, b / nu);
+        const int kb = (int)(std::lower_bound(cb.begin(), cb.end(), a) - cb.begin());
+        if (kb >= (int)cb.size() || cb[kb] != a || k > 255 || kb > 255) return false;
+        kab[tk][nb[tk]] = k;
+        kba[tk][nb[tk]] = kb;
+        dpk[tk][nb[tk]] = (di + 2) | (dj << 3);
+        bcol[tk][nb[tk]] = b;
+        ++nb[tk];
+      }
     }
     std::vector<unsigned long long> lists[kTasks][2];
     for (int kind = 0; kind < 2; ++kind) {
@@ -560,24 +665,25 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
       const std::vector<Point>& P = kind ? sh.bend : sh.mem;
       for (int dt = 0; dt < 3; ++dt)
         for (int dc = 0; dc < 3; ++dc) {
-          const int t = j - 2 + dt, s = i - 2 + dc;
-          if (t < 0 || t >= Sv || s < 0 || s >= Su) continue;
-          const int an = t * Su + s;
-          for (int idx = 0; idx < aoff[an + 1] - aoff[an]; ++idx) {
+          const int t = j - 2 + dt, s2 = i - 2 + dc;
+          if (t < 0 || t >= Sv || s2 < 0 || s2 >= Su) continue;
+          const int an = t * Su + s2;
+          const int npts = aoff[an + 1] - aoff[an];
+          for (int idx = 0; idx < npts; ++idx) {
             const Point& p = P[ord[aoff[an] + idx]];
-            const int la = (i - s) + 3 * (j - t);
+            const int la = (i - s2) + 3 * (j - t);
             if (!((p.mask >> la) & 1)) continue;
             const unsigned long long base = (unsigned long long)dt | ((unsigned long long)dc << 2) |
                                             ((unsigned long long)kind << 4) | ((unsigned long long)idx << 5) |
                                             ((unsigned long long)la << 9);
-            lists[5][kind].push_back(base | (0xFFFFFull << 13));
+            lists[5][kind].push_back(base | (0xFFFull << 13));
             for (int tk = 0; tk < 5; ++tk) {
               unsigned long long lbs = 0;
               bool any = false;
-              for (int m = 0; m < 5; ++m) {
+              for (int m = 0; m < 3; ++m) {
                 unsigned long long lb = 15;
                 if (m < nb[tk]) {
-                  const int b = c0[klo[tk] + m], ib = b % nu - s, jb = b / nu - t;
+                  const int b = bcol[tk][m], ib = b % nu - s2, jb = b / nu - t;
                   if (ib >= 0 && ib < 3 && jb >= 0 && jb < 3 && ((p.mask >> (ib + 3 * jb)) & 1)) {
                     lb = (unsigned long long)(ib + 3 * jb);
                     any = true;
@@ -591,19 +697,33 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
         }
     }
     for (int tk = 0; tk < kTasks; ++tk) {
-      int4 h;
-      h.x = (int)ents.size();
-      h.y = (int)lists[tk][0].size() | ((int)lists[tk][1].size() << 16);
-      h.z = tk < 5 ? (klo[tk] | (nb[tk] << 8)) : 0;
-      h.w = 0;
+      int4 h0, h1;
+      h0.x = (int)ents.size();
+      h0.y = (int)lists[tk][0].size() | ((int)lists[tk][1].size() << 16);
+      h0.z = tk < 5 ? nb[tk] : 0;
+      h0.w = 0;
+      h1 = make_int4(0, 0, 0, 0);
+      if (tk < 5)
+        for (int m = 0; m < nb[tk]; ++m) {
+          h1.x |= kab[tk][m] << (8 * m);
+          h1.y |= kba[tk][m] << (8 * m);
+          h1.z |= dpk[tk][m] << (5 * m);
+        }
       ents.insert(ents.end(), lists[tk][0].begin(), lists[tk][0].end());
       ents.insert(ents.end(), lists[tk][1].begin(), lists[tk][1].end());
-      tasks.push_back(h);
+      tasks.push_back(h0);
+      tasks.push_back(h1);
     }
     return true;
   };
+  // representatives: owned rows first (their anchor windows lie inside the slab's point list, so
+  // their programs are complete); the two halo rows above a slab only add classes not seen yet
+  // (entries below the slab window are skipped at run time anyway)
   int nprog = 0;
-  for (int j = sh.r0; j < sh.r1; ++j) {
+  std::vector<int> rows;
+  for (int j = sh.r0; j < sh.r1; ++j) rows.push_back(j);
+  for (int j = std::max(0, sh.r0 - 2); j < sh.r0; ++j) rows.push_back(j);
+  for (int j : rows) {
     const int cv = bclass(j, sh.n_v);
     for (int i = 0; i < nu; ++i) {
       const int key = (bclass(i, nu) * kNCls + cv) * 2 + ((i + j) & 1);
@@ -612,15 +732,28 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
       if (!build_prog(i, j)) return 1;
     }
   }
+  // consistency: the structural pattern equals the slab's pattern on every owned row
+  for (int j = sh.r0; j < sh.r1; j += std::max(1, (sh.r1 - sh.r0) / 7))
+    for (int i = 0; i < nu; i += std::max(1, nu / 7)) {
+      const std::vector<int> c = row_cols(i, j);
+      const int64_t al = (int64_t)(j - sh.r0) * nu + i;
+      if ((int)c.size() != sh.row_ptr[al + 1] - sh.row_ptr[al] ||
+          !std::equal(c.begin(), c.end(), sh.col_idx.begin() + sh.row_ptr[al])) {
+        err = "internal: structural pattern mismatch";
+        return -1;
+      }
+    }
   // ---- upload
   std::vector<int32_t> rp(sh.row_ptr.begin(), sh.row_ptr.end());
   bool ok = upload(dalloc, &tt.m_aoff, m_aoff) && upload(dalloc, &tt.b_aoff, b_aoff) &&
             upload(dalloc, &tt.m_info, m_info) && upload(dalloc, &tt.b_info, b_info) &&
             upload(dalloc, &tt.utab, utab) && upload(dalloc, &tt.vtab, vtab) && upload(dalloc, &tt.stab, stab) &&
             upload(dalloc, &tt.m_geo, m_geo) && upload(dalloc, &tt.b_geo, b_geo) && upload(dalloc, &tt.lut, lut) &&
-            upload(dalloc, &tt.tasks, tasks) && upload(dalloc, &tt.ent, ents) && upload(dalloc, &tt.row_ptr, rp);
+            upload(dalloc, &tt.tasks, tasks) && upload(dalloc, &tt.ent, ents) && upload(dalloc, &tt.row_ptr, rp) &&
+            upload(dalloc, &tt.chunks, chunks);
   if (!ok) { err = "tile tables: device allocation failed"; return -7; }
-  if (cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tt.smem) != cudaSuccess) {
+  const size_t smax = std::max(tt.smem_l[0], tt.smem_l[1]);
+  if (cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax) != cudaSuccess) {
     cudaGetLastError();
     return 1;
   }
@@ -632,6 +765,7 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
               int nbatch, double* d_E, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride,
               cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc) {
   const int64_t need = (int64_t)nbatch * tt.nstrips * tt.nchunks;
+  (void)0;
   if (need > tt.e_cap) {
     void* p = dalloc(need * sizeof(double));
     if (!p) return -7;
@@ -642,8 +776,7 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
   A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride; A.epart = tt.e_part;
   A.n_u = tt.n_u; A.n_v = tt.n_v; A.Su = tt.Su; A.Sv = tt.Sv; A.r0 = tt.r0; A.r1 = tt.r1;
   A.xlo = sh.xlo; A.xhi = sh.xhi;
-  A.capm = tt.capm; A.capb = tt.capb; A.chunk = tt.chunk; A.nchunks = tt.nchunks; A.nstrips = tt.nstrips;
-  A.max_row_blocks = tt.max_row_blocks;
+  A.nchunks_total = tt.nchunks; A.nstrips = tt.nstrips;
   A.affine = tt.affine; A.project = (flags & 1) ? 1 : 0;
   A.G00 = tt.G[0]; A.G01 = tt.G[1]; A.G10 = tt.G[2]; A.G11 = tt.G[3]; A.detJ = tt.detJ;
   A.mu1 = (flags & 2) ? 0.0 : mat.mu_st1;
@@ -656,9 +789,19 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
   A.utab = tt.utab; A.vtab = tt.vtab; A.stab = tt.stab; A.m_geo = tt.m_geo; A.b_geo = tt.b_geo;
   A.Mm = (int64_t)sh.mem.size(); A.Bm = (int64_t)sh.bend.size();
   A.lut = tt.lut; A.tasks = tt.tasks; A.ent = tt.ent; A.row_ptr = tt.row_ptr;
-  dim3 grid(tt.nstrips, tt.nchunks, nbatch);
-  k_tile<<<grid, kThreads, tt.smem, st>>>(A);
-  int nl = 1;
+  int nl = 0;
+  int base = 0;
+  for (int L = 0; L < 2; ++L) {   // interior chunks, then boundary chunks
+    if (tt.nch_l[L] == 0) continue;
+    A.capm = tt.capm_l[L];
+    A.capb = tt.capb_l[L];
+    A.chunk_base = base;
+    A.chunks = tt.chunks + base;
+    dim3 grid(tt.nstrips, tt.nch_l[L], nbatch);
+    k_tile<<<grid, kThreads, tt.smem_l[L], st>>>(A);
+    ++nl;
+    base += tt.nch_l[L];
+  }
   if (d_E) {
     k_energy_final<<<nbatch, 256, 0, st>>>(tt.e_part, tt.nstrips * tt.nchunks, d_E);
     ++nl;

@@ -24,13 +24,13 @@ constexpr int kNCls = 13;      // boundary-distance classes per direction
 struct TileTables {
   int ok = 0;
   int n_u = 0, n_v = 0, Su = 0, Sv = 0, r0 = 0, r1 = 0, xlo = 0;
-  int capm = 0, capb = 0;          // ring pool capacities (points)
-  int nstrips = 0, chunk = 0, nchunks = 0;
-  int max_row_blocks = 0;          // max blocks of one strip row segment
+  int nstrips = 0, nchunks = 0;
+  int capm_l[2] = {1, 1}, capb_l[2] = {1, 1}, nch_l[2] = {0, 0};   // per chunk list (interior, boundary)
+  size_t smem_l[2] = {0, 0};
+  int2* chunks = nullptr;          // [nchunks] (ra, rb): interior chunks then boundary chunks
   int affine = 0;
   double G[4] = {0, 0, 0, 0};      // affine: G[r*2+c]
   double detJ = 0;
-  size_t smem = 0;
   int32_t* m_aoff = nullptr;       // [Sv*Su+1] anchor -> first membrane point (points sorted by anchor)
   int32_t* b_aoff = nullptr;
   uint2* m_info = nullptr;         // per sorted point: (u-table | v-table << 16, shape | anchor column << 16)
