@@ -37,7 +37,7 @@ METRIC = "elements/sec for fp64 energy+grad+Hessian assembly; HBM GB/s & FP64 % 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C2", choices=["C2", "C4"])
@@ -71,7 +71,7 @@ class Clocks:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -103,6 +103,15 @@ class Clocks:
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def traffic_ratio():
+    """DRAM bytes per algorithmic byte of k_tile from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            return float(json.load(f)["dram_bytes_per_algorithmic_byte"])
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def peaks():
@@ -244,7 +253,7 @@ def bench_ours(args, rank, world, local_rank):
     achieved = alg / (call_avg * 1e-3) / 1e9
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        v, th, n, t = run_oracle_sample(sheets[:3], args.flags, budget_s=20.0)
+        v, th, n, t = run_oracle_sample(sheets, args.flags, budget_s=15.0)
         cpu = {"value": v, "unit": "elements/s", "cores": th, "kind": "oracle",
                "sample": f"{n} of the {n_units} {args.config} states, E+g+H, {t:.1f} s of CPU work, {th} threads"}
     line = {
@@ -257,7 +266,9 @@ def bench_ours(args, rank, world, local_rank):
                    "path": "generic" if (flags & B.GENERIC_PATH) else "tile",
                    "l2": "working set per step = %.2f GB of outputs > 126 MB L2 (no flush needed)" % (alg / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "peak_kind": peak_kind,
+                     "traffic": (None if traffic_ratio() is None or (flags & B.GENERIC_PATH) else traffic_ratio() * alg),
+                     "traffic_source": "dram read+write per algorithmic byte of k_tile, profiles/r01_traffic.json",
+                     "peak_kind": peak_kind,
                      "per_launch": "one bsf_eval_all_batch call (%d states): %d algorithmic bytes, avg %.1f us"
                                    % (n_units, alg, call_avg * 1e3)},
         "cpu_baseline": cpu,

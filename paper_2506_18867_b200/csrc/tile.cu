@@ -78,17 +78,19 @@ constexpr int kBS = 13;    // bending:  [0,9) L^_e  [9,12) D^  [12] pad
 
 __device__ __forceinline__ int wrap(int q, int cap) { return q >= cap ? q - cap : q; }
 
-// Warp-cooperative store of one 3x3 block per lane (9 lanes per 72-byte block); pos < 0 skips.
+// Warp-cooperative store of one 3x3 block per lane: lanes 9k..9k+8 store block 3r+k of round r
+// (72 contiguous bytes each); pos < 0 skips.  `transpose` selects H^T.
 __device__ __forceinline__ void warp_store_block(double* wb, const double (&blk)[9], bool transpose, int pos,
                                                  double* vals, int lane) {
 #pragma unroll
   for (int q = 0; q < 9; ++q) wb[lane * 9 + q] = transpose ? blk[3 * (q % 3) + q / 3] : blk[q];
   __syncwarp();
+  const int sub = lane / 9, el = lane - sub * 9;
 #pragma unroll
-  for (int rr = 0; rr < 9; ++rr) {
-    const int f = rr * 32 + lane, owner = f / 9, el = f - owner * 9;
+  for (int rr = 0; rr < 11; ++rr) {
+    const int owner = min(3 * rr + sub, 31);
     const int po = __shfl_sync(0xffffffffu, pos, owner);
-    if (po >= 0) vals[(int64_t)po * 9 + el] = wb[f];
+    if (lane < 27 && 3 * rr + sub < 32 && po >= 0) vals[(int64_t)po * 9 + el] = wb[owner * 9 + el];
   }
   __syncwarp();
 }
@@ -277,33 +279,40 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
     // forward pairs reach into the first owned rows (transpose-only)
     const bool halo_step = (j0 < ra);
     if (halo_step && !(ra == A.r0 && A.r0 > 0)) continue;
-    // ---------------- 4. gather: symmetric forward tasks (b after a), both H_ab and H_ab^T written
+    // ---------------- 4. gather: symmetric forward tasks (b after a), both H_ab and H_ab^T written.
+    // warps 0-1: group 0 (diagonal row) for control points 0-15 / 16-31 of the step, the entry list
+    // split between lane halves; warps 2-5: groups 1-4; warp 6: gradient.
     {
       const int warp = tid >> 5, lane = tid & 31;
-      const int r = lane / kTX, c = lane - r * kTX;
+      const bool split = (warp < 2);
+      const int cpi = split ? warp * 16 + (lane & 15) : lane;
+      const int half = split ? (lane >> 4) : 0;
+      const int task = split ? 0 : (warp < 6 ? warp - 1 : 5);
+      const int r = cpi / kTX, c = cpi - r * kTX;
       const int i = i0 + c, j = j0 + r;
       const bool owned_row = (j >= A.r0);
       bool active = (i < A.n_u) && (j < rb) && (j >= 0);
-      if (warp == 0 || warp == 5) active = active && owned_row;        // T0 / gradient: owned rows only
-      active = active && ((warp < 5) ? want_h : want_g);
+      if (task == 0 || task == 5) active = active && owned_row;        // group 0 / gradient: owned rows only
+      active = active && ((task < 5) ? want_h : want_g);
       const int anchor_min = max(0, ra - 2);
       int4 h0 = make_int4(0, 0, 0, 0), h1 = make_int4(0, 0, 0, 0);
       int a_loc = 0;
       if (active) {
         const int pid = A.lut[(bclass(i, A.n_u) * kNCls + bclass(j, A.n_v)) * 2 + ((i + j) & 1)];
-        h0 = A.tasks[(pid * kTasks + warp) * 2];
-        h1 = A.tasks[(pid * kTasks + warp) * 2 + 1];
+        h0 = A.tasks[(pid * kTasks + task) * 2];
+        h1 = A.tasks[(pid * kTasks + task) * 2 + 1];
         a_loc = (j - A.r0) * A.n_u + i;
       }
       const int n_m = active ? (h0.y & 0xFFFF) : 0, n_b = active ? (h0.y >> 16) : 0;
       const int nmax_m = __reduce_max_sync(0xffffffffu, n_m), nmax_b = __reduce_max_sync(0xffffffffu, n_b);
       const unsigned long long* ent = A.ent + h0.x;
-      if (warp < 5) {
+      if (task < 5) {
         double acc0[9], acc1[9], acc2[9];
         double dg0 = 0.0, dg1 = 0.0, dg2 = 0.0;
 #pragma unroll
         for (int q = 0; q < 9; ++q) { acc0[q] = 0.0; acc1[q] = 0.0; acc2[q] = 0.0; }
-        for (int e = 0; e < nmax_m; ++e) {
+        const int estep = split ? 2 : 1;
+        for (int e = half; e < nmax_m; e += estep) {
           if (e < n_m) {
             const unsigned long long E = __ldg(ent + e);
             const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
@@ -341,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
           }
         }
         const unsigned long long* entb = ent + n_m;
-        for (int e = 0; e < nmax_b; ++e) {
+        for (int e = half; e < nmax_b; e += estep) {
           if (e < n_b) {
             const unsigned long long E = __ldg(entb + e);
             const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
@@ -359,7 +368,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
         acc0[0] += dg0; acc0[4] += dg0; acc0[8] += dg0;
         acc1[0] += dg1; acc1[4] += dg1; acc1[8] += dg1;
         acc2[0] += dg2; acc2[4] += dg2; acc2[8] += dg2;
-        // ---- warp-cooperative writes: 9 lanes per 72-byte block, through a 288-double buffer
+        if (split) {   // combine the two lane halves (same control point, complementary entries)
+#pragma unroll
+          for (int q = 0; q < 9; ++q) {
+            acc0[q] += __shfl_xor_sync(0xffffffffu, acc0[q], 16);
+            acc1[q] += __shfl_xor_sync(0xffffffffu, acc1[q], 16);
+            acc2[q] += __shfl_xor_sync(0xffffffffu, acc2[q], 16);
+          }
+        }
+        // ---- warp-cooperative writes (72-byte blocks).  Split warps: the lower half stores H_ab, the
+        // upper half H_ab^T of the same block in one pass.
         const int nb = active ? (h0.z & 0xF) : 0;
         const int nbmax = __reduce_max_sync(0xffffffffu, nb);
         double* wb = wbuf + warp * 288;
@@ -374,8 +392,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
     const int pf = (mv && owned_row) ? rpa + kab : -1;                                              \
     int pt = -1;                                                                                    \
     if (mv && !(di == 0 && dj == 0) && jb >= A.r0 && jb < A.r1) pt = A.row_ptr[a_loc + di + dj * A.n_u] + kba; \
-    warp_store_block(wb, ACC, false, pf, vals, lane);                                               \
-    warp_store_block(wb, ACC, true, pt, vals, lane);                                                \
+    if (split) {                                                                                    \
+      warp_store_block(wb, ACC, half == 1, half ? pt : pf, vals, lane);                             \
+    } else {                                                                                        \
+      warp_store_block(wb, ACC, false, pf, vals, lane);                                             \
+      warp_store_block(wb, ACC, true, pt, vals, lane);                                              \
+    }                                                                                               \
   }
         BSF_OUT(0, acc0)
         BSF_OUT(1, acc1)
@@ -600,7 +622,12 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
   // blocks: T0 dj=0 di 0..2 | T1a dj=1 di -2..0 | T1b dj=1 di 1..2 | T2a dj=2 di -2..-1 | T2b dj=2 di 0..2.
   // Task 5 gathers the gradient.  Block ranks come from the structural pattern of ANY row (also rows
   // outside the slab), so one program serves every control point of its class.
-  static const int tdj[5] = {0, 1, 1, 2, 2}, tlo[5] = {0, -2, 1, -2, 0}, thi[5] = {2, 0, 2, -1, 2};
+  static const int grp_n[5] = {3, 3, 3, 3, 1};
+  static const int grp_off[5][3][2] = {{{0, 0}, {1, 0}, {2, 0}},
+                                       {{-2, 1}, {-1, 1}, {0, 1}},
+                                       {{1, 1}, {2, 1}, {-2, 2}},
+                                       {{-1, 2}, {0, 2}, {1, 2}},
+                                       {{2, 2}, {0, 0}, {0, 0}}};
   struct SPt { int ou, ov; uint16_t mask; };
   std::vector<SPt> spts;
   std::vector<int32_t> s_aoff(nanch + 1, 0);
@@ -644,10 +671,12 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
     int nb[5], kab[5][3], kba[5][3], dpk[5][3], bcol[5][3];
     for (int tk = 0; tk < 5; ++tk) {
       nb[tk] = 0;
-      for (int k = 0; k < (int)ca.size(); ++k) {
-        const int b = ca[k], di = b % nu - i, dj = b / nu - j;
-        if (dj != tdj[tk] || di < tlo[tk] || di > thi[tk]) continue;
-        if (nb[tk] == 3) return false;
+      for (int g = 0; g < grp_n[tk]; ++g) {
+        const int di = grp_off[tk][g][0], dj = grp_off[tk][g][1];
+        if (i + di < 0 || i + di >= nu || j + dj >= sh.n_v) continue;
+        const int b = (j + dj) * nu + i + di;
+        const int k = (int)(std::lower_bound(ca.begin(), ca.end(), b) - ca.begin());
+        if (k >= (int)ca.size() || ca[k] != b) continue;
         const std::vector<int> cb = row_cols(b % nu, b / nu);
         const int kb = (int)(std::lower_bound(cb.begin(), cb.end(), a) - cb.begin());
         if (kb >= (int)cb.size() || cb[kb] != a || k > 255 || kb > 255) return false;
@@ -657,6 +686,12 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
         bcol[tk][nb[tk]] = b;
         ++nb[tk];
       }
+    }
+    {   // every forward block of the row must belong to a group
+      int fwd = 0, tot = 0;
+      for (int b : ca) if (b > a) ++fwd;
+      for (int tk = 0; tk < 5; ++tk) tot += nb[tk];
+      if (tot != fwd + 1) return false;
     }
     std::vector<unsigned long long> lists[kTasks][2];
     for (int kind = 0; kind < 2; ++kind) {

@@ -17,8 +17,8 @@ namespace bsf {
 constexpr int kTX = 16;        // strip width (control points)
 constexpr int kRS = 2;         // output rows per step
 constexpr int kRing = kRS + 2; // anchor rows resident in the ring
-constexpr int kTasks = 6;      // dj = -2..2 Hessian tasks + 1 gradient task per control point
-constexpr int kThreads = 32 * kTasks;
+constexpr int kTasks = 6;      // program tasks per control point: 5 forward-block groups + gradient
+constexpr int kThreads = 32 * 7;   // warps 0-1 group 0 (split), 2-5 groups 1-4, 6 gradient
 constexpr int kNCls = 13;      // boundary-distance classes per direction
 
 struct TileTables {
