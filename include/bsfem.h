@@ -135,12 +135,25 @@ bsf_status bsf_assemble_hessian(bsf_handle h, const double* d_x, double* d_vals,
 bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, double* d_grad,
                         double* d_vals, int flags, bsf_stream stream);
 
-/* Multi-GPU slab halo exchange: sends the 2 owned boundary rows to the neighbour
- * slabs and receives their 2 rows into d_x's halo rows, over the NCCL communicator `nccl_comm`
- * (an ncclComm_t whose ranks are the slabs in row order).  d_x has the layout described above.
- * Returns BSF_E_NCCL if the library was built without NCCL or the comm call fails. */
+/* ---- Multi-GPU row slabs.  NCCL is loaded at run time
+ * (libnccl.so.2 of the process, e.g. torch's); without it these calls return BSF_E_NCCL. */
+
+/* Rank 0 creates a 128-byte NCCL unique id (host buffer) to broadcast to the other ranks. */
+bsf_status bsf_nccl_get_unique_id(void* out128);
+
+/* Create this rank's communicator (ranks = slabs in row order) on CUDA device `device`. */
+bsf_status bsf_nccl_comm_init(int nranks, const void* id128, int rank, int device, void** comm);
+bsf_status bsf_nccl_comm_destroy(void* comm);
+
+/* Halo exchange: sends the 2 first / last owned rows to the previous / next slab and receives
+ * theirs into d_x's halo rows (layout as above), as one NCCL group on `stream`.  Every slab must
+ * own >= 2 rows.  No Hessian data is communicated (each slab recomputes the <= 2 rows of shared
+ * quadrature points). */
 bsf_status bsf_halo_exchange(bsf_handle h, double* d_x, void* nccl_comm, int rank, int nranks,
                              bsf_stream stream);
+
+/* In-place sum all-reduce of n doubles (the slab energies) over the communicator. */
+bsf_status bsf_allreduce_sum(double* d_buf, int64_t n, void* nccl_comm, bsf_stream stream);
 
 /* Number of kernel launches the most recent compute call enqueued (for the bench's claim). */
 int bsf_last_launch_count(bsf_handle h);

@@ -26,7 +26,8 @@ _STATUS = {0: "OK", -1: "INVALID_ARG", -2: "KNOTS", -3: "TOO_SMALL", -4: "DEGENE
 
 SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_material", "bsf_get_sizes",
            "bsf_get_pattern", "bsf_eval_all_batch", "bsf_eval_energy", "bsf_eval_gradient", "bsf_assemble_hessian", "bsf_eval_all",
-           "bsf_halo_exchange", "bsf_last_launch_count", "bsf_last_error"]
+           "bsf_halo_exchange", "bsf_nccl_get_unique_id", "bsf_nccl_comm_init", "bsf_nccl_comm_destroy",
+           "bsf_allreduce_sum", "bsf_last_launch_count", "bsf_last_error"]
 
 
 class BsfError(RuntimeError):
@@ -69,6 +70,10 @@ def lib():
         L.bsf_eval_gradient.argtypes = [vp, vp, vp, C.c_int, vp]
         L.bsf_assemble_hessian.argtypes = [vp, vp, vp, C.c_int, vp]
         L.bsf_halo_exchange.argtypes = [vp, vp, vp, C.c_int, C.c_int, vp]
+        L.bsf_nccl_get_unique_id.argtypes = [vp]
+        L.bsf_nccl_comm_init.argtypes = [C.c_int, vp, C.c_int, C.c_int, C.POINTER(vp)]
+        L.bsf_nccl_comm_destroy.argtypes = [vp]
+        L.bsf_allreduce_sum.argtypes = [vp, C.c_int64, vp, vp]
         L.bsf_last_launch_count.argtypes = [vp]
         for s in SYMBOLS:
             getattr(L, s).restype = C.c_int if s not in ("bsf_last_error",) else C.c_char_p

@@ -340,8 +340,52 @@ int bsf_last_launch_count(bsf_handle h) { return h ? h->last_launches : 0; }
 
 }  // extern "C"
 
+namespace bsf {
+int nccl_unique_id(void* out128, std::string& err);
+int nccl_comm_init(void** comm, int nranks, const void* id128, int rank, std::string& err);
+int nccl_comm_destroy(void* comm, std::string& err);
+int nccl_halo_exchange(double* d_x, int n_u, int r0, int r1, int xlo, int xhi, int rank, int nranks, void* comm,
+                       void* stream, std::string& err);
+int nccl_allreduce_sum(double* d_buf, size_t n, void* comm, void* stream, std::string& err);
+}  // namespace bsf
+
+extern "C" bsf_status bsf_nccl_get_unique_id(void* out128) {
+  if (!out128) return fail(BSF_E_INVALID_ARG, "null id buffer");
+  std::string err;
+  return bsf::nccl_unique_id(out128, err) ? fail(BSF_E_NCCL, err) : BSF_OK;
+}
+
+extern "C" bsf_status bsf_nccl_comm_init(int nranks, const void* id128, int rank, int device, void** comm) {
+  if (!id128 || !comm || nranks < 1 || rank < 0 || rank >= nranks) return fail(BSF_E_INVALID_ARG, "bad comm arguments");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  std::string err;
+  const int rc = bsf::nccl_comm_init(comm, nranks, id128, rank, err);
+  cudaSetDevice(prev);
+  return rc ? fail(BSF_E_NCCL, err) : BSF_OK;
+}
+
+extern "C" bsf_status bsf_nccl_comm_destroy(void* comm) {
+  if (!comm) return BSF_OK;
+  std::string err;
+  return bsf::nccl_comm_destroy(comm, err) ? fail(BSF_E_NCCL, err) : BSF_OK;
+}
+
 extern "C" bsf_status bsf_halo_exchange(bsf_handle h, double* d_x, void* nccl_comm, int rank, int nranks,
                                         bsf_stream stream) {
-  (void)h; (void)d_x; (void)nccl_comm; (void)rank; (void)nranks; (void)stream;
-  return fail(BSF_E_NCCL, "halo exchange through NCCL is not built in this library version");
+  if (!h || !d_x || !nccl_comm || rank < 0 || rank >= nranks) return fail(BSF_E_INVALID_ARG, "bad halo arguments");
+  if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle");
+  const bsf::Sheet& sh = h->sh;
+  if ((rank > 0 && sh.r1 - sh.r0 < 2) || (rank < nranks - 1 && sh.r1 - sh.r0 < 2))
+    return fail(BSF_E_INVALID_ARG, "every slab must own at least 2 rows");
+  std::string err;
+  const int rc = bsf::nccl_halo_exchange(d_x, sh.n_u, sh.r0, sh.r1, sh.xlo, sh.xhi, rank, nranks, nccl_comm, stream, err);
+  return rc ? fail(BSF_E_NCCL, err) : BSF_OK;
+}
+
+extern "C" bsf_status bsf_allreduce_sum(double* d_buf, int64_t n, void* nccl_comm, bsf_stream stream) {
+  if (!d_buf || !nccl_comm || n < 0) return fail(BSF_E_INVALID_ARG, "bad allreduce arguments");
+  std::string err;
+  return bsf::nccl_allreduce_sum(d_buf, (size_t)n, nccl_comm, stream, err) ? fail(BSF_E_NCCL, err) : BSF_OK;
 }

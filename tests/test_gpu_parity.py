@@ -175,3 +175,30 @@ def test_batch_matches_single_calls():
     va = o.eval(sheets[1].x, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
     assert_parity(float(E[1]), G[1].cpu().numpy(), V[1].cpu().numpy(), Er, gr, vr, what="batch item 1",
                   hdiag=diag_block_norms(vr, rp, ci, 0, sheets[1].n_u), cmax=np.abs(sheets[1].x).max(), vabs=va)
+
+
+def test_slab_sheet_nccl_single_rank():
+    """The library's NCCL entry points on one rank (unique id, comm init, all-reduce) and the
+    SlabSheet driver against the oracle."""
+    import os
+    import torch.distributed as dist
+    from paper_2506_18867_b200 import distributed as D
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        comm = D.NcclComm(0, 1, 0)
+        sh = W.make_c2(state=5)
+        slab = D.SlabSheet(sh, 0, 1, device=0, comm=comm)
+        slab.load_owned(torch.from_numpy(sh.x).cuda())
+        E, g, v = slab.assemble(B.PROJECT_PSD)
+        buf = torch.tensor([1.5, -2.0], dtype=torch.float64, device="cuda")
+        B._check(B.lib().bsf_allreduce_sum(B.C.c_void_p(buf.data_ptr()), 2, comm.comm, B._stream(None)))
+        torch.cuda.synchronize()
+        assert buf.tolist() == [1.5, -2.0]
+        o = O.Oracle.from_sheet(sh)
+        Er, gr, vr = o.eval(sh.x, flags=O.FLAG_PROJECT)
+        assert rel_energy(float(E.item()), Er) <= TOL
+        comm.close()
+    finally:
+        dist.destroy_process_group()
