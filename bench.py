@@ -40,7 +40,7 @@ def parse():
     p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="C2", choices=["C2", "C4"])
+    p.add_argument("--config", default="C2", choices=["C2", "C4", "C5"])
     p.add_argument("--states", type=int, default=100)
     p.add_argument("--flags", type=int, default=1, help="1 = BSF_PROJECT_PSD")
     p.add_argument("--generic", action="store_true", help="force the generic gather path")
@@ -251,6 +251,85 @@ def bench_c4_slabs(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def bench_c5(args, rank, world, local_rank):
+    """C5: batch of 256^2 sheets with per-sheet side length / E / nu, 8 sheets per GPU (weak scaling:
+    rank r assembles sheets 8r..8r+7 of the 64-sheet set), one bsf_eval_all_batch_params launch."""
+    import torch
+    import paper_2506_18867_b200 as B
+    dev = torch.device("cuda", local_rank)
+    per = 8
+    allsh = W.make_c5()
+    sheets = [allsh[(rank * per + k) % len(allsh)] for k in range(per)]
+    h = B.Sheet.from_sheet(sheets[0], device=local_rank)
+    X = torch.stack([torch.from_numpy(q.x) for q in sheets]).to(dev)
+    X_host = X.cpu().pin_memory()
+    P = torch.from_numpy(np.stack([B.affine_params(q.rest_xy, B.material_from_young(q.E, q.nu, q.h))
+                                   for q in sheets])).to(dev)
+    E = torch.zeros(per, dtype=torch.float64, device=dev)
+    G = torch.zeros((per,) + tuple(X.shape[1:]), dtype=torch.float64, device=dev)
+    V = torch.zeros((per, h.nnzb, 3, 3), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    step = lambda: h.eval_all_batch_params(X, P, E, G, V, args.flags, stream)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    launches = h.last_launch_count()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local_rank) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            step()
+        t1.record(stream)
+        torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        torch.distributed.barrier()
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    el = (sheets[0].n_u - 2) ** 2
+    value = el * per * args.steps * world / (ms * 1e-3)
+    e_host = torch.zeros(per, dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize()
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(args.steps):
+        X.copy_(X_host, non_blocking=True)
+        step()
+        e_host.copy_(E, non_blocking=True)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = s0.elapsed_time(s1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+    if rank != 0:
+        return
+    peak, peak_kind = peaks()
+    alg = algorithmic_bytes(sheets[0].n_u ** 2, h.nnzb) * per
+    line = {
+        "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C5: %d sheets/GPU of 256x256 cps, per-sheet L/E/nu, one batched launch" % per,
+                   "elements_per_sheet": el, "l2": "%.2f GB of outputs per step > 126 MB L2" % (alg / 1e9)},
+        "roofline": {"bound": "hbm", "achieved": alg / (ms / args.steps * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": alg / (ms / args.steps * 1e-3) / 1e9 / peak, "traffic": None, "peak_kind": peak_kind},
+        "cpu_baseline": None,
+        "e2e": {"value": el * per * args.steps * world / (e2e_ms * 1e-3), "unit": "elements/s",
+                "h2d_bytes_per_step": int(X.numel() * 8), "d2h_bytes_per_step": 8 * per},
+        "gpu_launches": launches * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def bench_ours(args, rank, world, local_rank):
     import torch
     import paper_2506_18867_b200 as B
@@ -376,6 +455,8 @@ def main():
     try:
         if args.config == "C4":
             bench_c4_slabs(args, rank, world, local_rank)
+        elif args.config == "C5":
+            bench_c5(args, rank, world, local_rank)
         else:
             bench_ours(args, rank, world, local_rank)
     finally:

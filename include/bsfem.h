@@ -119,6 +119,16 @@ bsf_status bsf_eval_all_batch(bsf_handle h, int nbatch, const double* d_x, int64
                               double* d_energy, double* d_grad, int64_t grad_stride, double* d_vals,
                               int64_t vals_stride, int flags, bsf_stream stream);
 
+/* Batch of DIFFERENT sheets that share the handle's grid size, rules and pattern, each with its own
+ * affine rest map and stiffness (e.g. config C5: 64 flat sheets of side L_s and material E_s, nu_s).
+ * d_params: device, [nbatch][9] doubles = G00 G01 G10 G11 (G = (dX/d(u,v))^-1 of the item's affine
+ * rest map), det(dX/d(u,v)), mu_st1, mu_st2, mu_sh, mu_bd.  Requires an affine handle (flat
+ * Greville sheet); BSF_E_INVALID_ARG otherwise.  Other arguments as bsf_eval_all_batch. */
+bsf_status bsf_eval_all_batch_params(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride,
+                                     const double* d_params, double* d_energy, double* d_grad,
+                                     int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags,
+                                     bsf_stream stream);
+
 /* Energy only (the line-search call). d_energy: device, 1 double (overwritten). */
 bsf_status bsf_eval_energy(bsf_handle h, const double* d_x, double* d_energy, int flags,
                            bsf_stream stream);

@@ -15,7 +15,7 @@ import numpy as np
 
 from . import build as _build
 
-__all__ = ["Sheet", "Material", "material_from_young", "lib", "RULE_REDUCED", "RULE_G2_INTERIOR",
+__all__ = ["Sheet", "Material", "material_from_young", "affine_params", "lib", "RULE_REDUCED", "RULE_G2_INTERIOR",
            "RULE_G3_FULL", "PROJECT_PSD", "NO_MEMBRANE", "NO_BENDING", "GENERIC_PATH", "BsfError"]
 
 RULE_REDUCED, RULE_G2_INTERIOR, RULE_G3_FULL = 0, 1, 2
@@ -25,7 +25,7 @@ _STATUS = {0: "OK", -1: "INVALID_ARG", -2: "KNOTS", -3: "TOO_SMALL", -4: "DEGENE
            -5: "SINGULAR_STRETCH", -6: "CUDA", -7: "OOM", -8: "NCCL", -9: "NO_DEVICE"}
 
 SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_material", "bsf_get_sizes",
-           "bsf_get_pattern", "bsf_eval_all_batch", "bsf_eval_energy", "bsf_eval_gradient", "bsf_assemble_hessian", "bsf_eval_all",
+           "bsf_get_pattern", "bsf_eval_all_batch", "bsf_eval_all_batch_params", "bsf_eval_energy", "bsf_eval_gradient", "bsf_assemble_hessian", "bsf_eval_all",
            "bsf_halo_exchange", "bsf_nccl_get_unique_id", "bsf_nccl_comm_init", "bsf_nccl_comm_destroy",
            "bsf_allreduce_sum", "bsf_last_launch_count", "bsf_last_error"]
 
@@ -66,6 +66,8 @@ def lib():
         L.bsf_get_pattern.argtypes = [vp, ip, ip]
         L.bsf_eval_all.argtypes = [vp, vp, vp, vp, vp, C.c_int, vp]
         L.bsf_eval_all_batch.argtypes = [vp, C.c_int, vp, C.c_int64, vp, vp, C.c_int64, vp, C.c_int64, C.c_int, vp]
+        L.bsf_eval_all_batch_params.argtypes = [vp, C.c_int, vp, C.c_int64, vp, vp, vp, C.c_int64, vp, C.c_int64,
+                                                C.c_int, vp]
         L.bsf_eval_energy.argtypes = [vp, vp, vp, C.c_int, vp]
         L.bsf_eval_gradient.argtypes = [vp, vp, vp, C.c_int, vp]
         L.bsf_assemble_hessian.argtypes = [vp, vp, vp, C.c_int, vp]
@@ -108,6 +110,21 @@ def _stream(stream):
     import torch
     s = torch.cuda.current_stream() if stream is None else stream
     return C.c_void_p(s.cuda_stream)
+
+
+def affine_params(rest_xy, material) -> np.ndarray:
+    """Per-item parameters of bsf_eval_all_batch_params for a flat Greville rest grid.  The affine map
+    X(u, v) advances by one interior Greville spacing per knot span, so dX/du and dX/dv are the
+    interior control-point spacings (exact for Greville placement)."""
+    rest_xy = np.asarray(rest_xy, dtype=np.float64)
+    du = rest_xy[0, 3] - rest_xy[0, 2]
+    dv = rest_xy[3, 0] - rest_xy[2, 0]
+    J = np.array([[du[0], dv[0]], [du[1], dv[1]]])
+    G = np.linalg.inv(J)
+    if not isinstance(material, Material):
+        material = Material(*[float(v) for v in material])
+    return np.array([G[0, 0], G[0, 1], G[1, 0], G[1, 1], np.linalg.det(J), material.mu_st1, material.mu_st2,
+                     material.mu_sh, material.mu_bd])
 
 
 class Sheet:
@@ -192,6 +209,17 @@ class Sheet:
         vs = vals[0].numel() if vals is not None else 0
         _check(lib().bsf_eval_all_batch(self._h, int(B), _ptr(x), x[0].numel(), _ptr(energy), _ptr(grad), gs,
                                         _ptr(vals), vs, int(flags), _stream(stream)))
+
+    def eval_all_batch_params(self, x, params, energy=None, grad=None, vals=None, flags=0, stream=None):
+        """Batch of different affine sheets on this handle's grid: params [B, 9] (CUDA float64,
+        see affine_params())."""
+        B = x.shape[0]
+        if tuple(x.shape[1:]) != self.x_shape() or tuple(params.shape) != (B, 9):
+            raise ValueError("x must be [B, *x_shape()] and params [B, 9]")
+        gs = grad[0].numel() if grad is not None else 0
+        vs = vals[0].numel() if vals is not None else 0
+        _check(lib().bsf_eval_all_batch_params(self._h, int(B), _ptr(x), x[0].numel(), _ptr(params), _ptr(energy),
+                                               _ptr(grad), gs, _ptr(vals), vs, int(flags), _stream(stream)))
 
     def eval_energy(self, x, energy, flags=0, stream=None):
         _check(lib().bsf_eval_energy(self._h, _ptr(x), _ptr(energy), int(flags), _stream(stream)))

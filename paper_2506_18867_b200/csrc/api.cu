@@ -277,7 +277,7 @@ bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, doubl
   int nl = 0;
   int rc;
   if (h->tile_ok && !(flags & BSF_GENERIC_PATH))
-    rc = bsf::tile_eval(h->tt, h->sh, d_x, 0, m, flags, 1, d_energy, d_grad, 0, d_vals, 0, st, &nl, h->dalloc());
+    rc = bsf::tile_eval(h->tt, h->sh, d_x, 0, m, flags, 1, d_energy, d_grad, 0, d_vals, 0, st, &nl, h->dalloc(), nullptr);
   else
     rc = bsf::generic_eval(h->gt, d_x, m, flags, nnzb, nrows, d_energy, d_grad, d_vals, st, &nl);
   h->last_launches = nl;
@@ -286,9 +286,9 @@ bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, doubl
   return BSF_OK;
 }
 
-bsf_status bsf_eval_all_batch(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride, double* d_energy,
-                              double* d_grad, int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags,
-                              bsf_stream stream) {
+static bsf_status eval_batch_impl(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride, double* d_energy,
+                                  double* d_grad, int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags,
+                                  bsf_stream stream, const double* d_params) {
   if (!h || !d_x || nbatch < 0) return fail(BSF_E_INVALID_ARG, "null argument / negative batch");
   if (nbatch == 0) return BSF_OK;
   if (flags & ~15) return fail(BSF_E_INVALID_ARG, "unknown flag bits");
@@ -304,9 +304,13 @@ bsf_status bsf_eval_all_batch(bsf_handle h, int nbatch, const double* d_x, int64
   if (prev != h->device) cudaSetDevice(h->device);
   auto st = static_cast<cudaStream_t>(stream);
   int nl = 0, rc = 0;
+  if (d_params && !(h->tile_ok && h->sh.affine && !(flags & BSF_GENERIC_PATH))) {
+    if (prev != h->device) cudaSetDevice(prev);
+    return fail(BSF_E_INVALID_ARG, "per-item parameters need an affine sheet on the tile path");
+  }
   if (h->tile_ok && !(flags & BSF_GENERIC_PATH)) {
     rc = bsf::tile_eval(h->tt, h->sh, d_x, x_stride, h->mat, flags, nbatch, d_energy, d_grad, grad_stride, d_vals,
-                        vals_stride, st, &nl, h->dalloc());
+                        vals_stride, st, &nl, h->dalloc(), d_params);
   } else {
     const int64_t nrows = (int64_t)(h->sh.r1 - h->sh.r0) * h->sh.n_u, nnzb = (int64_t)h->sh.col_idx.size();
     for (int b = 0; b < nbatch && rc == 0; ++b) {
@@ -321,6 +325,21 @@ bsf_status bsf_eval_all_batch(bsf_handle h, int nbatch, const double* d_x, int64
   if (prev != h->device) cudaSetDevice(prev);
   if (rc) return check_cuda("kernel launch") == BSF_OK ? fail(BSF_E_CUDA, "launch failed") : BSF_E_CUDA;
   return BSF_OK;
+}
+
+bsf_status bsf_eval_all_batch(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride, double* d_energy,
+                              double* d_grad, int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags,
+                              bsf_stream stream) {
+  return eval_batch_impl(h, nbatch, d_x, x_stride, d_energy, d_grad, grad_stride, d_vals, vals_stride, flags, stream,
+                         nullptr);
+}
+
+bsf_status bsf_eval_all_batch_params(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride,
+                                     const double* d_params, double* d_energy, double* d_grad, int64_t grad_stride,
+                                     double* d_vals, int64_t vals_stride, int flags, bsf_stream stream) {
+  if (!d_params) return fail(BSF_E_INVALID_ARG, "null parameters");
+  return eval_batch_impl(h, nbatch, d_x, x_stride, d_energy, d_grad, grad_stride, d_vals, vals_stride, flags, stream,
+                         d_params);
 }
 
 bsf_status bsf_eval_energy(bsf_handle h, const double* d_x, double* d_energy, int flags, bsf_stream stream) {

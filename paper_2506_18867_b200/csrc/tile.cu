@@ -20,7 +20,6 @@
 
 #include <algorithm>
 #include <cmath>
-#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -71,14 +70,9 @@ struct TileArgs {
   const unsigned long long* ent;
   const int32_t* row_ptr;
   const int2* chunks;      // (ra, rb) per chunk of this launch
-  const int4* sb_hdr;      // kernel 2: [nprog][13] single-block task headers
-  const uint32_t* sb_ent;  // kernel 2: packed entries
-  const int* sched;        // kernel 2: [kW2][kSched] warp schedule
-  int estride;             // strips per chunk slot in e_part
-  const int16_t* laym;     // ring layout tables of this launch's strip width
-  const int16_t* layb;
-  const int32_t* rszm;
-  const int32_t* rszb;
+  const double* params;    // optional per-item [9]: G00 G01 G10 G11 detJ mu_st1 mu_st2 mu_sh mu_bd
+  double detJ_ref;         // det J the class weights were built with
+  int flags;
 };
 
 // point records in shared memory (array of structures, odd strides -> conflict-free 8-byte access)
@@ -104,39 +98,86 @@ __device__ __forceinline__ void warp_store_block(double* wb, const double (&blk)
   __syncwarp();
 }
 
+__global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x;
+  const int strip = blockIdx.x, chunk = A.chunk_base + blockIdx.y, item = blockIdx.z;
+  const int i0 = strip * kTX;
+  const int2 chr = A.chunks[blockIdx.y];
+  const int ra = chr.x, rb = chr.y;
+  const int slo = max(0, i0 - 2), shi = min(A.Su - 1, i0 + kTX - 1);
+  const double* __restrict__ x = A.x + item * A.xs;
 
+  // ---- shared memory carve-up
+  double* pos = reinterpret_cast<double*>(smem_raw);                   // [kPosRows][kPosCols][3]
+  double* pm = pos + kPosRows * kPosCols * 3;                          // [capm][kMS]
+  double* pb = pm + (int64_t)kMS * A.capm;                             // [capb][kBS]
+  double* wbuf = pb + (int64_t)kBS * A.capb;                           // [kThreads/32][288]
+  double* red = wbuf + (kThreads / 32) * 288;                          // [32]
+  int* astm = reinterpret_cast<int*>(red + 32);                        // [kRing][kAC]
+  int* astb = astm + kRing * kAC;                                      // [kRing][kAC]
 
-// ---- ring-row layout of the point pool.  Per anchor row: the first K points of every anchor column
-// in [idx][even columns | odd columns] order (lanes of a warp touch consecutive records ->
-// conflict-free shared memory), then the overflow points (boundary anchors only).  K = 2 membrane,
-// 1 bending.  ovf[ac] holds R + K*AC + (overflow prefix of ac) - K, so overflow slots are ovf + idx.
-__device__ __forceinline__ int pool_slot(int R, int AC, int K, int ac, int idx, int ovfbase, int cap) {
-  const int q = idx < K ? R + idx * AC + (ac & 1) * (AC >> 1) + (ac >> 1) : ovfbase + idx;
-  return wrap(q, cap);
-}
-
-// Lay out the new anchor rows of a step from the host-built tables: lay[(strip*Sv + t)*AC + ac] is
-// the overflow base of column ac relative to the row start, rsz[strip*Sv + t] the row size.  Every
-// thread advances the (uniform) ring heads; threads tid < AC write their column's base.
-template <int AC, int RS>
-__device__ __forceinline__ void ring_rows(const TileArgs& A, const int16_t* lay, const int32_t* rsz, int strip, int j0,
-                                          int cap, int* ovf, int* rowR, int& head, int tid) {
-#pragma unroll
-  for (int r = 0; r < RS; ++r) {
-    const int t = j0 + r;
-    const int rs = (t + 4) & 3;
-    const bool valid = (t >= 0 && t < A.Sv);
-    const int R = head;
-    if (tid < AC) ovf[rs * AC + tid] = R + (valid ? (int)lay[((int64_t)strip * A.Sv + t) * AC + tid] : 0);
-    if (tid == 0) rowR[rs] = R;
-    head = wrap(R + (valid ? rsz[(int64_t)strip * A.Sv + t] : 0), cap);
+  const bool want_h = A.vals != nullptr, want_g = A.g != nullptr;
+  double e_acc = 0.0;
+  // affine geometry and stiffness of this batch item (per-item parameters for batches of sheets)
+  double pG00 = A.G00, pG01 = A.G01, pG10 = A.G10, pG11 = A.G11, pdet = A.detJ;
+  double pmu1 = A.mu1, pmu2 = A.mu2, pmush = A.mush, pmubd = A.mubd;
+  if (A.params) {
+    const double* pp = A.params + 9 * (int64_t)item;
+    pG00 = pp[0]; pG01 = pp[1]; pG10 = pp[2]; pG11 = pp[3];
+    pdet = pp[4] / A.detJ_ref;
+    pmu1 = (A.flags & 2) ? 0.0 : pp[5];
+    pmu2 = (A.flags & 2) ? 0.0 : pp[6];
+    pmush = (A.flags & 2) ? 0.0 : pp[7];
+    pmubd = (A.flags & 4) ? 0.0 : pp[8];
   }
-}
+  int head_m = 0, head_b = 0;
 
-// ---- quadrature-point evaluation shared by both kernels (writes one point record)
-__device__ __forceinline__ void membrane_point(const TileArgs& A, int64_t p, double* rec, const double* pos,
-                                               int posCols, int t, int j0, int i0, int ra, int rb, int TX,
-                                               double& e_acc) {
+  for (int j0 = ra - 2; j0 < rb; j0 += kRS) {
+    // ---------------- 1. positions of cp rows j0 .. j0+kRS+1, cols i0-2 .. i0+kTX+1
+    for (int k = tid; k < kPosRows * kPosCols * 3; k += kThreads) {
+      const int row = k / (kPosCols * 3), rem = k - row * kPosCols * 3;
+      const int col = rem / 3, c = rem - col * 3;
+      const int R = j0 + row, Cc = i0 - 2 + col;
+      double v = 0.0;
+      if (R >= A.xlo && R < A.xhi && Cc >= 0 && Cc < A.n_u) v = x[((int64_t)(R - A.xlo) * A.n_u + Cc) * 3 + c];
+      pos[k] = v;
+    }
+    // ---------------- 2. ring bookkeeping for anchor rows j0, j0+1 (uniform in every thread)
+    int P0m[kRS], Nm[kRS], Hm[kRS], P0b[kRS], Nb[kRS], Hb[kRS];
+#pragma unroll
+    for (int r = 0; r < kRS; ++r) {
+      const int t = j0 + r;
+      const bool valid = (t >= 0 && t < A.Sv && slo <= shi);
+      P0m[r] = valid ? A.m_aoff[t * A.Su + slo] : 0;
+      Nm[r] = valid ? A.m_aoff[t * A.Su + shi + 1] - P0m[r] : 0;
+      P0b[r] = valid ? A.b_aoff[t * A.Su + slo] : 0;
+      Nb[r] = valid ? A.b_aoff[t * A.Su + shi + 1] - P0b[r] : 0;
+      Hm[r] = head_m;
+      Hb[r] = head_b;
+      head_m = wrap(head_m + Nm[r], A.capm);   // Nm <= capm
+      head_b = wrap(head_b + Nb[r], A.capb);
+      if (tid < kAC) {
+        const int s = i0 - 2 + tid, slot = (t + 4) & 3;
+        int sm = 0, sb = 0;
+        if (valid && s >= slo && s <= shi) {
+          sm = wrap(Hm[r] + (A.m_aoff[t * A.Su + s] - P0m[r]), A.capm);
+          sb = wrap(Hb[r] + (A.b_aoff[t * A.Su + s] - P0b[r]), A.capb);
+        }
+        astm[slot * kAC + tid] = sm;
+        astb[slot * kAC + tid] = sb;
+      }
+    }
+    __syncthreads();
+    // ---------------- 3. point phase
+    const int nmem = Nm[0] + Nm[1], ntot = nmem + Nb[0] + Nb[1];
+    for (int k = tid; k < ntot; k += kThreads) {
+      if (k < nmem) {
+        const int r = k < Nm[0] ? 0 : 1;
+        const int kk = r ? k - Nm[0] : k;
+        const int64_t p = P0m[r] + kk;
+        double* rec = pm + (int64_t)kMS * wrap(Hm[r] + kk, A.capm);
+        const int t = j0 + r;
         const uint2 info = A.m_info[p];
         const int ou = info.y >> 16;
         const double* tu = A.utab + (info.x & 0xFFFF) * 9;
@@ -158,12 +199,12 @@ __device__ __forceinline__ void membrane_point(const TileArgs& A, int64_t p, dou
             const double du = in ? dNu[iu] * Nv[jv] : 0.0, dv = in ? Nu[iu] * dNv[jv] : 0.0;
             rec[21 + 2 * e] = du;
             rec[22 + 2 * e] = dv;
-            const double* C = pos + ((t + jv - j0) * posCols + (ou + iu - (i0 - 2))) * 3;
+            const double* C = pos + ((t + jv - j0) * kPosCols + (ou + iu - (i0 - 2))) * 3;
 #pragma unroll
             for (int c = 0; c < 3; ++c) { Fu[c] = fma(C[c], du, Fu[c]); Fv[c] = fma(C[c], dv, Fv[c]); }
           }
         double G00, G01, G10, G11, w;
-        if (A.affine) { G00 = A.G00; G01 = A.G01; G10 = A.G10; G11 = A.G11; w = sh[0] * A.detJ; }
+        if (A.affine) { G00 = pG00; G01 = pG01; G10 = pG10; G11 = pG11; w = sh[0] * pdet; }
         else {
           G00 = A.m_geo[p]; G01 = A.m_geo[A.Mm + p]; G10 = A.m_geo[2 * A.Mm + p]; G11 = A.m_geo[3 * A.Mm + p];
           w = A.m_geo[4 * A.Mm + p];
@@ -172,8 +213,8 @@ __device__ __forceinline__ void membrane_point(const TileArgs& A, int64_t p, dou
 #pragma unroll
         for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * G00 + Fv[c] * G10; f2[c] = Fu[c] * G01 + Fv[c] * G11; }
         FSpace o;
-        fbw_point(f1, f2, A.mu1, A.mu2, A.mush, A.project != 0, o);
-        if (ou >= i0 && ou < i0 + TX && t >= ra && t < rb) e_acc += w * o.psi;
+        fbw_point(f1, f2, pmu1, pmu2, pmush, A.project != 0, o);
+        if (ou >= i0 && ou < i0 + kTX && t >= ra && t < rb) e_acc += w * o.psi;
         // P~_mu = w sum_beta G_mu,beta P_beta
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -200,11 +241,13 @@ __device__ __forceinline__ void membrane_point(const TileArgs& A, int64_t p, dou
           for (int c3 = 0; c3 < 3; ++c3)
             rec[12 + 3 * r3 + c3] =
                 c11 * o.A11[sym3(r3, c3)] + c12 * o.A12[3 * r3 + c3] + c21 * o.A12[3 * c3 + r3] + c22 * o.A22[sym3(r3, c3)];
-}
-
-__device__ __forceinline__ void bending_point(const TileArgs& A, int64_t p, double* rec, const double* pos,
-                                              int posCols, int t, int j0, int i0, int ra, int rb, int TX,
-                                              double& e_acc) {
+      } else {
+        const int kb = k - nmem;
+        const int r = kb < Nb[0] ? 0 : 1;
+        const int kk = r ? kb - Nb[0] : kb;
+        const int64_t p = P0b[r] + kk;
+        double* rec = pb + (int64_t)kBS * wrap(Hb[r] + kk, A.capb);
+        const int t = j0 + r;
         const uint2 info = A.b_info[p];
         const int ou = info.y >> 16;
         const double* tu = A.utab + (info.x & 0xFFFF) * 9;
@@ -212,17 +255,17 @@ __device__ __forceinline__ void bending_point(const TileArgs& A, int64_t p, doub
         const double* sh = A.stab + (info.y & 0xFFFF) * 2;
         double cuu, cvv, cuv, cu, cv, w;
         if (A.affine) {
-          cuu = A.G00 * A.G00 + A.G01 * A.G01;
-          cvv = A.G10 * A.G10 + A.G11 * A.G11;
-          cuv = 2.0 * (A.G00 * A.G10 + A.G01 * A.G11);
+          cuu = pG00 * pG00 + pG01 * pG01;
+          cvv = pG10 * pG10 + pG11 * pG11;
+          cuv = 2.0 * (pG00 * pG10 + pG01 * pG11);
           cu = 0.0; cv = 0.0;
-          w = sh[0] * A.detJ;
+          w = sh[0] * pdet;
         } else {
           w = A.b_geo[p]; cuu = A.b_geo[A.Bm + p]; cvv = A.b_geo[2 * A.Bm + p]; cuv = A.b_geo[3 * A.Bm + p];
           cu = A.b_geo[4 * A.Bm + p]; cv = A.b_geo[5 * A.Bm + p];
         }
         const int mask = (int)sh[1];
-        const double sw = sqrt(w * A.mubd);
+        const double sw = sqrt(w * pmubd);
         double lap[3] = {0, 0, 0};
 #pragma unroll
         for (int jv = 0; jv < 3; ++jv)
@@ -234,88 +277,16 @@ __device__ __forceinline__ void bending_point(const TileArgs& A, int64_t p, doub
               // Eq. `eq: Laplacian in parametric space`
               L = cuu * tu[6 + iu] * tv[jv] + cvv * tu[iu] * tv[6 + jv] + cuv * tu[3 + iu] * tv[3 + jv] +
                   cu * tu[3 + iu] * tv[jv] + cv * tu[iu] * tv[3 + jv];
-              const double* C = pos + ((t + jv - j0) * posCols + (ou + iu - (i0 - 2))) * 3;
+              const double* C = pos + ((t + jv - j0) * kPosCols + (ou + iu - (i0 - 2))) * 3;
               lap[0] += L * C[0]; lap[1] += L * C[1]; lap[2] += L * C[2];
             }
             rec[e] = sw * L;
           }
-        if (ou >= i0 && ou < i0 + TX && t >= ra && t < rb)
-          e_acc += 0.5 * w * A.mubd * (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
+        if (ou >= i0 && ou < i0 + kTX && t >= ra && t < rb)
+          e_acc += 0.5 * w * pmubd * (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
         rec[9] = sw * lap[0];
         rec[10] = sw * lap[1];
         rec[11] = sw * lap[2];
-      
-}
-
-__global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tid = threadIdx.x;
-  const int strip = blockIdx.x, chunk = A.chunk_base + blockIdx.y, item = blockIdx.z;
-  const int i0 = strip * kTX;
-  const int2 chr = A.chunks[blockIdx.y];
-  const int ra = chr.x, rb = chr.y;
-  const int slo = max(0, i0 - 2), shi = min(A.Su - 1, i0 + kTX - 1);
-  const double* __restrict__ x = A.x + item * A.xs;
-
-  // ---- shared memory carve-up
-  double* pos = reinterpret_cast<double*>(smem_raw);                   // [kPosRows][kPosCols][3]
-  double* pm = pos + kPosRows * kPosCols * 3;                          // [capm][kMS]
-  double* pb = pm + (int64_t)kMS * A.capm;                             // [capb][kBS]
-  double* wbuf = pb + (int64_t)kBS * A.capb;                           // [kThreads/32][288]
-  double* red = wbuf + (kThreads / 32) * 288;                          // [32]
-  int* astm = reinterpret_cast<int*>(red + 32);                        // [kRing][kAC]
-  int* astb = astm + kRing * kAC;                                      // [kRing][kAC]
-  int* rowRm = astb + kRing * kAC;                                     // [4] ring-row bases
-  int* rowRb = rowRm + 4;
-  int head_m = 0, head_b = 0;
-
-  const bool want_h = A.vals != nullptr, want_g = A.g != nullptr;
-  double e_acc = 0.0;
-
-  for (int j0 = ra - 2; j0 < rb; j0 += kRS) {
-    // ---------------- 1. positions of cp rows j0 .. j0+kRS+1, cols i0-2 .. i0+kTX+1
-    for (int k = tid; k < kPosRows * kPosCols * 3; k += kThreads) {
-      const int row = k / (kPosCols * 3), rem = k - row * kPosCols * 3;
-      const int col = rem / 3, c = rem - col * 3;
-      const int R = j0 + row, Cc = i0 - 2 + col;
-      double v = 0.0;
-      if (R >= A.xlo && R < A.xhi && Cc >= 0 && Cc < A.n_u) v = x[((int64_t)(R - A.xlo) * A.n_u + Cc) * 3 + c];
-      pos[k] = v;
-    }
-    // ---------------- 2. ring bookkeeping for anchor rows j0, j0+1 (uniform in every thread)
-    int P0m[kRS], Nm[kRS], P0b[kRS], Nb[kRS];
-#pragma unroll
-    for (int r = 0; r < kRS; ++r) {
-      const int t = j0 + r;
-      const bool valid = (t >= 0 && t < A.Sv && slo <= shi);
-      P0m[r] = valid ? A.m_aoff[t * A.Su + slo] : 0;
-      Nm[r] = valid ? A.m_aoff[t * A.Su + shi + 1] - P0m[r] : 0;
-      P0b[r] = valid ? A.b_aoff[t * A.Su + slo] : 0;
-      Nb[r] = valid ? A.b_aoff[t * A.Su + shi + 1] - P0b[r] : 0;
-    }
-    ring_rows<kAC, kRS>(A, A.laym, A.rszm, strip, j0, A.capm, astm, rowRm, head_m, tid);
-    ring_rows<kAC, kRS>(A, A.layb, A.rszb, strip, j0, A.capb, astb, rowRb, head_b, tid);
-    __syncthreads();
-    // ---------------- 3. point phase
-    const int nmem = Nm[0] + Nm[1], ntot = nmem + Nb[0] + Nb[1];
-    for (int k = tid; k < ntot; k += kThreads) {
-      if (k < nmem) {
-        const int r = k < Nm[0] ? 0 : 1;
-        const int kk = r ? k - Nm[0] : k;
-        const int64_t p = P0m[r] + kk;
-        const int t = j0 + r, ou = A.m_info[p].y >> 16, ac = ou - (i0 - 2), rs = (t + 4) & 3;
-        const int idx = (int)(p - A.m_aoff[t * A.Su + ou]);
-        double* rec = pm + (int64_t)kMS * pool_slot(rowRm[rs], kAC, 2, ac, idx, astm[rs * kAC + ac], A.capm);
-        membrane_point(A, p, rec, pos, kPosCols, t, j0, i0, ra, rb, kTX, e_acc);
-      } else {
-        const int kb = k - nmem;
-        const int r = kb < Nb[0] ? 0 : 1;
-        const int kk = r ? kb - Nb[0] : kb;
-        const int64_t p = P0b[r] + kk;
-        const int t = j0 + r, ou = A.b_info[p].y >> 16, ac = ou - (i0 - 2), rs = (t + 4) & 3;
-        const int idx = (int)(p - A.b_aoff[t * A.Su + ou]);
-        double* rec = pb + (int64_t)kBS * pool_slot(rowRb[rs], kAC, 1, ac, idx, astb[rs * kAC + ac], A.capb);
-        bending_point(A, p, rec, pos, kPosCols, t, j0, i0, ra, rb, kTX, e_acc);
       }
     }
     __syncthreads();
@@ -362,8 +333,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
             const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
             const int t = j - 2 + dt;
             if (t >= anchor_min) {
-              const int rs = (t + 4) & 3, ac = c + dc;
-            const double* rec = pm + kMS * pool_slot(rowRm[rs], kAC, 2, ac, idx, astm[rs * kAC + ac], A.capm);
+              const double* rec = pm + kMS * wrap(astm[((t + 4) & 3) * kAC + c + dc] + idx, A.capm);
               const double da1 = rec[21 + 2 * la], da2 = rec[22 + 2 * la];
               double Am[21];
 #pragma unroll
@@ -401,8 +371,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
             const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
             const int t = j - 2 + dt;
             if (t >= anchor_min) {
-              const int rs = (t + 4) & 3, ac = c + dc;
-            const double* rec = pb + kBS * pool_slot(rowRb[rs], kAC, 1, ac, idx, astb[rs * kAC + ac], A.capb);
+              const double* rec = pb + kBS * wrap(astb[((t + 4) & 3) * kAC + c + dc] + idx, A.capb);
               const double La = rec[la];
               const int lb0 = (E >> 13) & 15, lb1 = (E >> 17) & 15, lb2 = (E >> 21) & 15;
               dg0 = fma(La, lb0 != 15 ? rec[lb0 != 15 ? lb0 : 0] : 0.0, dg0);
@@ -456,8 +425,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
             const unsigned long long E = __ldg(ent + e);
             const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
             const int t = j - 2 + dt;
-            const int rs = (t + 4) & 3, ac = c + dc;
-            const double* rec = pm + kMS * pool_slot(rowRm[rs], kAC, 2, ac, idx, astm[rs * kAC + ac], A.capm);
+            const double* rec = pm + kMS * wrap(astm[((t + 4) & 3) * kAC + c + dc] + idx, A.capm);
             const double da1 = rec[21 + 2 * la], da2 = rec[22 + 2 * la];
             g0 = fma(da1, rec[39], fma(da2, rec[42], g0));
             g1 = fma(da1, rec[40], fma(da2, rec[43], g1));
@@ -470,8 +438,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
             const unsigned long long E = __ldg(entb + e);
             const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
             const int t = j - 2 + dt;
-            const int rs = (t + 4) & 3, ac = c + dc;
-            const double* rec = pb + kBS * pool_slot(rowRb[rs], kAC, 1, ac, idx, astb[rs * kAC + ac], A.capb);
+            const double* rec = pb + kBS * wrap(astb[((t + 4) & 3) * kAC + c + dc] + idx, A.capb);
             const double La = rec[la];
             g0 = fma(La, rec[9], g0);
             g1 = fma(La, rec[10], g1);
@@ -493,229 +460,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
   if (tid == 0) {
     double s = 0.0;
     for (int w = 0; w < kThreads / 32; ++w) s += red[w];
-    A.epart[((int64_t)item * A.nchunks_total + chunk) * A.estride + strip] = s;
-  }
-}
-
-
-// =============================================================================================
-// Kernel 2 (interior chunks): 32-column strips, single-block gather tasks with parity-uniform warps.
-// A warp-task = one forward block offset k (or the gradient) for the 32 control points of one
-// parity in the step (2 rows x 16 columns); heavy blocks (the diagonal row block) are split
-// between the two lane halves of a warp covering 16 control points.  Warps walk a host-built,
-// load-balanced schedule.  Every lane of an interior warp-task runs the same program, so loops
-// are uniform and each entry is one point's A~ contracted into one 3x3 block (36 DFMA).
-constexpr int kTX2 = 32, kRS2 = 2, kRing2 = 4, kW2 = 16, kThreads2 = 32 * kW2, kSched = 4;
-constexpr int kPosCols2 = kTX2 + 4, kPosRows2 = kRS2 + 2, kAC2 = kTX2 + 2;
-__constant__ int c_off_di[13] = {0, 1, 2, -2, -1, 0, 1, 2, -2, -1, 0, 1, 2};
-__constant__ int c_off_dj[13] = {0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 2};
-
-__global__ void __launch_bounds__(kThreads2, 1) k_tile2(const TileArgs A) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tid = threadIdx.x;
-  const int strip = blockIdx.x, chunk = A.chunk_base + blockIdx.y, item = blockIdx.z;
-  const int i0 = strip * kTX2;
-  const int2 chr = A.chunks[blockIdx.y];
-  const int ra = chr.x, rb = chr.y;
-  const int slo = max(0, i0 - 2), shi = min(A.Su - 1, i0 + kTX2 - 1);
-  const double* __restrict__ x = A.x + item * A.xs;
-
-  double* pos = reinterpret_cast<double*>(smem_raw);                   // [kPosRows2][kPosCols2][3]
-  double* pm = pos + kPosRows2 * kPosCols2 * 3;                        // [capm][kMS]
-  double* pb = pm + (int64_t)kMS * A.capm;                             // [capb][kBS]
-  double* wbuf = pb + (int64_t)kBS * A.capb;                           // [kW2][288]
-  double* red = wbuf + kW2 * 288;                                      // [32]
-  int* astm = reinterpret_cast<int*>(red + 32);                        // [kRing2][kAC2]
-  int* astb = astm + kRing2 * kAC2;
-  int* rowRm = astb + kRing2 * kAC2;
-  int* rowRb = rowRm + 4;
-  int* sched = rowRb + 4;                                              // [kW2][kSched]
-  int head_m = 0, head_b = 0;
-  if (tid < kW2 * kSched) sched[tid] = A.sched[tid];
-
-  const bool want_h = A.vals != nullptr, want_g = A.g != nullptr;
-  double e_acc = 0.0;
-
-  for (int j0 = ra - 2; j0 < rb; j0 += kRS2) {
-    for (int k = tid; k < kPosRows2 * kPosCols2 * 3; k += kThreads2) {
-      const int row = k / (kPosCols2 * 3), rem = k - row * kPosCols2 * 3;
-      const int col = rem / 3, c = rem - col * 3;
-      const int R = j0 + row, Cc = i0 - 2 + col;
-      double v = 0.0;
-      if (R >= A.xlo && R < A.xhi && Cc >= 0 && Cc < A.n_u) v = x[((int64_t)(R - A.xlo) * A.n_u + Cc) * 3 + c];
-      pos[k] = v;
-    }
-    int P0m[kRS2], Nm[kRS2], P0b[kRS2], Nb[kRS2];
-#pragma unroll
-    for (int r = 0; r < kRS2; ++r) {
-      const int t = j0 + r;
-      const bool valid = (t >= 0 && t < A.Sv && slo <= shi);
-      P0m[r] = valid ? A.m_aoff[t * A.Su + slo] : 0;
-      Nm[r] = valid ? A.m_aoff[t * A.Su + shi + 1] - P0m[r] : 0;
-      P0b[r] = valid ? A.b_aoff[t * A.Su + slo] : 0;
-      Nb[r] = valid ? A.b_aoff[t * A.Su + shi + 1] - P0b[r] : 0;
-    }
-    ring_rows<kAC2, kRS2>(A, A.laym, A.rszm, strip, j0, A.capm, astm, rowRm, head_m, tid);
-    ring_rows<kAC2, kRS2>(A, A.layb, A.rszb, strip, j0, A.capb, astb, rowRb, head_b, tid);
-    __syncthreads();
-    const int nmem = Nm[0] + Nm[1], ntot = nmem + Nb[0] + Nb[1];
-    for (int k = tid; k < ntot; k += kThreads2) {
-      if (k < nmem) {
-        const int r = k < Nm[0] ? 0 : 1;
-        const int kk = r ? k - Nm[0] : k;
-        const int64_t p = P0m[r] + kk;
-        const int t = j0 + r, ou = A.m_info[p].y >> 16, ac = ou - (i0 - 2), rs = (t + 4) & 3;
-        const int idx = (int)(p - A.m_aoff[t * A.Su + ou]);
-        double* rec = pm + (int64_t)kMS * pool_slot(rowRm[rs], kAC2, 2, ac, idx, astm[rs * kAC2 + ac], A.capm);
-        membrane_point(A, p, rec, pos, kPosCols2, t, j0, i0, ra, rb, kTX2, e_acc);
-      } else {
-        const int kb = k - nmem;
-        const int r = kb < Nb[0] ? 0 : 1;
-        const int kk = r ? kb - Nb[0] : kb;
-        const int64_t p = P0b[r] + kk;
-        const int t = j0 + r, ou = A.b_info[p].y >> 16, ac = ou - (i0 - 2), rs = (t + 4) & 3;
-        const int idx = (int)(p - A.b_aoff[t * A.Su + ou]);
-        double* rec = pb + (int64_t)kBS * pool_slot(rowRb[rs], kAC2, 1, ac, idx, astb[rs * kAC2 + ac], A.capb);
-        bending_point(A, p, rec, pos, kPosCols2, t, j0, i0, ra, rb, kTX2, e_acc);
-      }
-    }
-    __syncthreads();
-    const bool halo_step = (j0 < ra);
-    if (halo_step && !(ra == A.r0 && A.r0 > 0)) continue;
-    const int warp = tid >> 5, lane = tid & 31;
-    const int anchor_min = max(0, ra - 2);
-    for (int si = 0; si < kSched; ++si) {
-      const int code = sched[warp * kSched + si];
-      if (code < 0) break;
-      const int k = code & 15, split = (code >> 4) & 1, hsel = (code >> 5) & 1, par = (code >> 6) & 1;
-      const int cpi = split ? 16 * hsel + (lane & 15) : lane;
-      const int part = split ? (lane >> 4) : 0;
-      const int r = cpi >> 4, cc = cpi & 15;
-      const int c = 2 * cc + ((j0 + r + par) & 1);
-      const int i = i0 + c, j = j0 + r;
-      const bool owned_row = (j >= A.r0);
-      bool active = (i < A.n_u) && (j < rb) && (j >= 0);
-      const bool grad = (k == 13);
-      if (grad || k == 0) active = active && owned_row;
-      active = active && (grad ? want_g : want_h);
-      int pid = 0;
-      if (active) pid = A.lut[(bclass(i, A.n_u) * kNCls + bclass(j, A.n_v)) * 2 + ((i + j) & 1)];
-      const int a_loc = (j - A.r0) * A.n_u + i;
-      if (grad) {
-        const int4 h0 = active ? A.tasks[(pid * kTasks + 5) * 2] : make_int4(0, 0, 0, 0);
-        const int n_m = active ? (h0.y & 0xFFFF) : 0, n_b = active ? (h0.y >> 16) : 0;
-        const int nmax_m = __reduce_max_sync(0xffffffffu, n_m), nmax_b = __reduce_max_sync(0xffffffffu, n_b);
-        const unsigned long long* ent = A.ent + h0.x;
-        double g0 = 0.0, g1 = 0.0, g2 = 0.0;
-        for (int e = 0; e < nmax_m; ++e) {
-          if (e < n_m) {
-            const unsigned long long E = __ldg(ent + e);
-            const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
-            const int t = j - 2 + dt;
-            const int rs = (t + 4) & 3, ac = c + dc;
-            const double* rec = pm + kMS * pool_slot(rowRm[rs], kAC2, 2, ac, idx, astm[rs * kAC2 + ac], A.capm);
-            const double da1 = rec[21 + 2 * la], da2 = rec[22 + 2 * la];
-            g0 = fma(da1, rec[39], fma(da2, rec[42], g0));
-            g1 = fma(da1, rec[40], fma(da2, rec[43], g1));
-            g2 = fma(da1, rec[41], fma(da2, rec[44], g2));
-          }
-        }
-        for (int e = 0; e < nmax_b; ++e) {
-          if (e < n_b) {
-            const unsigned long long E = __ldg(ent + n_m + e);
-            const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
-            const int t = j - 2 + dt;
-            const int rs = (t + 4) & 3, ac = c + dc;
-            const double* rec = pb + kBS * pool_slot(rowRb[rs], kAC2, 1, ac, idx, astb[rs * kAC2 + ac], A.capb);
-            const double La = rec[la];
-            g0 = fma(La, rec[9], g0);
-            g1 = fma(La, rec[10], g1);
-            g2 = fma(La, rec[11], g2);
-          }
-        }
-        if (active) {
-          double* gd = A.g + item * A.gs + 3 * (int64_t)a_loc;
-          gd[0] = g0; gd[1] = g1; gd[2] = g2;
-        }
-        continue;
-      }
-      const int4 hd = active ? A.sb_hdr[pid * 13 + k] : make_int4(0, 0, 0, 0);
-      const bool exists = active && ((hd.z >> 16) & 1);
-      const int n_m = exists ? (hd.y & 0xFFFF) : 0, n_b = exists ? (hd.y >> 16) : 0;
-      const int nmax_m = __reduce_max_sync(0xffffffffu, n_m), nmax_b = __reduce_max_sync(0xffffffffu, n_b);
-      if (__reduce_or_sync(0xffffffffu, exists ? 1u : 0u) == 0u) continue;
-      const uint32_t* ent = A.sb_ent + hd.x;
-      const int estep = split ? 2 : 1;
-      double acc[9];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) acc[q] = 0.0;
-      for (int e = part; e < nmax_m; e += estep) {
-        if (e < n_m) {
-          const uint32_t E = __ldg(ent + e);
-          const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 4) & 15, la = (E >> 8) & 15, lb = (E >> 12) & 15;
-          const int t = j - 2 + dt;
-          if (t >= anchor_min) {
-            const int rs = (t + 4) & 3, ac = c + dc;
-            const double* rec = pm + kMS * pool_slot(rowRm[rs], kAC2, 2, ac, idx, astm[rs * kAC2 + ac], A.capm);
-            const double da1 = rec[21 + 2 * la], da2 = rec[22 + 2 * la];
-            const double db1 = rec[21 + 2 * lb], db2 = rec[22 + 2 * lb];
-            const double k11 = da1 * db1, k22 = da2 * db2, k12 = da1 * db2, k21 = da2 * db1;
-#pragma unroll
-            for (int r3 = 0; r3 < 3; ++r3)
-#pragma unroll
-              for (int c3 = 0; c3 < 3; ++c3) {
-                double v = acc[3 * r3 + c3];
-                v = fma(k11, rec[sym3(r3, c3)], v);
-                v = fma(k22, rec[6 + sym3(r3, c3)], v);
-                v = fma(k12, rec[12 + 3 * r3 + c3], v);
-                v = fma(k21, rec[12 + 3 * c3 + r3], v);
-                acc[3 * r3 + c3] = v;
-              }
-          }
-        }
-      }
-      double dg = 0.0;
-      for (int e = part; e < nmax_b; e += estep) {
-        if (e < n_b) {
-          const uint32_t E = __ldg(ent + n_m + e);
-          const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 4) & 15, la = (E >> 8) & 15, lb = (E >> 12) & 15;
-          const int t = j - 2 + dt;
-          if (t >= anchor_min) {
-            const int rs = (t + 4) & 3, ac = c + dc;
-            const double* rec = pb + kBS * pool_slot(rowRb[rs], kAC2, 1, ac, idx, astb[rs * kAC2 + ac], A.capb);
-            dg = fma(rec[la], rec[lb], dg);
-          }
-        }
-      }
-      acc[0] += dg; acc[4] += dg; acc[8] += dg;
-      if (split) {
-#pragma unroll
-        for (int q = 0; q < 9; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], 16);
-      }
-      const int di = c_off_di[k], dj = c_off_dj[k];
-      const int kab = hd.z & 0xFF, kba = (hd.z >> 8) & 0xFF;
-      const int jb = j + dj;
-      double* vals = A.vals + item * A.vs;
-      const int pf = (exists && owned_row) ? A.row_ptr[a_loc] + kab : -1;
-      int pt = -1;
-      if (exists && k != 0 && jb >= A.r0 && jb < A.r1) pt = A.row_ptr[a_loc + di + dj * A.n_u] + kba;
-      double* wb = wbuf + warp * 288;
-      if (split) {
-        warp_store_block(wb, acc, part == 1, part ? pt : pf, vals, lane);
-      } else {
-        warp_store_block(wb, acc, false, pf, vals, lane);
-        if (k != 0) warp_store_block(wb, acc, true, pt, vals, lane);
-      }
-    }
-    __syncthreads();
-  }
-  for (int o = 16; o > 0; o >>= 1) e_acc += __shfl_xor_sync(0xffffffffu, e_acc, o);
-  if ((tid & 31) == 0) red[tid >> 5] = e_acc;
-  __syncthreads();
-  if (tid == 0) {
-    double s = 0.0;
-    for (int w = 0; w < kW2; ++w) s += red[w];
-    A.epart[((int64_t)item * A.nchunks_total + chunk) * A.estride + strip] = s;
+    A.epart[((int64_t)item * A.nchunks_total + chunk) * A.nstrips + strip] = s;
   }
 }
 
@@ -808,6 +553,7 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
     tt.G[0] = ref.G[0][0]; tt.G[1] = ref.G[0][1]; tt.G[2] = ref.G[1][0]; tt.G[3] = ref.G[1][1];
     tt.detJ = 1.0;
   }
+  tt.detJ_ref = detJ_ref;
   std::vector<double> m_geo, b_geo;
   if (!sh.affine) {
     const size_t M = sh.mem.size(), B = sh.bend.size();
@@ -837,65 +583,12 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
       cb[t] = std::max(cb[t], b_aoff[t * Su + shi + 1] - b_aoff[t * Su + slo]);
     }
   }
-  // ring row sizes (permuted layout): K*AC structured slots + overflow of anchors with > K points
-  auto row_sizes = [&](int TXw, std::vector<int>& szm, std::vector<int>& szb) {
-    const int AC = TXw + 2, ns = (nu + TXw - 1) / TXw;
-    szm.assign(Sv, 0);
-    szb.assign(Sv, 0);
-    for (int st = 0; st < ns; ++st) {
-      const int i0 = st * TXw, slo = std::max(0, i0 - 2), shi = std::min(Su - 1, i0 + TXw - 1);
-      if (slo > shi) continue;
-      for (int t = 0; t < Sv; ++t) {
-        int om = 0, ob = 0;
-        for (int s2 = slo; s2 <= shi; ++s2) {
-          om += std::max(0, m_aoff[t * Su + s2 + 1] - m_aoff[t * Su + s2] - 2);
-          ob += std::max(0, b_aoff[t * Su + s2 + 1] - b_aoff[t * Su + s2] - 1);
-        }
-        szm[t] = std::max(szm[t], 2 * AC + om);
-        szb[t] = std::max(szb[t], AC + ob);
-      }
-    }
-  };
-  // per-(strip, anchor row) layout tables for both strip widths (kernel 1: kTX, kernel 2: kTX2)
-  auto layout = [&](int TXw, std::vector<int16_t>& lm, std::vector<int16_t>& lb, std::vector<int32_t>& zm,
-                    std::vector<int32_t>& zb) {
-    const int AC = TXw + 2, ns = (nu + TXw - 1) / TXw;
-    lm.assign((size_t)ns * Sv * AC, 0); lb.assign((size_t)ns * Sv * AC, 0);
-    zm.assign((size_t)ns * Sv, 0); zb.assign((size_t)ns * Sv, 0);
-    for (int st = 0; st < ns; ++st) {
-      const int i0 = st * TXw, slo = std::max(0, i0 - 2), shi = std::min(Su - 1, i0 + TXw - 1);
-      for (int t = 0; t < Sv; ++t) {
-        int om = 0, ob = 0;
-        for (int ac = 0; ac < AC; ++ac) {
-          const int s2 = i0 - 2 + ac;
-          int cmn = 0, cbn = 0;
-          if (slo <= shi && s2 >= slo && s2 <= shi) {
-            cmn = m_aoff[t * Su + s2 + 1] - m_aoff[t * Su + s2];
-            cbn = b_aoff[t * Su + s2 + 1] - b_aoff[t * Su + s2];
-          }
-          lm[((size_t)st * Sv + t) * AC + ac] = (int16_t)(2 * AC + om - 2);
-          lb[((size_t)st * Sv + t) * AC + ac] = (int16_t)(AC + ob - 1);
-          om += std::max(0, cmn - 2);
-          ob += std::max(0, cbn - 1);
-        }
-        zm[(size_t)st * Sv + t] = 2 * AC + om;
-        zb[(size_t)st * Sv + t] = AC + ob;
-      }
-    }
-  };
-  std::vector<int16_t> lay1m, lay1b, lay2m, lay2b;
-  std::vector<int32_t> rsz1m, rsz1b, rsz2m, rsz2b;
-  layout(kTX, lay1m, lay1b, rsz1m, rsz1b);
-  layout(kTX2, lay2m, lay2b, rsz2m, rsz2b);
-  std::vector<int> szm1, szb1;
-  row_sizes(kTX, szm1, szb1);
-  (void)cm; (void)cb;
   auto ring_need = [&](int ra, int rb, int& pm_, int& pb_) {   // pool need of one chunk
     pm_ = 1; pb_ = 1;
     for (int j0 = ra - 2; j0 < rb; j0 += kRS) {
       int sm = 0, sb = 0;
       for (int t = j0 - 2; t <= j0 + 1; ++t)
-        if (t >= 0 && t < Sv) { sm += szm1[t]; sb += szb1[t]; }
+        if (t >= 0 && t < Sv) { sm += cm[t]; sb += cb[t]; }
       pm_ = std::max(pm_, sm);
       pb_ = std::max(pb_, sb);
     }
@@ -935,7 +628,7 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
     tt.nch_l[L] = (int)cl[L].size();
     tt.smem_l[L] = sizeof(double) * (kPosRows * kPosCols * 3 + (size_t)kMS * capm + (size_t)kBS * capb +
                                      (kThreads / 32) * 288 + 32) +
-                   sizeof(int) * (2 * kRing * kAC + 16);
+                   sizeof(int) * (2 * kRing * kAC);
     if (!cl[L].empty() && tt.smem_l[L] > 227 * 1024) return 1;
   }
   std::vector<int2> chunks(cl[0]);
@@ -988,8 +681,6 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
   std::vector<int16_t> lut(kNCls * kNCls * 2, -1);
   std::vector<int4> tasks;
   std::vector<unsigned long long> ents;
-  std::vector<int4> sb_hdr;
-  std::vector<uint32_t> sb_ents;
   auto build_prog = [&](int i, int j) {
     const std::vector<int> ca = row_cols(i, j);
     const int a = j * nu + i;
@@ -1056,53 +747,6 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
           }
         }
     }
-    // single-block programs (kernel 2): 13 forward offsets
-    {
-      static const int odi[13] = {0, 1, 2, -2, -1, 0, 1, 2, -2, -1, 0, 1, 2};
-      static const int odj[13] = {0, 0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 2};
-      for (int k = 0; k < 13; ++k) {
-        int4 hd = make_int4((int)sb_ents.size(), 0, 0, 0);
-        const int di = odi[k], dj = odj[k];
-        const int b = (j + dj) * nu + i + di;
-        bool exists = (i + di >= 0 && i + di < nu && j + dj < sh.n_v);
-        int kk = 0, kb = 0;
-        if (exists) {
-          kk = (int)(std::lower_bound(ca.begin(), ca.end(), b) - ca.begin());
-          exists = (kk < (int)ca.size() && ca[kk] == b);
-        }
-        if (exists) {
-          const std::vector<int> cb = row_cols(b % nu, b / nu);
-          kb = (int)(std::lower_bound(cb.begin(), cb.end(), a) - cb.begin());
-          if (kb >= (int)cb.size() || cb[kb] != a || kk > 255 || kb > 255) return false;
-          std::vector<uint32_t> lm, lbn;
-          for (int kind = 0; kind < 2; ++kind) {
-            const std::vector<int32_t>& aoff = kind ? b_aoff : m_aoff;
-            const std::vector<int>& ord = kind ? b_ord : m_ord;
-            const std::vector<Point>& P = kind ? sh.bend : sh.mem;
-            for (int dt = 0; dt < 3; ++dt)
-              for (int dc = 0; dc < 3; ++dc) {
-                const int t = j - 2 + dt, s2 = i - 2 + dc;
-                if (t < 0 || t >= Sv || s2 < 0 || s2 >= Su) continue;
-                const int an = t * Su + s2;
-                for (int idx = 0; idx < aoff[an + 1] - aoff[an]; ++idx) {
-                  const Point& p = P[ord[aoff[an] + idx]];
-                  const int la = (i - s2) + 3 * (j - t), ib = b % nu - s2, jb = b / nu - t;
-                  if (!((p.mask >> la) & 1)) continue;
-                  if (ib < 0 || ib > 2 || jb < 0 || jb > 2 || !((p.mask >> (ib + 3 * jb)) & 1)) continue;
-                  const uint32_t E = (uint32_t)dt | ((uint32_t)dc << 2) | ((uint32_t)idx << 4) | ((uint32_t)la << 8) |
-                                     ((uint32_t)(ib + 3 * jb) << 12);
-                  (kind ? lbn : lm).push_back(E);
-                }
-              }
-          }
-          hd.y = (int)lm.size() | ((int)lbn.size() << 16);
-          hd.z = kk | (kb << 8) | (1 << 16);
-          sb_ents.insert(sb_ents.end(), lm.begin(), lm.end());
-          sb_ents.insert(sb_ents.end(), lbn.begin(), lbn.end());
-        }
-        sb_hdr.push_back(hd);
-      }
-    }
     for (int tk = 0; tk < kTasks; ++tk) {
       int4 h0, h1;
       h0.x = (int)ents.size();
@@ -1139,64 +783,6 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
       if (!build_prog(i, j)) return 1;
     }
   }
-  // ---- kernel 2 (interior chunks): pool capacities for 32-column strips and the warp schedule,
-  // balanced with the interior class's entry counts (cost ~ 70 instructions per membrane entry,
-  // 6 per bending entry, 130 per block written).
-  {
-    tt.nstrips2 = (nu + kTX2 - 1) / kTX2;
-    std::vector<int> cm2, cb2;
-    row_sizes(kTX2, cm2, cb2);
-    int capm = 1, capb = 1;
-    for (const int2& ch : cl[0])
-      for (int j0 = ch.x - 2; j0 < ch.y; j0 += kRS2) {
-        int sm = 0, sb = 0;
-        for (int t = j0 - 2; t <= j0 + 1; ++t)
-          if (t >= 0 && t < Sv) { sm += cm2[t]; sb += cb2[t]; }
-        capm = std::max(capm, sm);
-        capb = std::max(capb, sb);
-      }
-    tt.capm2 = capm;
-    tt.capb2 = capb;
-    tt.smem2 = sizeof(double) * (kPosRows2 * kPosCols2 * 3 + (size_t)kMS * capm + (size_t)kBS * capb + kW2 * 288 + 32) +
-               sizeof(int) * (2 * kRing2 * kAC2 + kW2 * kSched + 16);
-    // interior class (or the most common class) decides the balance
-    int rep = -1;
-    const int key_int = (6 * kNCls + 6) * 2;
-    if (lut[key_int] >= 0) rep = lut[key_int];
-    std::vector<std::pair<double, int>> items;   // (cost, code)
-    for (int par = 0; par < 2; ++par) {
-      for (int k = 0; k < 13; ++k) {
-        double nmv = 4, nbv = 4;
-        if (rep >= 0) {
-          const int pr = (par == 0) ? lut[key_int] : (lut[key_int + 1] >= 0 ? lut[key_int + 1] : lut[key_int]);
-          const int4 hd = sb_hdr[pr * 13 + k];
-          nmv = hd.y & 0xFFFF; nbv = hd.y >> 16;
-        }
-        const double cost = 70.0 * nmv + 6.0 * nbv + 130.0 * (k == 0 ? 1 : 2);
-        if (nmv >= 8) {   // split between lane halves: two warp-tasks of 16 control points
-          for (int h = 0; h < 2; ++h) items.push_back({70.0 * nmv / 2 + 6.0 * nbv / 2 + 130.0, k | 16 | (h << 5) | (par << 6)});
-        } else {
-          items.push_back({cost, k | (par << 6)});
-        }
-      }
-      items.push_back({12.0 * 20 + 40.0, 13 | (par << 6)});   // gradient
-    }
-    std::sort(items.begin(), items.end(), [](auto& x, auto& y) { return x.first > y.first; });
-    std::vector<double> load(kW2, 0.0);
-    std::vector<std::vector<int>> wt(kW2);
-    for (auto& it : items) {   // longest processing time first
-      int best = -1;
-      for (int w = 0; w < kW2; ++w)
-        if ((int)wt[w].size() < kSched && (best < 0 || load[w] < load[best])) best = w;
-      if (best < 0) return 1;
-      wt[best].push_back(it.second);
-      load[best] += it.first;
-    }
-    tt.sched.assign(kW2 * kSched, -1);
-    for (int w = 0; w < kW2; ++w)
-      for (size_t q = 0; q < wt[w].size(); ++q) tt.sched[w * kSched + q] = wt[w][q];
-    tt.use_k2 = !cl[0].empty() && tt.smem2 <= 227 * 1024 && getenv("BSF_K2") != nullptr;   // opt-in (slower today)
-  }
   // consistency: the structural pattern equals the slab's pattern on every owned row
   for (int j = sh.r0; j < sh.r1; j += std::max(1, (sh.r1 - sh.r0) / 7))
     for (int i = 0; i < nu; i += std::max(1, nu / 7)) {
@@ -1215,16 +801,8 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
             upload(dalloc, &tt.utab, utab) && upload(dalloc, &tt.vtab, vtab) && upload(dalloc, &tt.stab, stab) &&
             upload(dalloc, &tt.m_geo, m_geo) && upload(dalloc, &tt.b_geo, b_geo) && upload(dalloc, &tt.lut, lut) &&
             upload(dalloc, &tt.tasks, tasks) && upload(dalloc, &tt.ent, ents) && upload(dalloc, &tt.row_ptr, rp) &&
-            upload(dalloc, &tt.chunks, chunks) && upload(dalloc, &tt.sb_hdr, sb_hdr) &&
-            upload(dalloc, &tt.sb_ent, sb_ents) && upload(dalloc, &tt.sched_d, tt.sched) &&
-            upload(dalloc, &tt.lay1m, lay1m) && upload(dalloc, &tt.lay1b, lay1b) && upload(dalloc, &tt.rsz1m, rsz1m) &&
-            upload(dalloc, &tt.rsz1b, rsz1b) && upload(dalloc, &tt.lay2m, lay2m) && upload(dalloc, &tt.lay2b, lay2b) &&
-            upload(dalloc, &tt.rsz2m, rsz2m) && upload(dalloc, &tt.rsz2b, rsz2b);
+            upload(dalloc, &tt.chunks, chunks);
   if (!ok) { err = "tile tables: device allocation failed"; return -7; }
-  if (tt.use_k2 && cudaFuncSetAttribute(k_tile2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tt.smem2) != cudaSuccess) {
-    cudaGetLastError();
-    tt.use_k2 = false;
-  }
   const size_t smax = std::max(tt.smem_l[0], tt.smem_l[1]);
   if (cudaFuncSetAttribute(k_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax) != cudaSuccess) {
     cudaGetLastError();
@@ -1236,8 +814,9 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
 
 int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_E, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride,
-              cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc) {
-  const int64_t need = (int64_t)nbatch * std::max(tt.nstrips, tt.nstrips2) * tt.nchunks;
+              cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc, const double* d_params) {
+  const int64_t need = (int64_t)nbatch * tt.nstrips * tt.nchunks;
+  (void)0;
   if (need > tt.e_cap) {
     void* p = dalloc(need * sizeof(double));
     if (!p) return -7;
@@ -1261,33 +840,22 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
   A.utab = tt.utab; A.vtab = tt.vtab; A.stab = tt.stab; A.m_geo = tt.m_geo; A.b_geo = tt.b_geo;
   A.Mm = (int64_t)sh.mem.size(); A.Bm = (int64_t)sh.bend.size();
   A.lut = tt.lut; A.tasks = tt.tasks; A.ent = tt.ent; A.row_ptr = tt.row_ptr;
-  A.sb_hdr = tt.sb_hdr; A.sb_ent = tt.sb_ent; A.sched = tt.sched_d;
-  A.estride = std::max(tt.nstrips, tt.nstrips2);
+  A.params = d_params; A.detJ_ref = tt.detJ_ref; A.flags = flags;
   int nl = 0;
   int base = 0;
-  if (d_E) { cudaMemsetAsync(tt.e_part, 0, sizeof(double) * need, st); }
   for (int L = 0; L < 2; ++L) {   // interior chunks, then boundary chunks
     if (tt.nch_l[L] == 0) continue;
+    A.capm = tt.capm_l[L];
+    A.capb = tt.capb_l[L];
     A.chunk_base = base;
     A.chunks = tt.chunks + base;
-    if (L == 0 && tt.use_k2 && !(flags & 16)) {
-      A.capm = tt.capm2;
-      A.capb = tt.capb2;
-      A.laym = tt.lay2m; A.layb = tt.lay2b; A.rszm = tt.rsz2m; A.rszb = tt.rsz2b;
-      dim3 grid(tt.nstrips2, tt.nch_l[L], nbatch);
-      k_tile2<<<grid, kThreads2, tt.smem2, st>>>(A);
-    } else {
-      A.capm = tt.capm_l[L];
-      A.capb = tt.capb_l[L];
-      A.laym = tt.lay1m; A.layb = tt.lay1b; A.rszm = tt.rsz1m; A.rszb = tt.rsz1b;
-      dim3 grid(tt.nstrips, tt.nch_l[L], nbatch);
-      k_tile<<<grid, kThreads, tt.smem_l[L], st>>>(A);
-    }
+    dim3 grid(tt.nstrips, tt.nch_l[L], nbatch);
+    k_tile<<<grid, kThreads, tt.smem_l[L], st>>>(A);
     ++nl;
     base += tt.nch_l[L];
   }
   if (d_E) {
-    k_energy_final<<<nbatch, 256, 0, st>>>(tt.e_part, std::max(tt.nstrips, tt.nstrips2) * tt.nchunks, d_E);
+    k_energy_final<<<nbatch, 256, 0, st>>>(tt.e_part, tt.nstrips * tt.nchunks, d_E);
     ++nl;
   }
   if (launches) *launches = nl;

@@ -8,7 +8,6 @@
 #include <cstdint>
 #include <functional>
 #include <string>
-#include <vector>
 
 #include "dev.hpp"
 #include "host.hpp"
@@ -29,19 +28,10 @@ struct TileTables {
   int capm_l[2] = {1, 1}, capb_l[2] = {1, 1}, nch_l[2] = {0, 0};   // per chunk list (interior, boundary)
   size_t smem_l[2] = {0, 0};
   int2* chunks = nullptr;          // [nchunks] (ra, rb): interior chunks then boundary chunks
-  // kernel 2 (interior chunks, 32-column strips, single-block parity-uniform tasks)
-  bool use_k2 = false;
-  int nstrips2 = 0, capm2 = 1, capb2 = 1;
-  size_t smem2 = 0;
-  int4* sb_hdr = nullptr;          // [nprog][13]: (entry offset, n_mem | n_bend<<16, k_ab | k_ba<<8 | exists<<16, 0)
-  uint32_t* sb_ent = nullptr;
-  std::vector<int> sched;          // [16][4] warp schedule codes (host copy)
-  int* sched_d = nullptr;
-  int16_t *lay1m = nullptr, *lay1b = nullptr, *lay2m = nullptr, *lay2b = nullptr;   // ring layouts
-  int32_t *rsz1m = nullptr, *rsz1b = nullptr, *rsz2m = nullptr, *rsz2b = nullptr;
   int affine = 0;
   double G[4] = {0, 0, 0, 0};      // affine: G[r*2+c]
   double detJ = 0;
+  double detJ_ref = 1.0;           // det J folded into the class weights (affine)
   int32_t* m_aoff = nullptr;       // [Sv*Su+1] anchor -> first membrane point (points sorted by anchor)
   int32_t* b_aoff = nullptr;
   uint2* m_info = nullptr;         // per sorted point: (u-table | v-table << 16, shape | anchor column << 16)
@@ -64,6 +54,7 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
 // Batched evaluation: item b uses x + b*x_stride, grad + b*g_stride, vals + b*v_stride, E + b.
 int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_E, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride,
-              cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc);
+              cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc,
+              const double* d_params = nullptr);
 
 }  // namespace bsf

@@ -202,3 +202,26 @@ def test_slab_sheet_nccl_single_rank():
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_c5_style_batch_of_different_sheets():
+    """Config C5 layout: independent sheets of one grid size with per-sheet side length, Young's
+    modulus and Poisson ratio in ONE launch (bsf_eval_all_batch_params), each against its own oracle."""
+    sheets = W.make_c5(count=4, n=40)
+    s = B.Sheet.from_sheet(sheets[0])
+    X = torch.stack([torch.from_numpy(q.x) for q in sheets]).cuda()
+    P = torch.from_numpy(np.stack([B.affine_params(q.rest_xy, B.material_from_young(q.E, q.nu, q.h))
+                                   for q in sheets])).cuda()
+    nb = len(sheets)
+    E = torch.zeros(nb, dtype=torch.float64, device="cuda")
+    G = torch.zeros((nb,) + tuple(X.shape[1:]), dtype=torch.float64, device="cuda")
+    V = torch.zeros((nb, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    s.eval_all_batch_params(X, P, E, G, V, B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    for k, q in enumerate(sheets):
+        o = O.Oracle.from_sheet(q)
+        Er, gr, vr = o.eval(q.x, flags=O.FLAG_PROJECT)
+        rp, ci = o.pattern()
+        va = o.eval(q.x, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
+        assert_parity(float(E[k]), G[k].cpu().numpy(), V[k].cpu().numpy(), Er, gr, vr, what=f"C5 item {k}",
+                      hdiag=diag_block_norms(vr, rp, ci, 0, q.n_u), cmax=np.abs(q.x).max(), vabs=va)
