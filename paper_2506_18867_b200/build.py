@@ -7,13 +7,13 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libbsfem.so")
+LIB = os.environ.get("BSF_LIB_PATH", os.path.join(HERE, "libbsfem.so"))
 SOURCES = ["host.cpp", "halo.cpp", "generic.cu", "tile.cu", "api.cu"]
 HEADERS = ["host.hpp", "dev.hpp", "fbw.cuh", "tile.hpp", "../../include/bsfem.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-         "-cudart", "static"]
+         "-cudart", "static"] + os.environ.get("BSF_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _stale() -> bool:
@@ -27,7 +27,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build" + ("_" + os.path.basename(LIB).replace(".so", "") if "BSF_LIB_PATH" in os.environ else ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     for src in SOURCES:

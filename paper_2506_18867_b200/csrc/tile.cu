@@ -81,6 +81,10 @@ constexpr int kBS = 13;    // bending:  [0,9) L^_e  [9,12) D^  [12] pad
 
 __device__ __forceinline__ int wrap(int q, int cap) { return q >= cap ? q - cap : q; }
 
+#ifdef BSF_PHASE_TIMERS
+__device__ unsigned long long g_phase[16];
+#endif
+
 // Warp-cooperative store of one 3x3 block per lane: lanes 9k..9k+8 store block 3r+k of round r
 // (72 contiguous bytes each); pos < 0 skips.  `transpose` selects H^T.
 __device__ __forceinline__ void warp_store_block(double* wb, const double (&blk)[9], bool transpose, int pos,
@@ -134,6 +138,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
   int head_m = 0, head_b = 0;
 
   for (int j0 = ra - 2; j0 < rb; j0 += kRS) {
+#ifdef BSF_PHASE_TIMERS
+    const long long T0 = clock64();
+#endif
     // ---------------- 1. positions of cp rows j0 .. j0+kRS+1, cols i0-2 .. i0+kTX+1
     for (int k = tid; k < kPosRows * kPosCols * 3; k += kThreads) {
       const int row = k / (kPosCols * 3), rem = k - row * kPosCols * 3;
@@ -169,6 +176,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
       }
     }
     __syncthreads();
+#ifdef BSF_PHASE_TIMERS
+    const long long T1 = clock64();
+#endif
     // ---------------- 3. point phase
     const int nmem = Nm[0] + Nm[1], ntot = nmem + Nb[0] + Nb[1];
     for (int k = tid; k < ntot; k += kThreads) {
@@ -292,6 +302,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
     __syncthreads();
     // prologue step (anchor rows ra-2, ra-1): no output, except the two halo rows above a slab whose
     // forward pairs reach into the first owned rows (transpose-only)
+#ifdef BSF_PHASE_TIMERS
+    const long long T2 = clock64();
+    if (tid == 0) { atomicAdd(&g_phase[0], (unsigned long long)(T1 - T0)); atomicAdd(&g_phase[1], (unsigned long long)(T2 - T1)); }
+#endif
     const bool halo_step = (j0 < ra);
     if (halo_step && !(ra == A.r0 && A.r0 > 0)) continue;
     // ---------------- 4. gather: symmetric forward tasks (b after a), both H_ab and H_ab^T written.
@@ -327,9 +341,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
 #pragma unroll
         for (int q = 0; q < 9; ++q) { acc0[q] = 0.0; acc1[q] = 0.0; acc2[q] = 0.0; }
         const int estep = split ? 2 : 1;
+        unsigned long long Ea = (half < n_m) ? __ldg(ent + half) : 0ull;
+        unsigned long long Eb = (half + estep < n_m) ? __ldg(ent + half + estep) : 0ull;
         for (int e = half; e < nmax_m; e += estep) {
+          const unsigned long long E = Ea;
+          Ea = Eb;
+          Eb = (e + 2 * estep < n_m) ? __ldg(ent + e + 2 * estep) : 0ull;
           if (e < n_m) {
-            const unsigned long long E = __ldg(ent + e);
             const int dt = E & 3, dc = (E >> 2) & 3, idx = (E >> 5) & 15, la = (E >> 9) & 15;
             const int t = j - 2 + dt;
             if (t >= anchor_min) {
@@ -451,6 +469,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
         }
       }
     }
+#ifdef BSF_PHASE_TIMERS
+    {
+      const long long T3 = clock64();
+      if ((tid & 31) == 0) atomicAdd(&g_phase[2 + (tid >> 5)], (unsigned long long)(T3 - T2));
+      __syncthreads();
+      if (tid == 0) { atomicAdd(&g_phase[9], (unsigned long long)(clock64() - T2)); atomicAdd(&g_phase[10], 1ull); }
+    }
+#endif
     __syncthreads();
   }
   // ---------------- energy partial of this CTA (fixed-order tree)
@@ -862,4 +888,11 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
   return cudaGetLastError() == cudaSuccess ? 0 : -6;
 }
 
+#ifdef BSF_PHASE_TIMERS
+extern "C" int bsf_debug_phase_timers(unsigned long long* out16, int reset) {
+  cudaMemcpyFromSymbol(out16, g_phase, sizeof(unsigned long long) * 16);
+  if (reset) { unsigned long long z[16] = {}; cudaMemcpyToSymbol(g_phase, z, sizeof(z)); }
+  return 0;
+}
+#endif
 }  // namespace bsf
