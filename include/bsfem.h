@@ -65,7 +65,8 @@ enum {
   BSF_PROJECT_PSD = 1,   /* per-term PSD projection of the FBW F-space Hessian (D7)  */
   BSF_NO_MEMBRANE = 2,   /* debug: drop the membrane terms                                       */
   BSF_NO_BENDING = 4,    /* debug: drop the bending terms                                        */
-  BSF_GENERIC_PATH = 8   /* force the generic point/gather kernels instead of the fused tile path */
+  BSF_GENERIC_PATH = 8,  /* force the generic point/gather kernels instead of the fused tile path */
+  BSF_TILE_ONLY = 16     /* debug: the tile kernel on the whole sheet, without the interior core kernel */
 };
 
 /* Stiffness symbols of Eq. `eq: FBW stretching and shearing energy` and
@@ -164,6 +165,11 @@ bsf_status bsf_halo_exchange(bsf_handle h, double* d_x, void* nccl_comm, int ran
 
 /* In-place sum all-reduce of n doubles (the slab energies) over the communicator. */
 bsf_status bsf_allreduce_sum(double* d_buf, int64_t n, void* nccl_comm, bsf_stream stream);
+
+/* Interior rectangle covered by the core kernel: rect4 = {i0, i1, j0, j1}, control
+ * points [i0,i1) x [j0,j1) of the owned rows; all zero if the handle has no core region (non-affine
+ * rest shape, non-REDUCED rules, small sheet, host-only handle).  Host call, no device work. */
+bsf_status bsf_get_core_rect(bsf_handle h, int32_t* rect4);
 
 /* Number of kernel launches the most recent compute call enqueued (for the bench's claim). */
 int bsf_last_launch_count(bsf_handle h);

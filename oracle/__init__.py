@@ -148,7 +148,10 @@ class Oracle:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib().oracle_destroy(h)
+            try:
+                lib().oracle_destroy(h)
+            except TypeError:   # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     def pattern(self):

@@ -16,10 +16,10 @@ import numpy as np
 from . import build as _build
 
 __all__ = ["Sheet", "Material", "material_from_young", "affine_params", "lib", "RULE_REDUCED", "RULE_G2_INTERIOR",
-           "RULE_G3_FULL", "PROJECT_PSD", "NO_MEMBRANE", "NO_BENDING", "GENERIC_PATH", "BsfError"]
+           "RULE_G3_FULL", "PROJECT_PSD", "NO_MEMBRANE", "NO_BENDING", "GENERIC_PATH", "TILE_ONLY", "BsfError"]
 
 RULE_REDUCED, RULE_G2_INTERIOR, RULE_G3_FULL = 0, 1, 2
-PROJECT_PSD, NO_MEMBRANE, NO_BENDING, GENERIC_PATH = 1, 2, 4, 8
+PROJECT_PSD, NO_MEMBRANE, NO_BENDING, GENERIC_PATH, TILE_ONLY = 1, 2, 4, 8, 16
 
 _STATUS = {0: "OK", -1: "INVALID_ARG", -2: "KNOTS", -3: "TOO_SMALL", -4: "DEGENERATE_GEOMETRY",
            -5: "SINGULAR_STRETCH", -6: "CUDA", -7: "OOM", -8: "NCCL", -9: "NO_DEVICE"}
@@ -27,7 +27,7 @@ _STATUS = {0: "OK", -1: "INVALID_ARG", -2: "KNOTS", -3: "TOO_SMALL", -4: "DEGENE
 SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_material", "bsf_get_sizes",
            "bsf_get_pattern", "bsf_eval_all_batch", "bsf_eval_all_batch_params", "bsf_eval_energy", "bsf_eval_gradient", "bsf_assemble_hessian", "bsf_eval_all",
            "bsf_halo_exchange", "bsf_nccl_get_unique_id", "bsf_nccl_comm_init", "bsf_nccl_comm_destroy",
-           "bsf_allreduce_sum", "bsf_last_launch_count", "bsf_last_error"]
+           "bsf_allreduce_sum", "bsf_get_core_rect", "bsf_last_launch_count", "bsf_last_error"]
 
 
 class BsfError(RuntimeError):
@@ -77,6 +77,7 @@ def lib():
         L.bsf_nccl_comm_destroy.argtypes = [vp]
         L.bsf_allreduce_sum.argtypes = [vp, C.c_int64, vp, vp]
         L.bsf_last_launch_count.argtypes = [vp]
+        L.bsf_get_core_rect.argtypes = [vp, ip]
         for s in SYMBOLS:
             getattr(L, s).restype = C.c_int if s not in ("bsf_last_error",) else C.c_char_p
         _lib = L
@@ -160,7 +161,10 @@ class Sheet:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().bsf_destroy(self._h)
+            try:
+                lib().bsf_destroy(self._h)
+            except TypeError:   # interpreter shutdown: module globals already cleared
+                pass
             self._h = None
 
     __del__ = close
@@ -232,6 +236,12 @@ class Sheet:
 
     def last_launch_count(self) -> int:
         return int(lib().bsf_last_launch_count(self._h))
+
+    def core_rect(self):
+        """(i0, i1, j0, j1): control points whose rows the interior core kernel writes; zeros if none."""
+        r = (C.c_int32 * 4)()
+        _check(lib().bsf_get_core_rect(self._h, r))
+        return tuple(int(v) for v in r)
 
     def __call__(self, x, flags=0):
         """Convenience: allocate outputs, run, return (E tensor[1], grad, vals)."""

@@ -11,6 +11,7 @@
 #include "../../include/bsfem.h"
 #include "dev.hpp"
 #include "host.hpp"
+#include "core.hpp"
 #include "tile.hpp"
 
 namespace bsf {
@@ -33,6 +34,8 @@ struct bsf_sheet {
   bsf::GenericTables gt;
   bsf::TileTables tt;
   bool tile_ok = false;
+  bsf::CoreTables ct;
+  bool core_ok = false;
   std::vector<void*> allocs;
   int last_launches = 0;
   bool host_only = false;
@@ -224,6 +227,15 @@ bsf_status bsf_create(int n_u, int n_v, const double* knots_u, const double* kno
     const int trc = bsf::build_tiles(h->sh, h->tt, terr, h->dalloc());
     h->tile_ok = (trc == 0);
     if (trc < 0) s = fail(BSF_E_OOM, terr);
+    if (h->tile_ok) {   // interior core kernel (affine sheets, REDUCED rules): optional
+      const int crc = bsf::build_core(h->sh, h->tt.row_ptr, h->ct, terr, h->dalloc());
+      if (crc < 0) s = fail(BSF_E_CUDA, terr);
+      else if (crc == 0 && h->ct.ok) {
+        const int src = bsf::tile_set_core(h->tt, h->sh, h->ct, h->dalloc());
+        if (src < 0) s = fail(BSF_E_OOM, "frame work lists");
+        else h->core_ok = true;
+      }
+    }
   }
   cudaSetDevice(prev);
   if (s != BSF_OK) {
@@ -264,7 +276,7 @@ bsf_status bsf_get_pattern(bsf_handle h, int32_t* row_ptr, int32_t* col_idx) {
 bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, double* d_grad, double* d_vals, int flags,
                         bsf_stream stream) {
   if (!h || !d_x) return fail(BSF_E_INVALID_ARG, "null argument");
-  if (flags & ~15) return fail(BSF_E_INVALID_ARG, "unknown flag bits");
+  if (flags & ~31) return fail(BSF_E_INVALID_ARG, "unknown flag bits");
   if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
   cudaError_t pe = cudaGetLastError();
   if (pe != cudaSuccess) return fail(BSF_E_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(pe));
@@ -277,7 +289,8 @@ bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, doubl
   int nl = 0;
   int rc;
   if (h->tile_ok && !(flags & BSF_GENERIC_PATH))
-    rc = bsf::tile_eval(h->tt, h->sh, d_x, 0, m, flags, 1, d_energy, d_grad, 0, d_vals, 0, st, &nl, h->dalloc(), nullptr);
+    rc = bsf::tile_eval(h->tt, h->sh, d_x, 0, m, flags, 1, d_energy, d_grad, 0, d_vals, 0, st, &nl, h->dalloc(), nullptr,
+                        (h->core_ok && !(flags & BSF_TILE_ONLY)) ? &h->ct : nullptr);
   else
     rc = bsf::generic_eval(h->gt, d_x, m, flags, nnzb, nrows, d_energy, d_grad, d_vals, st, &nl);
   h->last_launches = nl;
@@ -291,7 +304,7 @@ static bsf_status eval_batch_impl(bsf_handle h, int nbatch, const double* d_x, i
                                   bsf_stream stream, const double* d_params) {
   if (!h || !d_x || nbatch < 0) return fail(BSF_E_INVALID_ARG, "null argument / negative batch");
   if (nbatch == 0) return BSF_OK;
-  if (flags & ~15) return fail(BSF_E_INVALID_ARG, "unknown flag bits");
+  if (flags & ~31) return fail(BSF_E_INVALID_ARG, "unknown flag bits");
   if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
   const int64_t xn = (int64_t)(h->sh.xhi - h->sh.xlo) * h->sh.n_u * 3;
   const int64_t gn = (int64_t)(h->sh.r1 - h->sh.r0) * h->sh.n_u * 3, vn = (int64_t)h->sh.col_idx.size() * 9;
@@ -310,7 +323,8 @@ static bsf_status eval_batch_impl(bsf_handle h, int nbatch, const double* d_x, i
   }
   if (h->tile_ok && !(flags & BSF_GENERIC_PATH)) {
     rc = bsf::tile_eval(h->tt, h->sh, d_x, x_stride, h->mat, flags, nbatch, d_energy, d_grad, grad_stride, d_vals,
-                        vals_stride, st, &nl, h->dalloc(), d_params);
+                        vals_stride, st, &nl, h->dalloc(), d_params,
+                        (h->core_ok && !(flags & BSF_TILE_ONLY)) ? &h->ct : nullptr);
   } else {
     const int64_t nrows = (int64_t)(h->sh.r1 - h->sh.r0) * h->sh.n_u, nnzb = (int64_t)h->sh.col_idx.size();
     for (int b = 0; b < nbatch && rc == 0; ++b) {
@@ -356,6 +370,16 @@ bsf_status bsf_assemble_hessian(bsf_handle h, const double* d_x, double* d_vals,
 }
 
 int bsf_last_launch_count(bsf_handle h) { return h ? h->last_launches : 0; }
+
+bsf_status bsf_get_core_rect(bsf_handle h, int32_t* rect4) {
+  if (!h || !rect4) return fail(BSF_E_INVALID_ARG, "null argument");
+  const bool on = h->core_ok;
+  rect4[0] = on ? h->ct.CI0 : 0;
+  rect4[1] = on ? h->ct.CI1 : 0;
+  rect4[2] = on ? h->ct.RJ0 : 0;
+  rect4[3] = on ? h->ct.RJ1 : 0;
+  return BSF_OK;
+}
 
 }  // extern "C"
 

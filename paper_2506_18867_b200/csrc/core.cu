@@ -1,0 +1,805 @@
+// k_core: the fused interior kernel.  See core.hpp for the configuration it exploits.
+//
+// One CTA owns a strip of kW = 32 control-point columns over a chunk of rows of one sheet (grid.z =
+// batch item) and walks it kRows = 2 rows per step:
+//   1. point phase: the quadrature points of the two new knot rows of the strip window — membrane
+//      F~ = sum_e C_e d_e, F = F~ G, FBW Psi, P, A with the optional per-term PSD
+//      projection (fbw.cuh), stored in the parametric frame as
+//      A~ = w (G (x) I) A (G (x) I)^T split into A~uu, A~vv, S = A~uv + A~uv^T, D = A~uv - A~uv^T and
+//      P~ = w G P; bending Lap phi = sum_e L_e C_e — into a shared-memory ring of
+//      5 knot rows, channel-major (SoA), V / H point sets split by knot parity;
+//   2. gather: warp (parity pi, role) — 32 same-parity control points of the 2 rows — accumulates ONE
+//      entry (r, c) (and its transpose) of all 23 blocks of each lane's block row over the 12
+//      incident membrane points, with the compile-time incidence table of parity pi and constant
+//      coefficients k_uu, k_vv, k_s, k_a (core.hpp), in registers:
+//          H_ab[r][c] = sum_q k_uu A~uu[rc] + k_vv A~vv[rc] + k_s S[rc] + k_a D[rc]
+//      plus the constant bending blocks beta_ab I3 (the bending Hessian of an affine interior is
+//      state independent: sum_q w mu L_a L_b); diagonal roles also gather g_a[r];
+//   3. the two rows' outputs are staged in shared memory in their final BSR order and written with
+//      two TMA bulk copies (cp.async.bulk shared -> global), overlapping the next step's point phase.
+// Every block row is computed completely by its own control point (no transposes across rows), so
+// rows, slabs and chunks are independent and no atomics are used.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <type_traits>
+#include <vector>
+
+#include "core.hpp"
+#include "fbw.cuh"
+
+namespace bsf {
+
+namespace {
+using namespace core;
+
+struct CoreArgs {
+  const double* x;
+  int64_t xs;
+  double* g;
+  int64_t gs;
+  double* vals;
+  int64_t vs;
+  double* epart;
+  int64_t e_stride, e_off;
+  const int32_t* row_ptr;
+  int64_t rp_base, rp_stride;
+  const double* params;
+  int n_u, xlo, xhi, r0;
+  int CI0, CI1, RJ0, RJ1, nstrips, nchunks;
+  int project, flags, dbg;
+  double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
+  const double* tabs;      // device [104]: S[4][9][2] | LA[9] | LB[9] | LC[9] | what[5]
+  double what[5];
+  double S[4][9][2];       // per-set basis coefficients, compile-time indexed in the gather
+};
+
+// shared constants block (doubles)
+constexpr int kCstL = 0;        // [9]  L_e  (bending Laplacian coefficients of this item)
+constexpr int kCstLw = 9;       // [9]  w_b mu_bd L_e
+constexpr int kCstBeta = 18;    // [23] bending Hessian blocks beta_ab
+constexpr int kCstS = 41;       // [72] S[set][e][2]
+constexpr int kCstRed = 113;    // [24] energy reduction
+constexpr int kCstW = 137;      // [5]  parametric weights of the sets and of the bending points
+constexpr int kCstN = 142;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ int ring_slot(int q) { return (unsigned)(q + 7 * kRing) % kRing; }   // q >= -49
+
+#ifdef BSF_PHASE_TIMERS
+__device__ unsigned long long g_core_t[16];
+#define CT_MARK(v) const long long v = clock64()
+#define CT_ADD(i, d) atomicAdd(&g_core_t[i], (unsigned long long)(d))
+#else
+#define CT_MARK(v)
+#define CT_ADD(i, d)
+#endif
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
+// Gather of one warp: PI = parity of the lanes' control points; the warp's role is one entry (r, c)
+// of the 3x3 blocks.  For every incident point q (slot) of the lane's control point a:
+//     Yu = d_a,u A~uu[rc] + d_a,v A~vu[rc],   Yv = d_a,u A~uv[rc] + d_a,v A~vv[rc]
+//     H_ab[r][c] += d_b,u Yu + d_b,v Yv            for each block b of q's stencil
+// (= sum_{mu,nu} d_a,mu d_b,nu A~_mu,nu[r][c]).  d comes from the 4 x 9 x 2 per-set basis table S,
+// indexed at compile time (static_for over the parity's incidence table), so the 23 accumulators live
+// in registers and every coefficient is a uniform-register operand.  base0[d] / base1[d]
+// (d = dq + 2): lane's record pointer for knot row j+h+dq for even / odd knot-column offsets dp.
+// Diagonal roles (r == c) add the constant bending blocks and gather g_a[r]; bb0 / bb1 address the
+// bending arrays (channel r).  Staging stores wait on `bar` (previous bulk store has read the buffer).
+template <int PI>
+__device__ __forceinline__ void gather_role(const double (&S)[4][9][2], const double* const (&base0)[4],
+                                            const double* const (&base1)[4], const double* const (&bb0)[3],
+                                            const double* const (&bb1)[3], int o_uu, int o_vv, int o_rc, int o_cr,
+                                            int o_pu, int o_pv, bool diag, const double* __restrict__ cst,
+                                            double* st_lane, double* gdst, bool active, uint32_t bar,
+                                            uint32_t parity) {
+  double acc[kNB];
+#pragma unroll
+  for (int k = 0; k < kNB; ++k) acc[k] = 0.0;
+  double g = 0.0;
+  static_for<0, make_template(PI).nslot>([&](auto SI) {
+    constexpr int s = decltype(SI)::value;
+    constexpr Template T = make_template(PI);
+    constexpr int dp = T.s_dp[s], dq = T.s_dq[s], set = T.s_set[s], ea = T.s_ea[s];
+    const double* b = ((dp & 1) ? base1[dq + 2] : base0[dq + 2]) + set * kSetD + ((dp + 2) >> 1);
+    const double auu = b[o_uu], avv = b[o_vv], arc = b[o_rc], acr = b[o_cr];
+    const double dau = S[set][ea][0], dav = S[set][ea][1];
+    const double Yu = fma(dau, auu, dav * acr), Yv = fma(dau, arc, dav * avv);
+    static_for<T.s_c0[s], T.s_c0[s] + T.s_nc[s]>([&](auto CI) {
+      constexpr int c = decltype(CI)::value;
+      constexpr Template T2 = make_template(PI);
+      constexpr int k = T2.c_blk[c], eb = T2.c_eb[c];
+      acc[k] = fma(S[set][eb][0], Yu, fma(S[set][eb][1], Yv, acc[k]));
+    });
+    if (diag) g = fma(dau, b[o_pu], fma(dav, b[o_pv], g));
+  });
+  if (diag) {
+    static_for<0, kBSlots>([&](auto KI) {
+      constexpr int k = decltype(KI)::value;
+      constexpr int dp = bslot_dp(k), dq = bslot_dq(k);
+      const double* b = ((dp & 1) ? bb1[dq + 2] : bb0[dq + 2]) + ((dp + 2) >> 1);
+      g = fma(cst[kCstLw + k], b[0], g);
+    });
+    if (gdst && active) *gdst = g;
+#pragma unroll
+    for (int k = 0; k < kNB; ++k) acc[k] += cst[kCstBeta + k];
+  }
+  if (!st_lane) return;
+  mbar_wait(bar, parity);
+  if (!active) return;
+#pragma unroll
+  for (int k = 0; k < kNB; ++k) st_lane[k * 9] = acc[k];
+}
+
+// Stage the positions of cp rows [prow0, prow0 + nrows), cols [i0-3, i0+kW+3) (zero outside the array)
+// with asynchronous 8-byte copies (cp.async; the caller waits before the barrier that publishes them).
+// Thread tid copies elements tid, tid + kThreads, ... of the [nrows][kPosC][3] block.
+__device__ __forceinline__ void load_pos_async(double* pos, const double* __restrict__ x, const CoreArgs& A, int i0,
+                                               int prow0, int nrows, int tid) {
+  for (int k = tid; k < nrows * kPosC * 3; k += kThreads) {
+    const int row = k / (kPosC * 3), rem = k - row * (kPosC * 3);
+    const int col = rem / 3, c = rem - col * 3;
+    const int R = prow0 + row, Cc = i0 - 3 + col;
+    const bool in = R >= A.xlo && R < A.xhi && Cc >= 0 && Cc < A.n_u;
+    const double* src = in ? &x[((int64_t)(R - A.xlo) * A.n_u + Cc) * 3 + c] : x;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(pos + k)), "l"(src),
+                 "r"(in ? 8 : 0)
+                 : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// Same for the 5-row blocks of the main loop, with the element -> (row, col, component) map of this
+// thread precomputed (kPosStep <= 2 kThreads: at most two elements per thread).
+struct PosMap {
+  int n;            // elements of this thread (0..2)
+  int off[2];       // (row * n_u + col - (i0 - 3)) * 3 + c relative to the block origin, or -1 if the column is off the sheet
+  int row[2];
+  uint32_t dst[2];  // shared offsets (bytes) within a block
+};
+
+__device__ __forceinline__ void load_pos_step(uint32_t pos_s, const double* __restrict__ x, const CoreArgs& A,
+                                              const PosMap& pm, int i0, int prow0) {
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    if (e < pm.n) {
+      const int R = prow0 + pm.row[e];
+      const bool in = pm.off[e] >= 0 && R >= A.xlo && R < A.xhi;
+      const double* src = in ? x + ((int64_t)(prow0 - A.xlo) * A.n_u + (i0 - 3)) * 3 + pm.off[e] : x;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(pos_s + pm.dst[e]), "l"(src),
+                   "r"(in ? 8 : 0)
+                   : "memory");
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+struct PointCtx {
+  double G00, G01, G10, G11, det, mu1, mu2, mush, mubd, wb;
+  int i0, i1, ja, jb;
+  bool project;
+  bool diagG;      // G01 == G10 == 0 (axis-aligned rest sheet): F, A~ and P~ by scaling
+};
+
+// Quadrature points of two consecutive knot rows q0, q0+1: item it in [0, 6 kKC) =
+//   [membrane of row q0 (V- nV, V+ nV, H- nH, H+ nH) | membrane of row q0+1 | bending q0 | bending q0+1],
+// each set ordered by its knot index k = lp >> 1 (conflict-free record writes; membrane items first so
+// that warps do not diverge between the two kinds).  pos holds cp rows from prow0.
+// Returns the point's owned energy.
+__device__ __forceinline__ double eval_item(double* ring, const double* pos, int prow0, const double* cst,
+                                         const PointCtx& P, int q0, int it) {
+  const int nmem = 2 * kKC;
+  if (it >= 2 * nmem) {
+    // bending: per row lp even knots then lp odd knots
+    const int rb = it - 2 * nmem, r = rb >= kKC, rr = rb - r * kKC, q = q0 + r, nE = (kKC + 1) / 2;
+    const int lp = rr < nE ? 2 * rr : 2 * (rr - nE) + 1;
+    const int p = P.i0 - 2 + lp;
+    double* row = ring + ring_slot(q) * kRowD;
+    double lap[3] = {0, 0, 0};
+#pragma unroll
+    for (int jv = 0; jv < 3; ++jv)
+#pragma unroll
+      for (int iu = 0; iu < 3; ++iu) {
+        const int e = 3 * jv + iu;
+        if (e == 8) continue;
+        const double L = cst[kCstL + e];
+        const double* C = pos + ((q + jv - prow0) * kPosC + (p + iu - (P.i0 - 3))) * 3;
+        lap[0] = fma(L, C[0], lap[0]); lap[1] = fma(L, C[1], lap[1]); lap[2] = fma(L, C[2], lap[2]);
+      }
+    double* rec = row + 4 * kSetD + (lp & 1) * kBendD + (lp >> 1);
+    rec[0] = lap[0];
+    rec[kKH] = lap[1];
+    rec[2 * kKH] = lap[2];
+    if (p >= P.i0 && p < P.i1 && q >= P.ja && q < P.jb)
+      return 0.5 * P.wb * P.mubd * (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
+    return 0.0;
+  }
+  const int r = it >= nmem, mi = it - r * nmem, q = q0 + r;
+  double* row = ring + ring_slot(q) * kRowD;
+  const int pv = (q + P.i0) & 1;                 // lp parity of the V knots of this row (p + q even)
+  const int nV = (kKC - pv + 1) / 2, nH = kKC - nV;
+  int set, k;
+  if (mi < 2 * nV) { set = mi >= nV; k = mi - set * nV; }
+  else { const int x = mi - 2 * nV; set = 2 + (x >= nH); k = x - (set - 2) * nH; }
+  const int lp = 2 * k + ((set < 2) ? pv : 1 - pv), p = P.i0 - 2 + lp;
+  const int s = p + (set == 2 ? -1 : 0), tq = q + (set == 0 ? -1 : 0);   // anchor
+  const double* Sset = cst + kCstS + set * 18;
+  double Fu[3] = {0, 0, 0}, Fv[3] = {0, 0, 0};
+#pragma unroll
+  for (int jv = 0; jv < 3; ++jv)
+#pragma unroll
+    for (int iu = 0; iu < 3; ++iu) {
+      const int e = 3 * jv + iu;
+      const double du = Sset[2 * e], dv = Sset[2 * e + 1];
+      const double* C = pos + ((tq + jv - prow0) * kPosC + (s + iu - (P.i0 - 3))) * 3;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) { Fu[c] = fma(C[c], du, Fu[c]); Fv[c] = fma(C[c], dv, Fv[c]); }
+    }
+  const double wq = cst[kCstW + set] * P.det;
+  double f1[3], f2[3];   // F_beta = sum_mu F~_mu G_mu,beta
+  if (P.diagG) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * P.G00; f2[c] = Fv[c] * P.G11; }
+  } else {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * P.G00 + Fv[c] * P.G10; f2[c] = Fu[c] * P.G01 + Fv[c] * P.G11; }
+  }
+  FSpace o;
+  fbw_point(f1, f2, P.mu1, P.mu2, P.mush, P.project, o);
+  double* rec = row + set * kSetD + k;
+  if (P.diagG) {   // A~uu = w G00^2 A11, A~vv = w G11^2 A22, A~uv = w G00 G11 A12, P~ = w (G00 P1, G11 P2)
+    const double su = wq * P.G00, sv = wq * P.G11;
+    const double auu = su * P.G00, avv = sv * P.G11, auv = su * P.G11;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      rec[(21 + c) * kKH] = su * o.P1[c];
+      rec[(24 + c) * kKH] = sv * o.P2[c];
+    }
+#pragma unroll
+    for (int e6 = 0; e6 < 6; ++e6) {
+      rec[e6 * kKH] = auu * o.A11[e6];
+      rec[(6 + e6) * kKH] = avv * o.A22[e6];
+    }
+#pragma unroll
+    for (int e9 = 0; e9 < 9; ++e9) rec[(12 + e9) * kKH] = auv * o.A12[e9];
+    if (s >= P.i0 && s < P.i1 && tq >= P.ja && tq < P.jb) return wq * o.psi;
+    return 0.0;
+  }
+  // P~_mu = w sum_beta G_mu,beta P_beta
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    rec[(21 + c) * kKH] = wq * (P.G00 * o.P1[c] + P.G01 * o.P2[c]);
+    rec[(24 + c) * kKH] = wq * (P.G10 * o.P1[c] + P.G11 * o.P2[c]);
+  }
+  // A~_mu,nu = w sum_{beta,gamma} G_mu,beta G_nu,gamma A_beta,gamma
+  const double a11 = wq * P.G00 * P.G00, a12 = wq * P.G00 * P.G01, a22 = wq * P.G01 * P.G01;
+  const double b11 = wq * P.G10 * P.G10, b12 = wq * P.G10 * P.G11, b22 = wq * P.G11 * P.G11;
+  const double c11 = wq * P.G00 * P.G10, c12 = wq * P.G00 * P.G11, c21 = wq * P.G01 * P.G10, c22 = wq * P.G01 * P.G11;
+#pragma unroll
+  for (int r3 = 0; r3 < 3; ++r3)
+#pragma unroll
+    for (int c3 = r3; c3 < 3; ++c3) {
+      const int e6 = sym3(r3, c3);
+      const double A11 = o.A11[e6], A22 = o.A22[e6];
+      const double A12rc = o.A12[3 * r3 + c3], A12cr = o.A12[3 * c3 + r3];
+      rec[e6 * kKH] = a11 * A11 + a12 * (A12rc + A12cr) + a22 * A22;
+      rec[(6 + e6) * kKH] = b11 * A11 + b12 * (A12rc + A12cr) + b22 * A22;
+      rec[(12 + 3 * r3 + c3) * kKH] = c11 * A11 + c12 * A12rc + c21 * A12cr + c22 * A22;   // A~uv[r][c]
+      if (r3 != c3) rec[(12 + 3 * c3 + r3) * kKH] = c11 * A11 + c12 * A12cr + c21 * A12rc + c22 * A22;
+    }
+  if (s >= P.i0 && s < P.i1 && tq >= P.ja && tq < P.jb) return wq * o.psi;
+  return 0.0;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw);   // [kRing][kRowD]
+  double* stage = ring + kRing * kRowD;                  // [2][kStageRow]  (16-B aligned: kRing*kRowD even)
+  double* posb = stage + 2 * kStageRow;                  // [kPosD]
+  double* cst = posb + kPosD;                            // [kCstN]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(cst + kCstN);
+  const int tid = threadIdx.x;
+  CT_MARK(TK0);
+  const int strip = blockIdx.x, chunk = blockIdx.y, item = blockIdx.z;
+  const int i0 = A.CI0 + strip * kW, i1 = min(i0 + kW, A.CI1);
+  const int nsteps = (A.RJ1 - A.RJ0 + kRows - 1) / kRows;
+  const int sa = chunk * nsteps / A.nchunks, sb = (chunk + 1) * nsteps / A.nchunks;
+  const int ja = A.RJ0 + kRows * sa, jb = min(A.RJ0 + kRows * sb, A.RJ1);
+  const double* __restrict__ x = A.x + item * A.xs;
+  double* vals = A.vals ? A.vals + item * A.vs : nullptr;
+  double* gout = A.g ? A.g + item * A.gs : nullptr;
+
+  // ---- per-item affine map and stiffness
+  PointCtx P;
+  P.G00 = A.G00; P.G01 = A.G01; P.G10 = A.G10; P.G11 = A.G11; P.det = A.detJ;
+  P.mu1 = A.mu1; P.mu2 = A.mu2; P.mush = A.mush; P.mubd = A.mubd;
+  if (A.params) {
+    const double* pp = A.params + 9 * (int64_t)item;
+    P.G00 = pp[0]; P.G01 = pp[1]; P.G10 = pp[2]; P.G11 = pp[3]; P.det = pp[4];
+    P.mu1 = (A.flags & 2) ? 0.0 : pp[5];
+    P.mu2 = (A.flags & 2) ? 0.0 : pp[6];
+    P.mush = (A.flags & 2) ? 0.0 : pp[7];
+    P.mubd = (A.flags & 4) ? 0.0 : pp[8];
+  }
+  P.i0 = i0; P.i1 = i1; P.ja = ja; P.jb = jb; P.project = A.project != 0;
+  P.diagG = (P.G01 == 0.0 && P.G10 == 0.0);
+  const double cuu = P.G00 * P.G00 + P.G01 * P.G01, cvv = P.G10 * P.G10 + P.G11 * P.G11;
+  const double cuv = 2.0 * (P.G00 * P.G10 + P.G01 * P.G11);
+  P.wb = A.what[4] * P.det;
+  if (tid < 9) {
+    const double L = (tid == 8) ? 0.0 : cuu * A.tabs[72 + tid] + cvv * A.tabs[81 + tid] + cuv * A.tabs[90 + tid];
+    cst[kCstL + tid] = L;
+    cst[kCstLw + tid] = P.wb * P.mubd * L;
+  }
+  if (tid < 72) cst[kCstS + tid] = A.tabs[tid];
+  if (tid < 5) cst[kCstW + tid] = A.tabs[99 + tid];
+  const uint32_t bar = smem_u32(mbar);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid < kNB) {   // beta_ab = w mu sum_{bending q containing a, b} L_a(q) L_b(q)
+    double s = 0.0;
+    for (int k = 0; k < kBSlots; ++k)
+      for (int e = 0; e < 8; ++e) {
+        const int di = bslot_dp(k) + e % 3, dj = bslot_dq(k) + e / 3;
+        if (block_index(di, dj) == tid) s += cst[kCstL + k] * cst[kCstL + e];
+      }
+    cst[kCstBeta + tid] = P.wb * P.mubd * s;
+  }
+
+  double e_acc = 0.0;
+  // ---- warp roles: warps 0-8 gather block entry (r, c) = (warp / 3, warp % 3) for both parities;
+  // warps 9-15 evaluate the quadrature points of the next step (7 x 30 lanes = the 210 points)
+  const int warp = tid >> 5, lane = tid & 31;
+  const int role = warp < kGatherWarps ? warp : 0;
+  const int rr = role / 3, cc = role - 3 * (role / 3);
+  const bool diag = rr == cc;
+  const int o_uu = sym3(rr, cc) * kKH, o_vv = (6 + sym3(rr, cc)) * kKH;
+  const int o_rc = (12 + 3 * rr + cc) * kKH, o_cr = (12 + 3 * cc + rr) * kKH;
+  const int o_pu = (21 + rr) * kKH, o_pv = (24 + rr) * kKH;
+  const int h = lane >> 4, m = lane & 15;
+  const int pw = warp - kGatherWarps;   // point warp index
+
+  CT_MARK(TK1);
+  if (ja < jb) {
+    // Iteration m evaluates the quadrature points of knot rows q0 = ja-3+2m, q0+1 ("pair m") and, for
+    // m >= 3, gathers the rows of step k = m-3 (j = ja+2k, needing knot rows j-2 .. j+2 = pairs k..k+2).
+    // Pairs 0-2 form the prologue.  Positions of pair m+1 are fetched asynchronously during m.
+    const int nst = (jb - ja + kRows - 1) / kRows;
+    PosMap pm;
+    pm.n = 0;
+    for (int e = 0; e < 2; ++e) {
+      const int kk = tid + e * kThreads;
+      if (kk < kPosStep) {
+        const int row = kk / (kPosC * 3), rem = kk - row * (kPosC * 3), col = rem / 3, c = rem - col * 3;
+        const int Cc = i0 - 3 + col;
+        pm.row[e] = row;
+        pm.off[e] = (Cc >= 0 && Cc < A.n_u) ? (row * A.n_u + col) * 3 + c : -1;
+        pm.dst[e] = kk * 8;
+        pm.n = e + 1;
+      }
+    }
+    const uint32_t pos_s = smem_u32(posb);
+    load_pos_async(posb, x, A, i0, ja - 4, 5, tid);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    for (int mi = 0; mi <= nst + 2; ++mi) {
+      const int q0 = ja - 3 + 2 * mi, k = mi - 3, j = ja + kRows * k;
+      CT_MARK(T0);
+#ifdef BSF_PHASE_TIMERS
+      if (tid == 0 && mi == 3) CT_ADD(12, T0 - TK1);
+#endif
+      // (a) positions of the next pair (async) and the quadrature points of this pair
+      if (mi + 1 <= nst + 1) load_pos_step(pos_s + ((mi + 1) & 1) * (kPosStep * 8), x, A, pm, i0, q0 + 1);
+      if (mi <= nst + 1 && pw >= 0 && lane < 30 && !((A.dbg & 1) && k >= 0))
+        e_acc += eval_item(ring, posb + (mi & 1) * kPosStep, q0 - 1, cst, P, q0, pw * 30 + lane);
+      CT_MARK(T1);
+      if (k >= 0) {
+        // (b) the issuing thread releases the staging buffer once the previous bulk store has read it
+        if (tid == 0) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(bar) : "memory");
+        }
+        // (c) gather of rows j, j+1: lanes = 16 control points of parity PI in each of the two rows
+        if (warp < kGatherWarps && !(A.dbg & 2)) {
+          // ring rows of knot rows jr-2 .. jr+1 of this lane's row jr = j + h (parity independent)
+          const double* rowp[4];
+          {
+            int sl = ring_slot(j + h - 2);
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+              rowp[d] = ring + sl * kRowD + m;
+              sl = (sl == kRing - 1) ? 0 : sl + 1;
+            }
+          }
+#pragma unroll 1
+          for (int PI = 0; PI < 2; ++PI) {
+            const int jr = j + h;
+            const int sigma = (PI + jr + i0) & 1;
+            const int i = i0 + 2 * m + sigma;
+            const bool active = (i < i1) && (jr < jb);
+            const double* base0[4];
+            const double* base1[4];
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+              base0[d] = rowp[d];
+              base1[d] = rowp[d] + sigma;
+            }
+            const double* bb0[3];
+            const double* bb1[3];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              const double* rb = rowp[d] + 4 * kSetD + rr * kKH;
+              bb0[d] = rb + sigma * kBendD;
+              bb1[d] = rb + (1 - sigma) * kBendD + sigma;
+            }
+            // staging: row h of the step; base parity matched to the global address (TMA needs equal
+            // alignment mod 16 on both sides)
+            double* st_lane = nullptr;
+            if (vals && !(A.dbg & 4)) {
+              const int64_t g0 = (A.rp_base + (int64_t)(jr - A.RJ0) * A.rp_stride + (int64_t)(i0 - A.CI0) * kNB) * 9;
+              const int pad = (int)(((uintptr_t)(vals + g0) >> 3) & 1);
+              st_lane = stage + h * kStageRow + pad + (i - i0) * (kNB * 9) + 3 * rr + cc;
+            }
+            double* gdst = (gout && diag) ? gout + ((int64_t)(jr - A.r0) * A.n_u + i) * 3 + rr : nullptr;
+            const uint32_t par = k & 1;
+            if (PI == 0)
+              gather_role<0>(A.S, base0, base1, bb0, bb1, o_uu, o_vv, o_rc, o_cr, o_pu, o_pv, diag, cst, st_lane,
+                             gdst, active, bar, par);
+            else
+              gather_role<1>(A.S, base0, base1, bb0, bb1, o_uu, o_vv, o_rc, o_cr, o_pu, o_pv, diag, cst, st_lane,
+                             gdst, active, bar, par);
+          }
+        }
+      }
+      CT_MARK(T2);
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      CT_MARK(T3);
+      __syncthreads();
+      CT_MARK(T4);
+#ifdef BSF_PHASE_TIMERS
+      if (k >= 0 && lane == 0) {
+        if (warp == kGatherWarps) { CT_ADD(0, T1 - T0); CT_ADD(7, T2 - T1); }
+        if (warp == 0) { CT_ADD(1, T2 - T1); CT_ADD(3, T3 - T2); CT_ADD(4, T4 - T3); CT_ADD(5, T4 - T0); CT_ADD(6, 1); }
+        if (warp == 2) CT_ADD(2, T2 - T1);
+      }
+#endif
+      // (d) bulk stores of the step's rows (head / tail doubles off the 16-B grid by plain stores)
+      if (k >= 0 && vals && tid < 5) {
+        for (int hh = 0; hh < kRows; ++hh) {
+          const int jr2 = j + hh;
+          if (jr2 >= jb) break;
+          const int64_t g0 = (A.rp_base + (int64_t)(jr2 - A.RJ0) * A.rp_stride + (int64_t)(i0 - A.CI0) * kNB) * 9;
+          double* gd = vals + g0;
+          const int pad = (int)(((uintptr_t)gd >> 3) & 1);
+          const double* sp = stage + hh * kStageRow + pad;
+          const int64_t nd = (int64_t)(i1 - i0) * (kNB * 9);
+          const int head = pad;                                  // 1 double if gd is 8 mod 16
+          const int tail = (int)((nd - head) & 1);               // 1 double if the end is 8 mod 16
+          if (tid == 0) {
+            const int64_t nb = (A.dbg & 8) ? 0 : nd - head - tail;
+            if (nb > 0)
+              asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gd + head),
+                           "r"(smem_u32(sp + head)), "r"((uint32_t)(nb * 8))
+                           : "memory");
+          } else if (tid == 1 + hh) {
+            if (head) gd[0] = sp[0];
+          } else if (tid == 3 + hh) {
+            if (tail) gd[nd - 1] = sp[nd - 1];
+          }
+        }
+        if (tid == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+#ifdef BSF_PHASE_TIMERS
+      if (k >= 0 && (tid == 0 || tid == 32)) { CT_MARK(T5); CT_ADD(tid ? 14 : 13, T5 - T4); }
+#endif
+    }
+  }
+  CT_MARK(TK2);
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#ifdef BSF_PHASE_TIMERS
+  if (tid == 0) { CT_ADD(8, TK1 - TK0); CT_ADD(9, TK2 - TK1); CT_ADD(10, 1); CT_ADD(11, clock64() - TK0); }
+#endif
+  // ---- energy partial of this CTA (fixed-order tree)
+  for (int o = 16; o > 0; o >>= 1) e_acc += __shfl_xor_sync(0xffffffffu, e_acc, o);
+  __syncthreads();
+  if ((tid & 31) == 0) cst[kCstRed + (tid >> 5)] = e_acc;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) s += cst[kCstRed + w];
+    A.epart[item * A.e_stride + A.e_off + (int64_t)chunk * A.nstrips + strip] = s;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------ host
+namespace {
+
+int set_of(const Point& P) {   // -1: not an interior-template membrane point
+  const uint16_t V = 0xDB;      // window entries iu in {0,1}: a point on a knot line u = p (2x3 stencil)
+  const uint16_t H = 0x3F;      // entries jv in {0,1}: a point on v = q (3x2)
+  const int par = (P.ou + P.ov) & 1;
+  if (P.mask == V) return par ? 0 : 1;          // V-: anchor (p, q-1), p+q even -> s+t odd
+  if (P.mask == H) return par ? 3 : 2;          // H-: anchor (p-1, q), p+q odd -> s+t even
+  return -1;
+}
+
+void point_du_dv(const Point& P, double (&S)[9][2]) {
+  for (int e = 0; e < 9; ++e) {
+    const int iu = e % 3, jv = e / 3;
+    const bool in = (P.mask >> e) & 1;
+    S[e][0] = in ? P.bu.d1[iu] * P.bv.N[jv] : 0.0;
+    S[e][1] = in ? P.bu.N[iu] * P.bv.d1[jv] : 0.0;
+  }
+}
+
+}  // namespace
+
+int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::string& err,
+               const std::function<void*(size_t)>& dalloc) {
+  ct = CoreTables();
+  ct.row_ptr = const_cast<int32_t*>(d_row_ptr);
+  if (!sh.affine || sh.mrule != RULE_REDUCED || sh.brule != RULE_REDUCED) return 1;
+  const int nu = sh.n_u, Su = sh.Su, Sv = sh.Sv;
+  if (nu < 16 || sh.n_v < 16) return 1;
+  // ---- anchor buckets
+  const int nanch = Su * Sv;
+  std::vector<int32_t> mh(nanch + 1, 0), bh(nanch + 1, 0);
+  for (const Point& P : sh.mem) ++mh[P.ov * Su + P.ou + 1];
+  for (const Point& P : sh.bend) ++bh[P.ov * Su + P.ou + 1];
+  for (int a = 0; a < nanch; ++a) { mh[a + 1] += mh[a]; bh[a + 1] += bh[a]; }
+  std::vector<int32_t> mi(sh.mem.size()), bi(sh.bend.size());
+  {
+    std::vector<int32_t> f(mh.begin(), mh.end() - 1), fb(bh.begin(), bh.end() - 1);
+    for (size_t k = 0; k < sh.mem.size(); ++k) mi[f[sh.mem[k].ov * Su + sh.mem[k].ou]++] = (int32_t)k;
+    for (size_t k = 0; k < sh.bend.size(); ++k) bi[fb[sh.bend[k].ov * Su + sh.bend[k].ou]++] = (int32_t)k;
+  }
+  // ---- representatives near the middle of the owned rows
+  const int jc = (sh.r0 + sh.r1) / 2, ic = nu / 2;
+  bool have[5] = {false, false, false, false, false};
+  for (int t = std::max(0, jc - 3); t <= std::min(Sv - 1, jc + 1); ++t)
+    for (int s = std::max(0, ic - 3); s <= std::min(Su - 1, ic + 1); ++s) {
+      const int an = t * Su + s;
+      for (int k = mh[an]; k < mh[an + 1]; ++k) {
+        const Point& P = sh.mem[mi[k]];
+        const int set = set_of(P);
+        if (set < 0 || have[set]) continue;
+        point_du_dv(P, ct.S[set]);
+        ct.what[set] = P.what;
+        have[set] = true;
+      }
+      for (int k = bh[an]; k < bh[an + 1]; ++k) {
+        const Point& P = sh.bend[bi[k]];
+        if (have[4] || P.mask != 0xFF) continue;
+        for (int e = 0; e < 9; ++e) {
+          const int iu = e % 3, jv = e / 3;
+          const bool in = (P.mask >> e) & 1;
+          ct.LA[e] = in ? P.bu.d2[iu] * P.bv.N[jv] : 0.0;
+          ct.LB[e] = in ? P.bu.N[iu] * P.bv.d2[jv] : 0.0;
+          ct.LC[e] = in ? P.bu.d1[iu] * P.bv.d1[jv] : 0.0;
+        }
+        ct.what[4] = P.what;
+        have[4] = true;
+      }
+    }
+  for (bool hv : have)
+    if (!hv) return 1;
+  // ---- per-control-point conformance with the template (owned rows)
+  const double tol = 1e-12;
+  auto close = [&](double a, double b) { return std::fabs(a - b) <= tol * std::max(1.0, std::fabs(b)); };
+  constexpr Template T0 = make_template(0), T1 = make_template(1);
+  auto conforms = [&](int i, int j) -> bool {
+    if (i < 2 || j < 2 || i > nu - 3 || j > sh.n_v - 3) return false;
+    const Template& T = ((i + j) & 1) ? T1 : T0;
+    // membrane: exactly the template's 12 points
+    int found = 0;
+    for (int t = j - 2; t <= j; ++t)
+      for (int s = i - 2; s <= i; ++s) {
+        if (s < 0 || t < 0 || s >= Su || t >= Sv) continue;
+        const int an = t * Su + s;
+        for (int k = mh[an]; k < mh[an + 1]; ++k) {
+          const Point& P = sh.mem[mi[k]];
+          const int ea = (i - s) + 3 * (j - t);
+          if (!((P.mask >> ea) & 1)) continue;
+          const int set = set_of(P);
+          if (set < 0) return false;
+          int slot = -1;
+          for (int z = 0; z < T.nslot; ++z)
+            if (T.s_set[z] == set && T.s_ea[z] == ea) slot = z;
+          if (slot < 0) return false;
+          if (!close(P.what, ct.what[set])) return false;
+          double S[9][2];
+          point_du_dv(P, S);
+          for (int e = 0; e < 9; ++e)
+            if (!close(S[e][0], ct.S[set][e][0]) || !close(S[e][1], ct.S[set][e][1])) return false;
+          ++found;
+        }
+      }
+    if (found != T.nslot) return false;
+    int bfound = 0;
+    for (int t = j - 2; t <= j; ++t)
+      for (int s = i - 2; s <= i; ++s) {
+        if (s < 0 || t < 0 || s >= Su || t >= Sv) continue;
+        const int an = t * Su + s;
+        for (int k = bh[an]; k < bh[an + 1]; ++k) {
+          const Point& P = sh.bend[bi[k]];
+          const int ea = (i - s) + 3 * (j - t);
+          if (!((P.mask >> ea) & 1)) continue;
+          if (P.mask != 0xFF || !close(P.what, ct.what[4])) return false;
+          for (int e = 0; e < 9; ++e) {
+            const int iu = e % 3, jv = e / 3;
+            const bool in = (P.mask >> e) & 1;
+            if (!close(in ? P.bu.d2[iu] * P.bv.N[jv] : 0.0, ct.LA[e]) ||
+                !close(in ? P.bu.N[iu] * P.bv.d2[jv] : 0.0, ct.LB[e]) ||
+                !close(in ? P.bu.d1[iu] * P.bv.d1[jv] : 0.0, ct.LC[e]))
+              return false;
+          }
+          ++bfound;
+        }
+      }
+    if (bfound != kBSlots) return false;
+    // pattern row: the 23 standard columns
+    const int64_t al = (int64_t)(j - sh.r0) * nu + i;
+    if (sh.row_ptr[al + 1] - sh.row_ptr[al] != kNB) return false;
+    for (int k = 0; k < kNB; ++k)
+      if (sh.col_idx[sh.row_ptr[al] + k] != (j + block_dj(k)) * nu + i + block_di(k)) return false;
+    return true;
+  };
+  // rectangle: conformant columns of the middle owned row, then the owned rows on which all of them conform
+  const int jm = std::min(std::max(jc, sh.r0), sh.r1 - 1);
+  int c0 = ic, c1 = ic;
+  if (!conforms(ic, jm)) return 1;
+  while (c0 - 1 >= 0 && conforms(c0 - 1, jm)) --c0;
+  while (c1 + 1 < nu && conforms(c1 + 1, jm)) ++c1;
+  ++c1;
+  auto row_ok = [&](int j) {
+    for (int i = c0; i < c1; ++i)
+      if (!conforms(i, j)) return false;
+    return true;
+  };
+  int j0 = jm, j1 = jm;
+  while (j0 - 1 >= sh.r0 && row_ok(j0 - 1)) --j0;
+  while (j1 + 1 < sh.r1 && row_ok(j1 + 1)) ++j1;
+  ++j1;
+  if (!row_ok(jm)) return 1;
+  if (c1 - c0 < 8 || j1 - j0 < 1) return 1;
+  ct.CI0 = c0; ct.CI1 = c1; ct.CJ0 = j0; ct.CJ1 = j1; ct.RJ0 = j0; ct.RJ1 = j1;
+  {   // row starts of the rectangle: affine in the row (every core row has the same frame columns)
+    auto rp = [&](int i, int j) { return (int64_t)sh.row_ptr[(int64_t)(j - sh.r0) * nu + i]; };
+    ct.rp_base = rp(c0, j0);
+    ct.rp_stride = (j1 - j0 > 1) ? rp(c0, j0 + 1) - rp(c0, j0) : 0;
+    for (int j = j0; j < j1; ++j)
+      for (int i = c0; i < c1; ++i)
+        if (rp(i, j) != ct.rp_base + (int64_t)(j - j0) * ct.rp_stride + (int64_t)(i - c0) * kNB) return 1;
+  }
+  ct.nstrips = (c1 - c0 + kW - 1) / kW;
+  // ---- coefficient tables
+  for (int pi = 0; pi < 2; ++pi) {
+    const Template T = make_template(pi);
+    for (int s = 0; s < T.nslot; ++s) {
+      const double* da = ct.S[T.s_set[s]][T.s_ea[s]];
+      ct.D[pi][s][0] = da[0];
+      ct.D[pi][s][1] = da[1];
+      for (int c = T.s_c0[s]; c < T.s_c0[s] + T.s_nc[s]; ++c) {
+        const double* db = ct.S[T.s_set[s]][T.c_eb[c]];
+        const double k11 = da[0] * db[0], k22 = da[1] * db[1], k12 = da[0] * db[1], k21 = da[1] * db[0];
+        ct.K[pi][c][0] = k11;
+        ct.K[pi][c][1] = k22;
+        ct.K[pi][c][2] = 0.5 * (k12 + k21);
+        ct.K[pi][c][3] = 0.5 * (k12 - k21);
+      }
+    }
+  }
+  {
+    const Point& ref = sh.mem.empty() ? sh.bend[0] : sh.mem[0];
+    ct.G[0] = ref.G[0][0]; ct.G[1] = ref.G[0][1]; ct.G[2] = ref.G[1][0]; ct.G[3] = ref.G[1][1];
+    ct.detJ = ref.detJ;
+  }
+  {
+    std::vector<double> tabs(104, 0.0);
+    std::memcpy(tabs.data(), ct.S, sizeof(ct.S));
+    std::memcpy(tabs.data() + 72, ct.LA, sizeof(ct.LA));
+    std::memcpy(tabs.data() + 81, ct.LB, sizeof(ct.LB));
+    std::memcpy(tabs.data() + 90, ct.LC, sizeof(ct.LC));
+    std::memcpy(tabs.data() + 99, ct.what, sizeof(ct.what));
+    void* p = dalloc(tabs.size() * sizeof(double));
+    if (!p || cudaMemcpy(p, tabs.data(), tabs.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+      err = "core: table upload failed";
+      return -7;
+    }
+    ct.d_tabs = static_cast<double*>(p);
+  }
+  ct.smem = sizeof(double) * ((size_t)kRing * kRowD + 2 * kStageRow + kPosD + kCstN) + 16;
+  if (ct.smem > 227 * 1024) { err = "core: shared memory budget"; return -1; }
+  if (cudaFuncSetAttribute(k_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  if (getenv("BSF_CORE_DEBUG")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k_core);
+    int nb = -1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_core, kThreads, ct.smem);
+    fprintf(stderr, "k_core: regs %d maxthreads %d local %zu static smem %zu dyn %zu maxdyn %d occ %d\n", fa.numRegs,
+            fa.maxThreadsPerBlock, fa.localSizeBytes, fa.sharedSizeBytes, ct.smem, fa.maxDynamicSharedSizeBytes, nb);
+  }
+  ct.ok = 1;
+  (void)err;
+  return 0;
+}
+
+int core_ctas_per_item(const CoreTables& ct, int nchunks) { return ct.nstrips * nchunks; }
+
+int core_pick_chunks(const CoreTables& ct, int nbatch) {
+  // enough CTAs for ~4 waves of 148 SMs (1 CTA / SM), chunks of >= 16 rows
+  const int rows = ct.RJ1 - ct.RJ0;
+  const int per = std::max(1, ct.nstrips * std::max(1, nbatch));
+  int nch = (4 * 148 + per - 1) / per;
+  nch = std::min(nch, std::max(1, rows / 16));
+  return std::max(1, nch);
+}
+
+int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
+              int nbatch, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride, double* e_part,
+              int64_t e_stride, int64_t e_off, int nchunks, const double* d_params, double detJ_ref,
+              cudaStream_t st) {
+  (void)detJ_ref;
+  CoreArgs A;
+  A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride;
+  A.epart = e_part; A.e_stride = e_stride; A.e_off = e_off;
+  A.row_ptr = ct.row_ptr; A.rp_base = ct.rp_base; A.rp_stride = ct.rp_stride; A.params = d_params;
+  A.n_u = sh.n_u; A.xlo = sh.xlo; A.xhi = sh.xhi; A.r0 = sh.r0;
+  A.CI0 = ct.CI0; A.CI1 = ct.CI1; A.RJ0 = ct.RJ0; A.RJ1 = ct.RJ1; A.nstrips = ct.nstrips; A.nchunks = nchunks;
+  A.project = (flags & 1) ? 1 : 0; A.flags = flags;
+  {
+    const char* e = getenv("BSF_CORE_DEBUG");   // profiling switches: 1 no points, 2 no gather, 4 no stores
+    A.dbg = e ? atoi(e) : 0;
+  }
+  A.G00 = ct.G[0]; A.G01 = ct.G[1]; A.G10 = ct.G[2]; A.G11 = ct.G[3]; A.detJ = ct.detJ;
+  A.mu1 = (flags & 2) ? 0.0 : mat.mu_st1;
+  A.mu2 = (flags & 2) ? 0.0 : mat.mu_st2;
+  A.mush = (flags & 2) ? 0.0 : mat.mu_sh;
+  A.mubd = (flags & 4) ? 0.0 : mat.mu_bd;
+  A.tabs = ct.d_tabs;
+  std::memcpy(A.what, ct.what, sizeof(A.what));
+  std::memcpy(A.S, ct.S, sizeof(A.S));
+  dim3 grid(ct.nstrips, nchunks, nbatch);
+  k_core<<<grid, kThreads, ct.smem, st>>>(A);
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
+}
+
+#ifdef BSF_PHASE_TIMERS
+extern "C" int bsf_debug_core_timers(unsigned long long* out16, int reset) {
+  cudaMemcpyFromSymbol(out16, g_core_t, sizeof(unsigned long long) * 16);
+  if (reset) { unsigned long long z[16] = {}; cudaMemcpyToSymbol(g_core_t, z, sizeof(z)); }
+  return 0;
+}
+#endif
+}  // namespace bsf

@@ -180,7 +180,7 @@ int generic_eval(const GenericTables& t, const double* d_x, const Mat& mat, int 
     }
   }
   if (launches) *launches = nl;
-  return cudaGetLastError() == cudaSuccess ? 0 : -6;
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
 }
 
 }  // namespace bsf

@@ -25,6 +25,7 @@
 #include <numeric>
 #include <vector>
 
+#include "core.hpp"
 #include "fbw.cuh"
 #include "tile.hpp"
 
@@ -70,6 +71,10 @@ struct TileArgs {
   const unsigned long long* ent;
   const int32_t* row_ptr;
   const int2* chunks;      // (ra, rb) per chunk of this launch
+  const int2* work;        // frame mode: (strip, chunk of this launch) per CTA; nullptr = full grid
+  int sk_i0, sk_i1, sk_j0, sk_j1;   // control points whose rows k_core writes (no gather here)
+  int ex_i0, ex_i1, ex_j0, ex_j1;   // anchors whose energy k_core counts
+  int64_t e_stride;        // energy partial slots per item
   const double* params;    // optional per-item [9]: G00 G01 G10 G11 detJ mu_st1 mu_st2 mu_sh mu_bd
   double detJ_ref;         // det J the class weights were built with
   int flags;
@@ -105,9 +110,11 @@ __device__ __forceinline__ void warp_store_block(double* wb, const double (&blk)
 __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x;
-  const int strip = blockIdx.x, chunk = A.chunk_base + blockIdx.y, item = blockIdx.z;
+  int strip = blockIdx.x, cl = blockIdx.y;
+  if (A.work) { const int2 w = A.work[blockIdx.x]; strip = w.x; cl = w.y; }
+  const int chunk = A.chunk_base + cl, item = blockIdx.z;
   const int i0 = strip * kTX;
-  const int2 chr = A.chunks[blockIdx.y];
+  const int2 chr = A.chunks[cl];
   const int ra = chr.x, rb = chr.y;
   const int slo = max(0, i0 - 2), shi = min(A.Su - 1, i0 + kTX - 1);
   const double* __restrict__ x = A.x + item * A.xs;
@@ -224,7 +231,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
         for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * G00 + Fv[c] * G10; f2[c] = Fu[c] * G01 + Fv[c] * G11; }
         FSpace o;
         fbw_point(f1, f2, pmu1, pmu2, pmush, A.project != 0, o);
-        if (ou >= i0 && ou < i0 + kTX && t >= ra && t < rb) e_acc += w * o.psi;
+        if (ou >= i0 && ou < i0 + kTX && t >= ra && t < rb &&
+            !(ou >= A.ex_i0 && ou < A.ex_i1 && t >= A.ex_j0 && t < A.ex_j1))
+          e_acc += w * o.psi;
         // P~_mu = w sum_beta G_mu,beta P_beta
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -292,7 +301,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
             }
             rec[e] = sw * L;
           }
-        if (ou >= i0 && ou < i0 + kTX && t >= ra && t < rb)
+        if (ou >= i0 && ou < i0 + kTX && t >= ra && t < rb &&
+            !(ou >= A.ex_i0 && ou < A.ex_i1 && t >= A.ex_j0 && t < A.ex_j1))
           e_acc += 0.5 * w * pmubd * (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
         rec[9] = sw * lap[0];
         rec[10] = sw * lap[1];
@@ -320,7 +330,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
       const int r = cpi / kTX, c = cpi - r * kTX;
       const int i = i0 + c, j = j0 + r;
       const bool owned_row = (j >= A.r0);
-      bool active = (i < A.n_u) && (j < rb) && (j >= 0);
+      bool active = (i < A.n_u) && (j < rb) && (j >= 0) &&
+                    !(i >= A.sk_i0 && i < A.sk_i1 && j >= A.sk_j0 && j < A.sk_j1);
       if (task == 0 || task == 5) active = active && owned_row;        // group 0 / gradient: owned rows only
       active = active && ((task < 5) ? want_h : want_g);
       const int anchor_min = max(0, ra - 2);
@@ -486,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
   if (tid == 0) {
     double s = 0.0;
     for (int w = 0; w < kThreads / 32; ++w) s += red[w];
-    A.epart[((int64_t)item * A.nchunks_total + chunk) * A.nstrips + strip] = s;
+    A.epart[(int64_t)item * A.e_stride + (int64_t)chunk * A.nstrips + strip] = s;
   }
 }
 
@@ -838,19 +849,80 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
   return 0;
 }
 
+int tile_set_core(TileTables& tt, const Sheet& sh, const CoreTables& ct, const std::function<void*(size_t)>& dalloc) {
+  // rows k_core writes completely: every control point of its rectangle; the tile kernel still
+  // processes those whose forward blocks reach owned frame rows (their transposes live there)
+  tt.sk[0] = ct.CI0 + 2;
+  tt.sk[1] = ct.CI1 - 2;
+  tt.sk[2] = ct.RJ0;
+  tt.sk[3] = (ct.RJ1 == sh.r1) ? sh.r1 : ct.RJ1 - 2;
+  tt.ex[0] = ct.CI0; tt.ex[1] = ct.CI1; tt.ex[2] = ct.RJ0; tt.ex[3] = ct.RJ1;
+  std::vector<int2> chunks(tt.nchunks);
+  if (cudaMemcpy(chunks.data(), tt.chunks, sizeof(int2) * tt.nchunks, cudaMemcpyDeviceToHost) != cudaSuccess) return -6;
+  int base = 0;
+  for (int L = 0; L < 2; ++L) {
+    std::vector<int2> work;
+    for (int c = 0; c < tt.nch_l[L]; ++c) {
+      const int2 ch = chunks[base + c];
+      for (int st = 0; st < tt.nstrips; ++st) {
+        const int i0 = st * kTX, i1 = std::min(tt.n_u, i0 + kTX);
+        bool need = false;
+        for (int j = ch.x; j < ch.y && !need; ++j)
+          for (int i = i0; i < i1 && !need; ++i) {
+            const bool skipped = i >= tt.sk[0] && i < tt.sk[1] && j >= tt.sk[2] && j < tt.sk[3];
+            const bool anchor = i < tt.Su && j < tt.Sv;
+            const bool excl = i >= tt.ex[0] && i < tt.ex[1] && j >= tt.ex[2] && j < tt.ex[3];
+            if (!skipped || (anchor && !excl)) need = true;
+          }
+        if (need) work.push_back(make_int2(st, c));
+      }
+    }
+    tt.nwork_l[L] = (int)work.size();
+    if (!work.empty() && !upload(dalloc, &tt.work_l[L], work)) return -7;
+    base += tt.nch_l[L];
+  }
+  tt.core = 1;
+  return 0;
+}
+
 int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_E, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride,
-              cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc, const double* d_params) {
-  const int64_t need = (int64_t)nbatch * tt.nstrips * tt.nchunks;
-  (void)0;
-  if (need > tt.e_cap) {
-    void* p = dalloc(need * sizeof(double));
-    if (!p) return -7;
-    tt.e_part = static_cast<double*>(p);
-    tt.e_cap = need;
+              cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc, const double* d_params,
+              const CoreTables* ct) {
+  const bool core = ct && tt.core && ct->ok;
+  const int64_t tile_slots = (int64_t)tt.nstrips * tt.nchunks;
+  int core_nch = 0, core_slots = 0;
+  if (core) {
+    core_nch = core_pick_chunks(*ct, nbatch);
+    core_slots = core_ctas_per_item(*ct, core_nch);
+  }
+  const int64_t e_stride = tile_slots + core_slots;
+  double* epart = nullptr;
+  if (core) {
+    // tile slots of (strip, chunk) pairs outside the work lists are never written: keep them zero
+    const int64_t need = (int64_t)nbatch * e_stride;
+    if (need > tt.e_core_cap || core_slots != tt.core_ctas) {
+      void* p = dalloc(need * sizeof(double));
+      if (!p) return -7;
+      if (cudaMemset(p, 0, need * sizeof(double)) != cudaSuccess) return -6;
+      tt.e_part_core = static_cast<double*>(p);
+      tt.e_core_cap = need;
+      tt.core_ctas = core_slots;
+    }
+    epart = tt.e_part_core;
+  } else {
+    const int64_t need = (int64_t)nbatch * tile_slots;
+    if (need > tt.e_cap) {
+      void* p = dalloc(need * sizeof(double));
+      if (!p) return -7;
+      tt.e_part = static_cast<double*>(p);
+      tt.e_cap = need;
+    }
+    epart = tt.e_part;
   }
   TileArgs A;
-  A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride; A.epart = tt.e_part;
+  A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride; A.epart = epart;
+  A.e_stride = e_stride;
   A.n_u = tt.n_u; A.n_v = tt.n_v; A.Su = tt.Su; A.Sv = tt.Sv; A.r0 = tt.r0; A.r1 = tt.r1;
   A.xlo = sh.xlo; A.xhi = sh.xhi;
   A.nchunks_total = tt.nchunks; A.nstrips = tt.nstrips;
@@ -867,6 +939,11 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
   A.Mm = (int64_t)sh.mem.size(); A.Bm = (int64_t)sh.bend.size();
   A.lut = tt.lut; A.tasks = tt.tasks; A.ent = tt.ent; A.row_ptr = tt.row_ptr;
   A.params = d_params; A.detJ_ref = tt.detJ_ref; A.flags = flags;
+  const int big = 1 << 30;
+  A.sk_i0 = core ? tt.sk[0] : big; A.sk_i1 = core ? tt.sk[1] : big;
+  A.sk_j0 = core ? tt.sk[2] : big; A.sk_j1 = core ? tt.sk[3] : big;
+  A.ex_i0 = core ? tt.ex[0] : big; A.ex_i1 = core ? tt.ex[1] : big;
+  A.ex_j0 = core ? tt.ex[2] : big; A.ex_j1 = core ? tt.ex[3] : big;
   int nl = 0;
   int base = 0;
   for (int L = 0; L < 2; ++L) {   // interior chunks, then boundary chunks
@@ -875,17 +952,33 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     A.capb = tt.capb_l[L];
     A.chunk_base = base;
     A.chunks = tt.chunks + base;
-    dim3 grid(tt.nstrips, tt.nch_l[L], nbatch);
-    k_tile<<<grid, kThreads, tt.smem_l[L], st>>>(A);
-    ++nl;
+    if (core) {
+      A.work = tt.work_l[L];
+      if (tt.nwork_l[L] > 0) {
+        dim3 grid(tt.nwork_l[L], 1, nbatch);
+        k_tile<<<grid, kThreads, tt.smem_l[L], st>>>(A);
+        ++nl;
+      }
+    } else {
+      A.work = nullptr;
+      dim3 grid(tt.nstrips, tt.nch_l[L], nbatch);
+      k_tile<<<grid, kThreads, tt.smem_l[L], st>>>(A);
+      ++nl;
+    }
     base += tt.nch_l[L];
   }
+  if (core) {
+    const int rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, epart,
+                             e_stride, tile_slots, core_nch, d_params, tt.detJ_ref, st);
+    if (rc) return rc;
+    ++nl;
+  }
   if (d_E) {
-    k_energy_final<<<nbatch, 256, 0, st>>>(tt.e_part, tt.nstrips * tt.nchunks, d_E);
+    k_energy_final<<<nbatch, 256, 0, st>>>(epart, (int)e_stride, d_E);
     ++nl;
   }
   if (launches) *launches = nl;
-  return cudaGetLastError() == cudaSuccess ? 0 : -6;
+  return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
 }
 
 #ifdef BSF_PHASE_TIMERS

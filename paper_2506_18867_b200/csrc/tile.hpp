@@ -47,7 +47,23 @@ struct TileTables {
   int32_t* row_ptr = nullptr;      // owned rows' pattern (device copy)
   double* e_part = nullptr;        // per-CTA energy partials (grown on demand)
   int64_t e_cap = 0;
+  // frame mode (the interior core kernel covers a rectangle): CTAs of the tile kernel
+  // restricted to the (strip, chunk) pairs that touch the frame, per chunk list
+  int core = 0;
+  int sk[4] = {0, 0, 0, 0};        // skipped control points [i0,i1) x [j0,j1): rows written by k_core
+  int ex[4] = {0, 0, 0, 0};        // anchors whose energy k_core counts
+  int2* work_l[2] = {nullptr, nullptr};
+  int nwork_l[2] = {0, 0};
+  int core_ctas = 0;               // k_core CTAs per item (energy partial slots)
+  int core_nchunks = 0;
+  double* e_part_core = nullptr;   // [item][tile slots | core slots], tile slots of dropped pairs stay 0
+  int64_t e_core_cap = 0;
 };
+
+struct CoreTables;
+
+// Switch a tile table set to frame mode around the core rectangle (uploads the work lists).
+int tile_set_core(TileTables& tt, const Sheet& sh, const CoreTables& ct, const std::function<void*(size_t)>& dalloc);
 
 int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::function<void*(size_t)>& dalloc);
 
@@ -55,6 +71,6 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
 int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_E, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride,
               cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc,
-              const double* d_params = nullptr);
+              const double* d_params = nullptr, const CoreTables* ct = nullptr);
 
 }  // namespace bsf

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 import paper_2506_18867_b200 as B  # noqa: E402
 
-PATHS = [0, B.GENERIC_PATH]
+PATHS = [0, B.TILE_ONLY, B.GENERIC_PATH]   # core + frame tile kernels, tile kernel alone, generic
 
 
 def _gpu(sheet_obj, x, flags):
