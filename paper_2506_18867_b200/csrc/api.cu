@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <new>
@@ -12,6 +13,7 @@
 #include "dev.hpp"
 #include "host.hpp"
 #include "core.hpp"
+#include "frame.hpp"
 #include "tile.hpp"
 
 namespace bsf {
@@ -36,6 +38,7 @@ struct bsf_sheet {
   bool tile_ok = false;
   bsf::CoreTables ct;
   bool core_ok = false;
+  bsf::FrameTables ft;
   std::vector<void*> allocs;
   int last_launches = 0;
   bool host_only = false;
@@ -234,6 +237,10 @@ bsf_status bsf_create(int n_u, int n_v, const double* knots_u, const double* kno
         const int src = bsf::tile_set_core(h->tt, h->sh, h->ct, h->dalloc());
         if (src < 0) s = fail(BSF_E_OOM, "frame work lists");
         else h->core_ok = true;
+        if (h->core_ok && !getenv("BSF_FRAME_TILE")) {   // frame kernel (else: tile kernel on the frame)
+          const int frc = bsf::build_frame(h->sh, h->ct, h->ft, terr, h->dalloc());
+          if (frc < 0) s = fail(BSF_E_CUDA, terr);
+        }
       }
     }
   }
@@ -290,7 +297,7 @@ bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, doubl
   int rc;
   if (h->tile_ok && !(flags & BSF_GENERIC_PATH))
     rc = bsf::tile_eval(h->tt, h->sh, d_x, 0, m, flags, 1, d_energy, d_grad, 0, d_vals, 0, st, &nl, h->dalloc(), nullptr,
-                        (h->core_ok && !(flags & BSF_TILE_ONLY)) ? &h->ct : nullptr);
+                        (h->core_ok && !(flags & BSF_TILE_ONLY)) ? &h->ct : nullptr, &h->ft);
   else
     rc = bsf::generic_eval(h->gt, d_x, m, flags, nnzb, nrows, d_energy, d_grad, d_vals, st, &nl);
   h->last_launches = nl;
@@ -324,7 +331,7 @@ static bsf_status eval_batch_impl(bsf_handle h, int nbatch, const double* d_x, i
   if (h->tile_ok && !(flags & BSF_GENERIC_PATH)) {
     rc = bsf::tile_eval(h->tt, h->sh, d_x, x_stride, h->mat, flags, nbatch, d_energy, d_grad, grad_stride, d_vals,
                         vals_stride, st, &nl, h->dalloc(), d_params,
-                        (h->core_ok && !(flags & BSF_TILE_ONLY)) ? &h->ct : nullptr);
+                        (h->core_ok && !(flags & BSF_TILE_ONLY)) ? &h->ct : nullptr, &h->ft);
   } else {
     const int64_t nrows = (int64_t)(h->sh.r1 - h->sh.r0) * h->sh.n_u, nnzb = (int64_t)h->sh.col_idx.size();
     for (int b = 0; b < nbatch && rc == 0; ++b) {

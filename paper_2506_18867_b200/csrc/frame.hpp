@@ -1,0 +1,65 @@
+// Frame path: the control points around the core rectangle (DESIGN.md §5 "k_frame").
+//
+// Near the sheet's edges the quadrature configuration changes from control point to control point
+// (clipped dual cells, boundary spans with 2x3 / 3x3 Gauss rules, non-uniform end bases; PAPER.md:290-
+// 293, 571-573), so the frame is assembled from host-built per-block contribution lists instead of the
+// core's compile-time table.  The frame is cut into 4x4 tiles; one CTA per (tile, batch item) evaluates
+// the tile's incident quadrature points into shared memory and gathers every block of every tile row
+// in full (one thread per block; no transposes), so frame rows and core rows are written by disjoint
+// kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <functional>
+#include <string>
+
+#include "dev.hpp"
+#include "host.hpp"
+
+namespace bsf {
+
+struct CoreTables;
+
+namespace frame {
+constexpr int kMaxCp = 16;      // control points per tile (4 x 4)
+constexpr int kMaxNB = 25;      // blocks of a frame row
+constexpr int kSlots = kMaxNB + 1;          // threads per control point: one per block + the gradient
+constexpr int kThreads = ((kMaxCp * kSlots + 31) / 32) * 32;   // 416: one task per thread
+constexpr int kMChan = 27;      // membrane record: A~uu 6 | A~vv 6 | A~uv 9 | P~u 3 | P~v 3
+constexpr int kMCoef = 18;      // (dN/du Nv, Nu dN/dv) per window entry
+constexpr int kBChan = 12;      // bending record: sqrt(w mu) L_e 9 | sqrt(w mu) Lap phi 3
+}  // namespace frame
+
+struct FrameTables {
+  int ok = 0;
+  int ntiles = 0;
+  int maxM = 0, maxB = 0;      // per tile: membrane / bending points
+  size_t smem = 0;
+  int4* tile = nullptr;        // [ntiles] (i0, j0, tw | th << 8, ncp)
+  int32_t* tpm = nullptr;      // [ntiles+1] first membrane point of each tile
+  int32_t* tpb = nullptr;      // [ntiles+1] first bending point
+  int2* m_anc = nullptr;       // [M] anchor (ou, ov)
+  int32_t* m_own = nullptr;    // [M] 1 if the point's energy is counted by its tile
+  double* m_coef = nullptr;    // [M][18] parametric d-vectors (masked), [M] what at m_what
+  double* m_what = nullptr;
+  int2* b_anc = nullptr;
+  int32_t* b_own = nullptr;
+  double* b_coef = nullptr;    // [B][27] LA | LB | LC per window entry (masked)
+  double* b_what = nullptr;
+  uint2* lst = nullptr;        // [ntiles * kThreads] tasks: (first entry | count << 20, block index or ~a_loc)
+  uint32_t* ent = nullptr;     // entries: local point | ea << 10 | eb << 14 | bending << 18
+  int32_t* tent = nullptr;     // [ntiles+1] first entry of each tile
+};
+
+// Build the frame tables for the control points of the owned rows outside the core rectangle.
+// Returns 0 (ok = 1), 1 if not applicable (ok = 0), < 0 on errors.
+int build_frame(const Sheet& sh, const CoreTables& ct, FrameTables& ft, std::string& err,
+                const std::function<void*(size_t)>& dalloc);
+
+int frame_eval(const FrameTables& ft, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
+               int nbatch, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride, const int32_t* d_row_ptr,
+               double* e_part, int64_t e_stride, int64_t e_off, const double* d_params, const double* G4, double detJ,
+               cudaStream_t st);
+
+}  // namespace bsf

@@ -27,6 +27,7 @@
 
 #include "core.hpp"
 #include "fbw.cuh"
+#include "frame.hpp"
 #include "tile.hpp"
 
 namespace bsf {
@@ -888,8 +889,34 @@ int tile_set_core(TileTables& tt, const Sheet& sh, const CoreTables& ct, const s
 int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_E, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride,
               cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc, const double* d_params,
-              const CoreTables* ct) {
+              const CoreTables* ct, const FrameTables* ft) {
   const bool core = ct && tt.core && ct->ok;
+  if (core && ft && ft->ok) {
+    // frame kernel (full frame rows) + core kernel (full core rows): disjoint rows, one energy array
+    // [item][frame tiles | core CTAs]; every slot is written on every call
+    const int core_nch = core_pick_chunks(*ct, nbatch);
+    const int64_t e_stride = ft->ntiles + core_ctas_per_item(*ct, core_nch);
+    const int64_t need = (int64_t)nbatch * e_stride;
+    if (need > tt.e_cap) {
+      void* p = dalloc(need * sizeof(double));
+      if (!p) return -7;
+      tt.e_part = static_cast<double*>(p);
+      tt.e_cap = need;
+    }
+    int rc = frame_eval(*ft, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
+                        tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, st);
+    if (rc) return rc;
+    rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
+                   ft->ntiles, core_nch, d_params, tt.detJ_ref, st);
+    if (rc) return rc;
+    int nl = 2;
+    if (d_E) {
+      k_energy_final<<<nbatch, 256, 0, st>>>(tt.e_part, (int)e_stride, d_E);
+      ++nl;
+    }
+    if (launches) *launches = nl;
+    return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
+  }
   const int64_t tile_slots = (int64_t)tt.nstrips * tt.nchunks;
   int core_nch = 0, core_slots = 0;
   if (core) {

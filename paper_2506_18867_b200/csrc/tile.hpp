@@ -71,6 +71,7 @@ int build_tiles(const Sheet& sh, TileTables& tt, std::string& err, const std::fu
 int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_E, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride,
               cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc,
-              const double* d_params = nullptr, const CoreTables* ct = nullptr);
+              const double* d_params = nullptr, const CoreTables* ct = nullptr,
+              const struct FrameTables* ft = nullptr);
 
 }  // namespace bsf
