@@ -47,6 +47,9 @@ struct bsf_sheet {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
+    if (tt.side) cudaStreamDestroy(tt.side);
+    if (tt.ev_fork) cudaEventDestroy(tt.ev_fork);
+    if (tt.ev_join) cudaEventDestroy(tt.ev_join);
     for (void* p : allocs) cudaFree(p);
     cudaSetDevice(prev);
   }

@@ -59,7 +59,7 @@ struct FrameArgs {
   const int32_t* b_own;
   const double* b_coef;
   const double* b_what;
-  const uint2* lst;       // [ntiles * kThreads] per thread: (first | count << 20, output) with output = global
+  const uint2* lst;       // [ntiles * kTasks] per task: (first | count << 20, output) with output = global
                           // block index (row_ptr + rank) or ~a_loc for the gradient; sorted by count
   const uint32_t* ent;    // tile-relative contribution entries
   const int32_t* tent;    // [ntiles+1]
@@ -68,7 +68,7 @@ struct FrameArgs {
 constexpr int kPosD = 8 * 8 * 3;    // (tw + 4) * (th + 4) * 3 for 4x4 tiles
 constexpr int kMRec = 28;           // 27 channels + pad (16-B aligned records)
 
-__global__ void __launch_bounds__(kThreads, 2) k_frame(const FrameArgs A) {
+__global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
   extern __shared__ __align__(16) double fsm[];
   const int tile = blockIdx.x, item = blockIdx.y, tid = threadIdx.x;
   const int4 ti = A.tile[tile];
@@ -96,9 +96,6 @@ __global__ void __launch_bounds__(kThreads, 2) k_frame(const FrameArgs A) {
   }
   const double cuu = G00 * G00 + G01 * G01, cvv = G10 * G10 + G11 * G11, cuv = 2.0 * (G00 * G10 + G01 * G11);
 
-  // this thread's (control point, block) or (control point, gradient) task; the host sorted the tile's
-  // tasks by list length so that the lanes of a warp run loops of similar length
-  const uint2 task = A.lst[tile * kThreads + tid];
 
   // ---- 1. positions and the tile's contribution entries
   const int npos = (th + 4) * PW * 3;
@@ -185,7 +182,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_frame(const FrameArgs A) {
   }
   __syncthreads();
 
-  // ---- 3. gather: thread = (control point, block) or (control point, gradient)
+  // ---- 3. gather: tasks = (control point, block) or (control point, gradient), sorted by list length on
+  // the host; thread tid takes tasks tid, tid + kThreads, ... (lanes of a warp run loops of similar length)
+  for (int tk = tid; tk < kTasks; tk += kThreads) {
+  const uint2 task = A.lst[tile * kTasks + tk];
   const int first = task.x & 0xFFFFF, cnt = task.x >> 20;
   const int out = (int)task.y;
   if (cnt > 0 && out >= 0) {
@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_frame(const FrameArgs A) {
     }
     double* gd = A.g + item * A.gs + 3 * (int64_t)(~out);
     gd[0] = g0; gd[1] = g1; gd[2] = g2;
+  }
   }
   // ---- energy partial of this CTA
   const int lane = tid & 31, warp = tid >> 5;
@@ -356,8 +357,8 @@ int build_frame(const Sheet& sh, const CoreTables& ct, FrameTables& ft, std::str
       }
     }
     std::stable_sort(ttask.begin(), ttask.end(), [](const uint2& a, const uint2& b) { return (a.x >> 20) > (b.x >> 20); });
-    if ((int)ttask.size() > kThreads) { err = "frame: too many tasks per tile"; return -1; }
-    ttask.resize(kThreads, make_uint2(0u, 0u));
+    if ((int)ttask.size() > kTasks) { err = "frame: too many tasks per tile"; return -1; }
+    ttask.resize(kTasks, make_uint2(0u, 0u));
     tasks.insert(tasks.end(), ttask.begin(), ttask.end());
     if (loc[0].size() > 1023 || loc[1].size() > 1023) { err = "frame: too many points per tile"; return -1; }
     std::vector<int> mg(loc[0].size()), bg(loc[1].size());

@@ -25,7 +25,8 @@ namespace frame {
 constexpr int kMaxCp = 16;      // control points per tile (4 x 4)
 constexpr int kMaxNB = 25;      // blocks of a frame row
 constexpr int kSlots = kMaxNB + 1;          // threads per control point: one per block + the gradient
-constexpr int kThreads = ((kMaxCp * kSlots + 31) / 32) * 32;   // 416: one task per thread
+constexpr int kTasks = kMaxCp * kSlots;     // 416 task slots per tile
+constexpr int kThreads = 224;               // 7 warps, <= 2 tasks per thread, 4 CTAs per SM
 constexpr int kMChan = 27;      // membrane record: A~uu 6 | A~vv 6 | A~uv 9 | P~u 3 | P~v 3
 constexpr int kMCoef = 18;      // (dN/du Nv, Nu dN/dv) per window entry
 constexpr int kBChan = 12;      // bending record: sqrt(w mu) L_e 9 | sqrt(w mu) Lap phi 3
@@ -47,7 +48,7 @@ struct FrameTables {
   int32_t* b_own = nullptr;
   double* b_coef = nullptr;    // [B][27] LA | LB | LC per window entry (masked)
   double* b_what = nullptr;
-  uint2* lst = nullptr;        // [ntiles * kThreads] tasks: (first entry | count << 20, block index or ~a_loc)
+  uint2* lst = nullptr;        // [ntiles * kTasks] tasks: (first entry | count << 20, block index or ~a_loc)
   uint32_t* ent = nullptr;     // entries: local point | ea << 10 | eb << 14 | bending << 18
   int32_t* tent = nullptr;     // [ntiles+1] first entry of each tile
 };

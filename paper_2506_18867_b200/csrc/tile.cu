@@ -903,12 +903,24 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
       tt.e_part = static_cast<double*>(p);
       tt.e_cap = need;
     }
+    // the two kernels write disjoint rows: the frame runs on a side stream forked from / joined to st
+    // (event fork-join, CUDA-graph capturable)
+    if (!tt.side) {
+      if (cudaStreamCreateWithFlags(&tt.side, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaEventCreateWithFlags(&tt.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&tt.ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return -6;
+    }
+    if (cudaEventRecord(tt.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(tt.side, tt.ev_fork, 0) != cudaSuccess)
+      return -6;
     int rc = frame_eval(*ft, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
-                        tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, st);
+                        tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, tt.side);
     if (rc) return rc;
     rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
                    ft->ntiles, core_nch, d_params, tt.detJ_ref, st);
     if (rc) return rc;
+    if (cudaEventRecord(tt.ev_join, tt.side) != cudaSuccess || cudaStreamWaitEvent(st, tt.ev_join, 0) != cudaSuccess)
+      return -6;
     int nl = 2;
     if (d_E) {
       k_energy_final<<<nbatch, 256, 0, st>>>(tt.e_part, (int)e_stride, d_E);

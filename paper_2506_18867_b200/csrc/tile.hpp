@@ -58,6 +58,8 @@ struct TileTables {
   int core_nchunks = 0;
   double* e_part_core = nullptr;   // [item][tile slots | core slots], tile slots of dropped pairs stay 0
   int64_t e_core_cap = 0;
+  cudaStream_t side = nullptr;     // frame kernel stream (fork / join with the caller's stream)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 struct CoreTables;
