@@ -66,7 +66,8 @@ constexpr int kCstBeta = 18;    // [23] bending Hessian blocks beta_ab
 constexpr int kCstS = 41;       // [72] S[set][e][2]
 constexpr int kCstRed = 113;    // [24] energy reduction
 constexpr int kCstW = 137;      // [5]  parametric weights of the sets and of the bending points
-constexpr int kCstN = 142;
+constexpr int kCstP = 142;      // [10] G00 G01 G10 G11 detJ mu1 mu2 mush mubd w_b of this item
+constexpr int kCstN = 152;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -233,7 +234,7 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
     rec[kKH] = lap[1];
     rec[2 * kKH] = lap[2];
     if (p >= P.i0 && p < P.i1 && q >= P.ja && q < P.jb)
-      return 0.5 * P.wb * P.mubd * (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
+      return 0.5 * cst[kCstP + 9] * cst[kCstP + 8] * (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
     return 0.0;
   }
   const int r = it >= nmem, mi = it - r * nmem, q = q0 + r;
@@ -257,21 +258,21 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
 #pragma unroll
       for (int c = 0; c < 3; ++c) { Fu[c] = fma(C[c], du, Fu[c]); Fv[c] = fma(C[c], dv, Fv[c]); }
     }
-  const double wq = cst[kCstW + set] * P.det;
+  const double wq = cst[kCstW + set] * cst[kCstP + 4];
   double f1[3], f2[3];   // F_beta = sum_mu F~_mu G_mu,beta
   if (P.diagG) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * P.G00; f2[c] = Fv[c] * P.G11; }
+    for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * cst[kCstP + 0]; f2[c] = Fv[c] * cst[kCstP + 3]; }
   } else {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * P.G00 + Fv[c] * P.G10; f2[c] = Fu[c] * P.G01 + Fv[c] * P.G11; }
+    for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * cst[kCstP + 0] + Fv[c] * cst[kCstP + 2]; f2[c] = Fu[c] * cst[kCstP + 1] + Fv[c] * cst[kCstP + 3]; }
   }
   FSpace o;
-  fbw_point(f1, f2, P.mu1, P.mu2, P.mush, P.project, o);
+  fbw_point(f1, f2, cst[kCstP + 5], cst[kCstP + 6], cst[kCstP + 7], P.project, o);
   double* rec = row + set * kSetD + k;
   if (P.diagG) {   // A~uu = w G00^2 A11, A~vv = w G11^2 A22, A~uv = w G00 G11 A12, P~ = w (G00 P1, G11 P2)
-    const double su = wq * P.G00, sv = wq * P.G11;
-    const double auu = su * P.G00, avv = sv * P.G11, auv = su * P.G11;
+    const double su = wq * cst[kCstP + 0], sv = wq * cst[kCstP + 3];
+    const double auu = su * cst[kCstP + 0], avv = sv * cst[kCstP + 3], auv = su * cst[kCstP + 3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       rec[(21 + c) * kKH] = su * o.P1[c];
@@ -290,13 +291,13 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
   // P~_mu = w sum_beta G_mu,beta P_beta
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    rec[(21 + c) * kKH] = wq * (P.G00 * o.P1[c] + P.G01 * o.P2[c]);
-    rec[(24 + c) * kKH] = wq * (P.G10 * o.P1[c] + P.G11 * o.P2[c]);
+    rec[(21 + c) * kKH] = wq * (cst[kCstP + 0] * o.P1[c] + cst[kCstP + 1] * o.P2[c]);
+    rec[(24 + c) * kKH] = wq * (cst[kCstP + 2] * o.P1[c] + cst[kCstP + 3] * o.P2[c]);
   }
   // A~_mu,nu = w sum_{beta,gamma} G_mu,beta G_nu,gamma A_beta,gamma
-  const double a11 = wq * P.G00 * P.G00, a12 = wq * P.G00 * P.G01, a22 = wq * P.G01 * P.G01;
-  const double b11 = wq * P.G10 * P.G10, b12 = wq * P.G10 * P.G11, b22 = wq * P.G11 * P.G11;
-  const double c11 = wq * P.G00 * P.G10, c12 = wq * P.G00 * P.G11, c21 = wq * P.G01 * P.G10, c22 = wq * P.G01 * P.G11;
+  const double a11 = wq * cst[kCstP + 0] * cst[kCstP + 0], a12 = wq * cst[kCstP + 0] * cst[kCstP + 1], a22 = wq * cst[kCstP + 1] * cst[kCstP + 1];
+  const double b11 = wq * cst[kCstP + 2] * cst[kCstP + 2], b12 = wq * cst[kCstP + 2] * cst[kCstP + 3], b22 = wq * cst[kCstP + 3] * cst[kCstP + 3];
+  const double c11 = wq * cst[kCstP + 0] * cst[kCstP + 2], c12 = wq * cst[kCstP + 0] * cst[kCstP + 3], c21 = wq * cst[kCstP + 1] * cst[kCstP + 2], c22 = wq * cst[kCstP + 1] * cst[kCstP + 3];
 #pragma unroll
   for (int r3 = 0; r3 < 3; ++r3)
 #pragma unroll
@@ -354,6 +355,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
     cst[kCstLw + tid] = P.wb * P.mubd * L;
   }
   if (tid < 72) cst[kCstS + tid] = A.tabs[tid];
+  if (tid == 0) {   // per-item doubles of the point phase live in shared memory (registers go to the gather)
+    cst[kCstP + 0] = P.G00; cst[kCstP + 1] = P.G01; cst[kCstP + 2] = P.G10; cst[kCstP + 3] = P.G11;
+    cst[kCstP + 4] = P.det; cst[kCstP + 5] = P.mu1; cst[kCstP + 6] = P.mu2; cst[kCstP + 7] = P.mush;
+    cst[kCstP + 8] = P.mubd; cst[kCstP + 9] = P.wb;
+  }
   if (tid < 5) cst[kCstW + tid] = A.tabs[99 + tid];
   const uint32_t bar = smem_u32(mbar);
   if (tid == 0) {
