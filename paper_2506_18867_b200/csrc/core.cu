@@ -109,10 +109,17 @@ __device__ __forceinline__ void static_for(F&& f) {
 // (d = dq + 2): lane's record pointer for knot row j+h+dq for even / odd knot-column offsets dp.
 // Diagonal roles (r == c) add the constant bending blocks and gather g_a[r]; bb0 / bb1 address the
 // bending arrays (channel r).  Staging stores wait on `bar` (previous bulk store has read the buffer).
+template <int IMM>
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(addr), "n"(IMM));
+  return v;
+}
+
 template <int PI>
-__device__ __forceinline__ void gather_role(const double (&S)[4][9][2], const double* const (&base0)[4],
-                                            const double* const (&base1)[4], const double* const (&bb0)[3],
-                                            const double* const (&bb1)[3], int o_uu, int o_vv, int o_rc, int o_cr,
+__device__ __forceinline__ void gather_role(const double (&S)[4][9][2], const uint32_t (&base0)[4],
+                                            const uint32_t (&base1)[4], const double* const (&bb0)[3],
+                                            const double* const (&bb1)[3], int o_rc, int o_cr,
                                             int o_pu, int o_pv, bool diag, const double* __restrict__ cst,
                                             double* st_lane, double* gdst, bool active, uint32_t bar,
                                             uint32_t parity) {
@@ -124,8 +131,10 @@ __device__ __forceinline__ void gather_role(const double (&S)[4][9][2], const do
     constexpr int s = decltype(SI)::value;
     constexpr Template T = make_template(PI);
     constexpr int dp = T.s_dp[s], dq = T.s_dq[s], set = T.s_set[s], ea = T.s_ea[s];
-    const double* b = ((dp & 1) ? base1[dq + 2] : base0[dq + 2]) + set * kSetD + ((dp + 2) >> 1);
-    const double auu = b[o_uu], avv = b[o_vv], arc = b[o_rc], acr = b[o_cr];
+    constexpr int imm = 8 * (set * kSetD + ((dp + 2) >> 1));   // byte offset within the knot row
+    const uint32_t bu = (dp & 1) ? base1[dq + 2] : base0[dq + 2];   // shared byte address (+ role uu)
+    const double auu = lds_f64<imm>(bu), avv = lds_f64<imm + 8 * 6 * kKH>(bu);
+    const double arc = lds_f64<imm>(bu + o_rc), acr = lds_f64<imm>(bu + o_cr);
     const double dau = S[set][ea][0], dav = S[set][ea][1];
     const double Yu = fma(dau, auu, dav * acr), Yv = fma(dau, arc, dav * avv);
     static_for<T.s_c0[s], T.s_c0[s] + T.s_nc[s]>([&](auto CI) {
@@ -134,7 +143,7 @@ __device__ __forceinline__ void gather_role(const double (&S)[4][9][2], const do
       constexpr int k = T2.c_blk[c], eb = T2.c_eb[c];
       acc[k] = fma(S[set][eb][0], Yu, fma(S[set][eb][1], Yv, acc[k]));
     });
-    if (diag) g = fma(dau, b[o_pu], fma(dav, b[o_pv], g));
+    if (diag) g = fma(dau, lds_f64<imm>(bu + o_pu), fma(dav, lds_f64<imm>(bu + o_pv), g));
   });
   if (diag) {
     static_for<0, kBSlots>([&](auto KI) {
@@ -448,12 +457,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
             const int sigma = (PI + jr + i0) & 1;
             const int i = i0 + 2 * m + sigma;
             const bool active = (i < i1) && (jr < jb);
-            const double* base0[4];
-            const double* base1[4];
+            uint32_t base0[4], base1[4];   // shared byte addresses of the role's A~uu channel
 #pragma unroll
             for (int d = 0; d < 4; ++d) {
-              base0[d] = rowp[d];
-              base1[d] = rowp[d] + sigma;
+              base0[d] = smem_u32(rowp[d]) + 8 * o_uu;
+              base1[d] = base0[d] + 8 * sigma;
             }
             const double* bb0[3];
             const double* bb1[3];
@@ -474,10 +482,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
             double* gdst = (gout && diag) ? gout + ((int64_t)(jr - A.r0) * A.n_u + i) * 3 + rr : nullptr;
             const uint32_t par = k & 1;
             if (PI == 0)
-              gather_role<0>(A.S, base0, base1, bb0, bb1, o_uu, o_vv, o_rc, o_cr, o_pu, o_pv, diag, cst, st_lane,
+              gather_role<0>(A.S, base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
+                             8 * (o_pv - o_uu), diag, cst, st_lane,
                              gdst, active, bar, par);
             else
-              gather_role<1>(A.S, base0, base1, bb0, bb1, o_uu, o_vv, o_rc, o_cr, o_pu, o_pv, diag, cst, st_lane,
+              gather_role<1>(A.S, base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
+                             8 * (o_pv - o_uu), diag, cst, st_lane,
                              gdst, active, bar, par);
           }
         }
