@@ -56,7 +56,6 @@ struct CoreArgs {
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
   const double* tabs;      // device [104]: S[4][9][2] | LA[9] | LB[9] | LC[9] | what[5]
   double what[5];
-  double S[4][9][2];       // per-set basis coefficients, compile-time indexed in the gather
 };
 
 // shared constants block (doubles)
@@ -117,7 +116,7 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
 }
 
 template <int PI>
-__device__ __forceinline__ void gather_role(const double (&S)[4][9][2], const uint32_t (&base0)[4],
+__device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
                                             const uint32_t (&base1)[4], const double* const (&bb0)[3],
                                             const double* const (&bb1)[3], int o_rc, int o_cr,
                                             int o_pu, int o_pv, bool diag, const double* __restrict__ cst,
@@ -135,13 +134,14 @@ __device__ __forceinline__ void gather_role(const double (&S)[4][9][2], const ui
     const uint32_t bu = (dp & 1) ? base1[dq + 2] : base0[dq + 2];   // shared byte address (+ role uu)
     const double auu = lds_f64<imm>(bu), avv = lds_f64<imm + 8 * 6 * kKH>(bu);
     const double arc = lds_f64<imm>(bu + o_rc), acr = lds_f64<imm>(bu + o_cr);
-    const double dau = S[set][ea][0], dav = S[set][ea][1];
+    constexpr double dau = kSetTable.v[set][ea][0], dav = kSetTable.v[set][ea][1];
     const double Yu = fma(dau, auu, dav * acr), Yv = fma(dau, arc, dav * avv);
     static_for<T.s_c0[s], T.s_c0[s] + T.s_nc[s]>([&](auto CI) {
       constexpr int c = decltype(CI)::value;
       constexpr Template T2 = make_template(PI);
       constexpr int k = T2.c_blk[c], eb = T2.c_eb[c];
-      acc[k] = fma(S[set][eb][0], Yu, fma(S[set][eb][1], Yv, acc[k]));
+      constexpr double bu = kSetTable.v[set][eb][0], bv = kSetTable.v[set][eb][1];
+      acc[k] = fma(bu, Yu, fma(bv, Yv, acc[k]));
     });
     if (diag) g = fma(dau, lds_f64<imm>(bu + o_pu), fma(dav, lds_f64<imm>(bu + o_pv), g));
   });
@@ -482,11 +482,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
             double* gdst = (gout && diag) ? gout + ((int64_t)(jr - A.r0) * A.n_u + i) * 3 + rr : nullptr;
             const uint32_t par = k & 1;
             if (PI == 0)
-              gather_role<0>(A.S, base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
+              gather_role<0>(base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
                              8 * (o_pv - o_uu), diag, cst, st_lane,
                              gdst, active, bar, par);
             else
-              gather_role<1>(A.S, base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
+              gather_role<1>(base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
                              8 * (o_pv - o_uu), diag, cst, st_lane,
                              gdst, active, bar, par);
           }
@@ -607,7 +607,7 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
         const Point& P = sh.mem[mi[k]];
         const int set = set_of(P);
         if (set < 0 || have[set]) continue;
-        point_du_dv(P, ct.S[set]);
+        std::memcpy(ct.S[set], kSetTable.v[set], sizeof(ct.S[set]));
         ct.what[set] = P.what;
         have[set] = true;
       }
@@ -805,7 +805,7 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
   A.mubd = (flags & 4) ? 0.0 : mat.mu_bd;
   A.tabs = ct.d_tabs;
   std::memcpy(A.what, ct.what, sizeof(A.what));
-  std::memcpy(A.S, ct.S, sizeof(A.S));
+
   dim3 grid(ct.nstrips, nchunks, nbatch);
   k_core<<<grid, kThreads, ct.smem, st>>>(A);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;

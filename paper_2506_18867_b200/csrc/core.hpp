@@ -100,6 +100,36 @@ constexpr Template make_template(int pi) {
   return T;
 }
 
+// Per-set parametric d-vectors (dN/du Nv, Nu dN/dv) of the 9 window entries of an interior point:
+// uniform quadratic bases on a span with local coordinate x, N = ((1-x)^2/2, (1+2x-2x^2)/2, x^2/2),
+// N' = (x-1, 1-2x, x); at a knot (right limit, x = 0) N = (1/2, 1/2, 0), N' = (-1, 1, 0); the Gauss
+// pair of a dual cell sits at x = g (span q / p) and x = 1-g (span q-1 / p-1), g = sqrt(3)/6 (the
+// rule's node literal, host.cpp).  Compile-time, so the gather's coefficients are immediates; create
+// time verifies every interior point's own tables against it (relative 1e-12).
+struct SetTable { double v[4][9][2]; };
+constexpr double kGauss = 0.28867513459481288225;
+constexpr SetTable make_set_table() {
+  SetTable T{};
+  const double xs[2] = {1.0 - kGauss, kGauss};   // set w = 0 (minus), 1 (plus)
+  for (int set = 0; set < 4; ++set) {
+    const double x = xs[set & 1];
+    const double Ng[3] = {0.5 * (1.0 - x) * (1.0 - x), 0.5 * (1.0 + 2.0 * x - 2.0 * x * x), 0.5 * x * x};
+    const double dg[3] = {x - 1.0, 1.0 - 2.0 * x, x};
+    const double Nk[3] = {0.5, 0.5, 0.0}, dk[3] = {-1.0, 1.0, 0.0};
+    for (int e = 0; e < 9; ++e) {
+      const int iu = e % 3, jv = e / 3;
+      const bool V = set < 2;   // V: u on the knot line, v at the Gauss node; H: the reverse
+      const double Nu = V ? Nk[iu] : Ng[iu], du = V ? dk[iu] : dg[iu];
+      const double Nv = V ? Ng[jv] : Nk[jv], dv = V ? dg[jv] : dk[jv];
+      const bool in = V ? iu < 2 : jv < 2;
+      T.v[set][e][0] = in ? du * Nv : 0.0;
+      T.v[set][e][1] = in ? Nu * dv : 0.0;
+    }
+  }
+  return T;
+}
+constexpr SetTable kSetTable = make_set_table();
+
 // Bending incidence: knots (i+dp, j+dq), dp, dq in [-2, 0], a at window entry (-dp, -dq) != (2, 2).
 constexpr int kBSlots = 8;
 constexpr int bslot_dp(int k) { return -(k % 3); }   // slot k: a sits at window entry k of the point
