@@ -59,8 +59,9 @@ struct FrameArgs {
   const int32_t* b_own;
   const double* b_coef;
   const double* b_what;
-  const uint2* lst;       // [ntiles * kTasks] per task: (first | count << 20, output) with output = global
-                          // block index (row_ptr + rank) or ~a_loc for the gradient; sorted by count
+  const uint4* lst;       // [ntiles * kTasks] per task: (first | count << 20, output, transposed output, 0):
+                          // output = global block index (row_ptr + rank) or ~a_loc for the gradient;
+                          // transposed output = block of H_ab^T in row b (frame pairs computed once) or -1
   const uint32_t* ent;    // tile-relative contribution entries
   const int32_t* tent;    // [ntiles+1]
 };
@@ -185,9 +186,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
   // ---- 3. gather: tasks = (control point, block) or (control point, gradient), sorted by list length on
   // the host; thread tid takes tasks tid, tid + kThreads, ... (lanes of a warp run loops of similar length)
   for (int tk = tid; tk < kTasks; tk += kThreads) {
-  const uint2 task = A.lst[tile * kTasks + tk];
+  const uint4 task = A.lst[tile * kTasks + tk];
   const int first = task.x & 0xFFFFF, cnt = task.x >> 20;
-  const int out = (int)task.y;
+  const int out = (int)task.y, outT = (int)task.z;
   if (cnt > 0 && out >= 0) {
     double h[9];
 #pragma unroll
@@ -219,6 +220,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
       double* dst = A.vals + item * A.vs + (int64_t)out * 9;
 #pragma unroll
       for (int k = 0; k < 9; ++k) dst[k] = h[k];
+      if (outT >= 0) {   // H_ba = H_ab^T (b a later frame control point)
+        double* dt = A.vals + item * A.vs + (int64_t)outT * 9;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) dt[k] = h[3 * (k % 3) + k / 3];
+      }
     }
   } else if (out < 0 && A.g) {
     double g0 = 0.0, g1 = 0.0, g2 = 0.0;
@@ -297,7 +303,7 @@ int build_frame(const Sheet& sh, const CoreTables& ct, FrameTables& ft, std::str
     for (size_t k = 0; k < sh.bend.size(); ++k) bi[fb[sh.bend[k].ov * Su + sh.bend[k].ou]++] = (int32_t)k;
   }
   std::vector<int4> tinfo;
-  std::vector<uint2> tasks;
+  std::vector<uint4> tasks;
   std::vector<int32_t> tpm{0}, tpb{0}, tent{0};
   std::vector<int2> m_anc, b_anc;
   std::vector<int32_t> m_own, b_own;
@@ -310,7 +316,7 @@ int build_frame(const Sheet& sh, const CoreTables& ct, FrameTables& ft, std::str
     std::map<int, int> loc[2];   // global point -> local index, per kind
     auto in_tile = [&](int i, int j) { return i >= T.i0 && i < T.i1 && j >= T.j0 && j < T.j1; };
     const size_t tbase = ent.size();
-    std::vector<uint2> ttask;
+    std::vector<uint4> ttask;
     for (int slot = 0; slot < ncp; ++slot) {
       const int i = T.i0 + slot % tw, j = T.j0 + slot / tw;
       const int64_t al = (int64_t)(j - r0) * nu + i;
@@ -347,18 +353,34 @@ int build_frame(const Sheet& sh, const CoreTables& ct, FrameTables& ft, std::str
             }
           }
       }
+      const int32_t a_glob = j * nu + i;
       for (int k = 0; k < kSlots; ++k) {
         if (k < kMaxNB && k >= nb) continue;
+        int32_t outT = -1;
+        if (k < kMaxNB) {   // frame-frame pairs: computed once, by the earlier control point
+          const int32_t b = c0[k];
+          const int bi = b % nu, bj = b / nu;
+          const bool bframe = bj >= r0 && bj < r1 && !(bi >= ct.CI0 && bi < ct.CI1 && bj >= ct.RJ0 && bj < ct.RJ1);
+          if (bframe && b < a_glob) continue;
+          if (bframe && b > a_glob) {
+            const int64_t bl = (int64_t)(bj - r0) * nu + bi;
+            const int32_t* d0 = sh.col_idx.data() + sh.row_ptr[bl];
+            const int32_t* d1 = sh.col_idx.data() + sh.row_ptr[bl + 1];
+            const int32_t* pa = std::lower_bound(d0, d1, a_glob);
+            if (pa == d1 || *pa != a_glob) { err = "frame: pattern not symmetric"; return -1; }
+            outT = sh.row_ptr[bl] + (int32_t)(pa - d0);
+          }
+        }
         const size_t f = ent.size() - tbase;
         if (f >= (1u << 20) || per[k].size() >= 4096) { err = "frame: program too long"; return -1; }
         const int32_t outi = (k == kSlots - 1) ? ~(int32_t)al : sh.row_ptr[al] + k;
-        ttask.push_back(make_uint2((uint32_t)f | ((uint32_t)per[k].size() << 20), (uint32_t)outi));
+        ttask.push_back(make_uint4((uint32_t)f | ((uint32_t)per[k].size() << 20), (uint32_t)outi, (uint32_t)outT, 0u));
         ent.insert(ent.end(), per[k].begin(), per[k].end());
       }
     }
-    std::stable_sort(ttask.begin(), ttask.end(), [](const uint2& a, const uint2& b) { return (a.x >> 20) > (b.x >> 20); });
+    std::stable_sort(ttask.begin(), ttask.end(), [](const uint4& a, const uint4& b) { return (a.x >> 20) > (b.x >> 20); });
     if ((int)ttask.size() > kTasks) { err = "frame: too many tasks per tile"; return -1; }
-    ttask.resize(kTasks, make_uint2(0u, 0u));
+    ttask.resize(kTasks, make_uint4(0u, 0u, 0xFFFFFFFFu, 0u));
     tasks.insert(tasks.end(), ttask.begin(), ttask.end());
     if (loc[0].size() > 1023 || loc[1].size() > 1023) { err = "frame: too many points per tile"; return -1; }
     std::vector<int> mg(loc[0].size()), bg(loc[1].size());

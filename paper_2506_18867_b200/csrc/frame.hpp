@@ -48,7 +48,7 @@ struct FrameTables {
   int32_t* b_own = nullptr;
   double* b_coef = nullptr;    // [B][27] LA | LB | LC per window entry (masked)
   double* b_what = nullptr;
-  uint2* lst = nullptr;        // [ntiles * kTasks] tasks: (first entry | count << 20, block index or ~a_loc)
+  uint4* lst = nullptr;        // [ntiles * kTasks] tasks: (first | count << 20, block or ~a_loc, transposed block or -1, 0)
   uint32_t* ent = nullptr;     // entries: local point | ea << 10 | eb << 14 | bending << 18
   int32_t* tent = nullptr;     // [ntiles+1] first entry of each tile
 };
