@@ -80,8 +80,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
   double* mch = pos + kPosD;               // [maxM][kMRec]  A~uu 6 | A~vv 6 | A~uv 9 | P~u 3 | P~v 3
   double* mcf = mch + kMRec * maxM;        // [maxM][18]     (du, dv) per window entry
   double* bch = mcf + kMCoef * maxM;       // [maxB][12]     sqrt(w mu) L_e 9 | sqrt(w mu) Lap phi 3
-  double* red = bch + kBChan * maxB;       // [16]
-  uint32_t* sent = reinterpret_cast<uint32_t*>(red + 16);   // [tile entries]
+  double* red = bch + kBChan * maxB;       // [16] energy reduction
+  double* kc = red + 16;                   // [16] per-item constants (kept out of registers)
+  uint32_t* sent = reinterpret_cast<uint32_t*>(kc + 16);   // [tile entries]
   const double* __restrict__ x = A.x + item * A.xs;
 
   // ---- per-item affine map and stiffness
@@ -95,7 +96,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
     mush = (A.flags & 2) ? 0.0 : pp[7];
     mubd = (A.flags & 4) ? 0.0 : pp[8];
   }
-  const double cuu = G00 * G00 + G01 * G01, cvv = G10 * G10 + G11 * G11, cuv = 2.0 * (G00 * G10 + G01 * G11);
+  if (tid == 0) {
+    kc[0] = G00; kc[1] = G01; kc[2] = G10; kc[3] = G11; kc[4] = det; kc[5] = mu1; kc[6] = mu2; kc[7] = mush;
+    kc[8] = mubd; kc[9] = G00 * G00 + G01 * G01; kc[10] = G10 * G10 + G11 * G11; kc[11] = 2.0 * (G00 * G10 + G01 * G11);
+  }
 
 
   // ---- 1. positions and the tile's contribution entries
@@ -134,49 +138,56 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) { Fu[c] = fma(C[c], du, Fu[c]); Fv[c] = fma(C[c], dv, Fv[c]); }
       }
-      const double wq = A.m_what[p] * det;
+      const double wq = A.m_what[p] * kc[4];
       double f1[3], f2[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * G00 + Fv[c] * G10; f2[c] = Fu[c] * G01 + Fv[c] * G11; }
-      FSpace o;
-      fbw_point(f1, f2, mu1, mu2, mush, A.project != 0, o);
-      if (A.m_own[p]) e_acc += wq * o.psi;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        rec[21 + c] = wq * (G00 * o.P1[c] + G01 * o.P2[c]);
-        rec[24 + c] = wq * (G10 * o.P1[c] + G11 * o.P2[c]);
-      }
-      const double a11 = wq * G00 * G00, a12 = wq * G00 * G01, a22 = wq * G01 * G01;
-      const double b11 = wq * G10 * G10, b12 = wq * G10 * G11, b22 = wq * G11 * G11;
-      const double c11 = wq * G00 * G10, c12 = wq * G00 * G11, c21 = wq * G01 * G10, c22 = wq * G01 * G11;
-#pragma unroll
-      for (int r3 = 0; r3 < 3; ++r3)
-#pragma unroll
-        for (int c3 = r3; c3 < 3; ++c3) {
+      for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * kc[0] + Fv[c] * kc[2]; f2[c] = Fu[c] * kc[1] + Fv[c] * kc[3]; }
+      double psi;
+      const auto emit_p = [&](int c, double P1c, double P2c) {   // P~_mu = w sum_beta G_mu,beta P_beta
+        rec[21 + c] = wq * (kc[0] * P1c + kc[1] * P2c);
+        rec[24 + c] = wq * (kc[2] * P1c + kc[3] * P2c);
+      };
+      if (kc[1] == 0.0 && kc[2] == 0.0) {   // axis-aligned rest map: A~ by entrywise scaling
+        const double auu = wq * kc[0] * kc[0], avv = wq * kc[3] * kc[3], auv = wq * kc[0] * kc[3];
+        psi = fbw_emit(f1, f2, kc[5], kc[6], kc[7], A.project != 0, emit_p,
+                       [&](int r3, int c3, double A11, double A22, double A12rc, double A12cr) {
           const int e6 = sym3(r3, c3);
-          const double A11 = o.A11[e6], A22 = o.A22[e6];
-          const double A12rc = o.A12[3 * r3 + c3], A12cr = o.A12[3 * c3 + r3];
+          rec[e6] = auu * A11;
+          rec[6 + e6] = avv * A22;
+          rec[12 + 3 * r3 + c3] = auv * A12rc;
+          if (r3 != c3) rec[12 + 3 * c3 + r3] = auv * A12cr;
+        });
+      } else {
+        const double wG00 = wq * kc[0], wG01 = wq * kc[1], wG10 = wq * kc[2], wG11 = wq * kc[3];
+        const double a11 = wG00 * kc[0], a12 = wG00 * kc[1], a22 = wG01 * kc[1];
+        const double b11 = wG10 * kc[2], b12 = wG10 * kc[3], b22 = wG11 * kc[3];
+        const double c11 = wG00 * kc[2], c12 = wG00 * kc[3], c21 = wG01 * kc[2], c22 = wG01 * kc[3];
+        psi = fbw_emit(f1, f2, kc[5], kc[6], kc[7], A.project != 0, emit_p,
+                       [&](int r3, int c3, double A11, double A22, double A12rc, double A12cr) {
+          const int e6 = sym3(r3, c3);
           rec[e6] = a11 * A11 + a12 * (A12rc + A12cr) + a22 * A22;
           rec[6 + e6] = b11 * A11 + b12 * (A12rc + A12cr) + b22 * A22;
           rec[12 + 3 * r3 + c3] = c11 * A11 + c12 * A12rc + c21 * A12cr + c22 * A22;
           if (r3 != c3) rec[12 + 3 * c3 + r3] = c11 * A11 + c12 * A12cr + c21 * A12rc + c22 * A22;
-        }
+        });
+      }
+      if (A.m_own[p]) e_acc += wq * psi;
     } else {
       const int tb = t - M, q = b0 + tb;
       const int2 an = A.b_anc[q];
       const double* cf = A.b_coef + 27 * (int64_t)q;
-      const double w = A.b_what[q] * det;
-      const double sw = sqrt(w * mubd);
+      const double w = A.b_what[q] * kc[4];
+      const double sw = sqrt(w * kc[8]);
       double* rec = bch + tb * kBChan;
       double lap[3] = {0, 0, 0};
 #pragma unroll
       for (int e = 0; e < 9; ++e) {
-        const double L = cuu * cf[e] + cvv * cf[9 + e] + cuv * cf[18 + e];
+        const double L = kc[9] * cf[e] + kc[10] * cf[9 + e] + kc[11] * cf[18 + e];
         const double* C = pos + ((an.y + e / 3 - (j0 - 2)) * PW + (an.x + e % 3 - (i0 - 2))) * 3;
         lap[0] = fma(L, C[0], lap[0]); lap[1] = fma(L, C[1], lap[1]); lap[2] = fma(L, C[2], lap[2]);
         rec[e] = sw * L;
       }
-      if (A.b_own[q]) e_acc += 0.5 * w * mubd * (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
+      if (A.b_own[q]) e_acc += 0.5 * w * kc[8] * (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
 #pragma unroll
       for (int c = 0; c < 3; ++c) rec[9 + c] = sw * lap[c];
     }
@@ -425,7 +436,7 @@ int build_frame(const Sheet& sh, const CoreTables& ct, FrameTables& ft, std::str
   ft.ntiles = (int)tiles.size();
   ft.maxM = std::max(ft.maxM, 1);
   ft.maxB = std::max(ft.maxB, 1);
-  ft.smem = sizeof(double) * ((size_t)kPosD + (size_t)(kMRec + kMCoef) * ft.maxM + (size_t)kBChan * ft.maxB + 16) +
+  ft.smem = sizeof(double) * ((size_t)kPosD + (size_t)(kMRec + kMCoef) * ft.maxM + (size_t)kBChan * ft.maxB + 32) +
             sizeof(uint32_t) * (size_t)max_te;
   if (ft.smem > 227 * 1024) { err = "frame: shared memory budget"; return 1; }
   const bool ok = upload(dalloc, &ft.tile, tinfo) && upload(dalloc, &ft.tpm, tpm) && upload(dalloc, &ft.tpb, tpb) &&
