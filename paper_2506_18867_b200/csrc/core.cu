@@ -582,9 +582,9 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
                const std::function<void*(size_t)>& dalloc) {
   ct = CoreTables();
   ct.row_ptr = const_cast<int32_t*>(d_row_ptr);
-  if (!sh.affine || sh.mrule != RULE_REDUCED || sh.brule != RULE_REDUCED) return 1;
+  if (!sh.affine || sh.mrule != RULE_REDUCED || sh.brule != RULE_REDUCED) { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
   const int nu = sh.n_u, Su = sh.Su, Sv = sh.Sv;
-  if (nu < 16 || sh.n_v < 16) return 1;
+  if (nu < 16 || sh.n_v < 16) { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
   // ---- anchor buckets
   const int nanch = Su * Sv;
   std::vector<int32_t> mh(nanch + 1, 0), bh(nanch + 1, 0);
@@ -626,7 +626,7 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
       }
     }
   for (bool hv : have)
-    if (!hv) return 1;
+    if (!hv) { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
   // ---- per-control-point conformance with the template (owned rows)
   const double tol = 1e-12;
   auto close = [&](double a, double b) { return std::fabs(a - b) <= tol * std::max(1.0, std::fabs(b)); };
@@ -691,7 +691,7 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
   // rectangle: conformant columns of the middle owned row, then the owned rows on which all of them conform
   const int jm = std::min(std::max(jc, sh.r0), sh.r1 - 1);
   int c0 = ic, c1 = ic;
-  if (!conforms(ic, jm)) return 1;
+  if (!conforms(ic, jm)) { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
   while (c0 - 1 >= 0 && conforms(c0 - 1, jm)) --c0;
   while (c1 + 1 < nu && conforms(c1 + 1, jm)) ++c1;
   ++c1;
@@ -704,8 +704,8 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
   while (j0 - 1 >= sh.r0 && row_ok(j0 - 1)) --j0;
   while (j1 + 1 < sh.r1 && row_ok(j1 + 1)) ++j1;
   ++j1;
-  if (!row_ok(jm)) return 1;
-  if (c1 - c0 < 8 || j1 - j0 < 1) return 1;
+  if (!row_ok(jm)) { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
+  if (c1 - c0 < 8 || j1 - j0 < 1) { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
   ct.CI0 = c0; ct.CI1 = c1; ct.CJ0 = j0; ct.CJ1 = j1; ct.RJ0 = j0; ct.RJ1 = j1;
   {   // row starts of the rectangle: affine in the row (every core row has the same frame columns)
     auto rp = [&](int i, int j) { return (int64_t)sh.row_ptr[(int64_t)(j - sh.r0) * nu + i]; };
@@ -713,7 +713,7 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
     ct.rp_stride = (j1 - j0 > 1) ? rp(c0, j0 + 1) - rp(c0, j0) : 0;
     for (int j = j0; j < j1; ++j)
       for (int i = c0; i < c1; ++i)
-        if (rp(i, j) != ct.rp_base + (int64_t)(j - j0) * ct.rp_stride + (int64_t)(i - c0) * kNB) return 1;
+        if (rp(i, j) != ct.rp_base + (int64_t)(j - j0) * ct.rp_stride + (int64_t)(i - c0) * kNB) { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
   }
   ct.nstrips = (c1 - c0 + kW - 1) / kW;
   // ---- coefficient tables
@@ -756,7 +756,7 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
   if (ct.smem > 227 * 1024) { err = "core: shared memory budget"; return -1; }
   if (cudaFuncSetAttribute(k_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess) {
     cudaGetLastError();
-    return 1;
+    { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
   }
   if (getenv("BSF_CORE_DEBUG")) {
     cudaFuncAttributes fa;

@@ -257,7 +257,9 @@ int build_sheet(int n_u, int n_v, const double* ku, const double* kv, const doub
       else { sh.mem.push_back(P); sh.mem_eown.push_back(own); }
     }
   }
-  // affine detection: constant G and det J (relative 1e-13), vanishing second-order terms
+  // affine detection: constant G and det J, vanishing second-order terms, up to the rounding of the
+  // rest-map evaluation (it grows with the parametric coordinate: 2.3e-13 relative at 1024^2; a
+  // Greville sheet stays affine up to ~1e5 spans with the 1e-11 bound)
   {
     bool aff = true;
     const std::vector<Point>* lists[2] = {&sh.mem, &sh.bend};
@@ -268,8 +270,8 @@ int build_sheet(int n_u, int n_v, const double* ku, const double* kv, const doub
         for (const Point& P : *L) {
           for (int r = 0; r < 2 && aff; ++r)
             for (int c = 0; c < 2; ++c)
-              if (std::fabs(P.G[r][c] - ref->G[r][c]) > 1e-13 * gs) aff = false;
-          if (std::fabs(P.c_u) > 1e-12 * gs * gs || std::fabs(P.c_v) > 1e-12 * gs * gs) aff = false;
+              if (std::fabs(P.G[r][c] - ref->G[r][c]) > 1e-11 * gs) aff = false;
+          if (std::fabs(P.c_u) > 1e-11 * gs * gs || std::fabs(P.c_v) > 1e-11 * gs * gs) aff = false;
           if (!aff) break;
         }
     }
