@@ -106,7 +106,8 @@ class Clocks:
 
 
 def traffic_ratio():
-    """DRAM bytes per algorithmic byte of k_tile from the committed ncu --set full capture."""
+    """DRAM bytes per algorithmic byte of one assembly call (k_frame + k_core) from the committed
+    ncu --set full capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
             return float(json.load(f)["dram_bytes_per_algorithmic_byte"])
@@ -423,11 +424,11 @@ def bench_ours(args, rank, world, local_rank):
         "config": {"workload": f"{args.config}: {ref.n_u}x{ref.n_v} cps, {n_units} states/step/GPU, "
                                f"reduced membrane+bending rules, PSD projection={bool(flags & 1)}",
                    "elements_per_state": el_per_unit, "nnzb": h.nnzb,
-                   "path": "generic" if (flags & B.GENERIC_PATH) else "tile",
+                   "path": "generic" if (flags & B.GENERIC_PATH) else ("core+frame" if h.core_rect()[1] else "tile"),
                    "l2": "working set per step = %.2f GB of outputs > 126 MB L2 (no flush needed)" % (alg / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (None if traffic_ratio() is None or (flags & B.GENERIC_PATH) else traffic_ratio() * alg),
-                     "traffic_source": "dram read+write per algorithmic byte of k_tile, profiles/r01_traffic.json",
+                     "traffic_source": "dram read+write per algorithmic byte of k_frame + k_core (one call), profiles/r01_traffic.json",
                      "peak_kind": peak_kind,
                      "per_launch": "one bsf_eval_all_batch call (%d states): %d algorithmic bytes, avg %.1f us"
                                    % (n_units, alg, call_avg * 1e3)},
