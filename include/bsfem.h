@@ -130,6 +130,20 @@ bsf_status bsf_eval_all_batch_params(bsf_handle h, int nbatch, const double* d_x
                                      int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags,
                                      bsf_stream stream);
 
+/* Host-buffer variant (end-to-end use): the positions of the nbatch states come from HOST memory h_x
+ * (item b at h_x + b*x_stride; page-locked memory lets the upload overlap the computation) and are
+ * uploaded into the caller's device buffer d_x_stage (same layout) in chunks of `chunk` items (0: batch/10,
+ * then doubling each chunk)
+ * on an internal copy stream, each chunk's assembly starting as soon as its positions have arrived.
+ * d_params: optional per-item parameters (as bsf_eval_all_batch_params; device).  Energies go to d_energy
+ * (device, nbatch doubles; required if h_energy is given) and, if h_energy is not NULL, are copied back to
+ * the host buffer h_energy at the end of `stream` (valid after the stream synchronises).  Gradient and
+ * Hessian outputs stay on the device as in bsf_eval_all_batch.  Asynchronous w.r.t. the host. */
+bsf_status bsf_eval_all_batch_host(bsf_handle h, int nbatch, const double* h_x, int64_t x_stride, double* d_x_stage,
+                                   const double* d_params, double* h_energy, double* d_energy, double* d_grad,
+                                   int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags, int chunk,
+                                   bsf_stream stream);
+
 /* Energy only (the line-search call). d_energy: device, 1 double (overwritten). */
 bsf_status bsf_eval_energy(bsf_handle h, const double* d_x, double* d_energy, int flags,
                            bsf_stream stream);

@@ -27,7 +27,7 @@ _STATUS = {0: "OK", -1: "INVALID_ARG", -2: "KNOTS", -3: "TOO_SMALL", -4: "DEGENE
 SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_material", "bsf_get_sizes",
            "bsf_get_pattern", "bsf_eval_all_batch", "bsf_eval_all_batch_params", "bsf_eval_energy", "bsf_eval_gradient", "bsf_assemble_hessian", "bsf_eval_all",
            "bsf_halo_exchange", "bsf_nccl_get_unique_id", "bsf_nccl_comm_init", "bsf_nccl_comm_destroy",
-           "bsf_allreduce_sum", "bsf_get_core_rect", "bsf_last_launch_count", "bsf_last_error"]
+           "bsf_allreduce_sum", "bsf_get_core_rect", "bsf_eval_all_batch_host", "bsf_last_launch_count", "bsf_last_error"]
 
 
 class BsfError(RuntimeError):
@@ -78,6 +78,8 @@ def lib():
         L.bsf_allreduce_sum.argtypes = [vp, C.c_int64, vp, vp]
         L.bsf_last_launch_count.argtypes = [vp]
         L.bsf_get_core_rect.argtypes = [vp, ip]
+        L.bsf_eval_all_batch_host.argtypes = [vp, C.c_int, vp, C.c_int64, vp, vp, vp, vp, vp, C.c_int64, vp,
+                                              C.c_int64, C.c_int, C.c_int, vp]
         for s in SYMBOLS:
             getattr(L, s).restype = C.c_int if s not in ("bsf_last_error",) else C.c_char_p
         _lib = L
@@ -104,6 +106,15 @@ def _ptr(t):
         return None
     if not t.is_cuda or not t.is_contiguous():
         raise ValueError("expected a contiguous CUDA tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _hptr(t):
+    """Host tensor pointer (contiguous CPU float64; page-locked for asynchronous copies)."""
+    if t is None:
+        return None
+    if t.is_cuda or not t.is_contiguous():
+        raise ValueError("expected a contiguous CPU tensor")
     return C.c_void_p(t.data_ptr())
 
 
@@ -213,6 +224,23 @@ class Sheet:
         vs = vals[0].numel() if vals is not None else 0
         _check(lib().bsf_eval_all_batch(self._h, int(B), _ptr(x), x[0].numel(), _ptr(energy), _ptr(grad), gs,
                                         _ptr(vals), vs, int(flags), _stream(stream)))
+
+    def eval_all_batch_host(self, x_host, x_stage, energy=None, energy_host=None, grad=None, vals=None, params=None,
+                            flags=0, chunk=0, stream=None):
+        """End-to-end batched pass from HOST positions: x_host [B, *x_shape()] (CPU float64, pinned for
+        overlap) is uploaded chunk by chunk into x_stage (CUDA, same shape) while earlier chunks compute;
+        energies land in `energy` (CUDA [B]) and, if given, in `energy_host` (CPU [B], valid after the
+        stream synchronises)."""
+        B = x_host.shape[0]
+        if tuple(x_host.shape[1:]) != self.x_shape() or tuple(x_stage.shape) != tuple(x_host.shape):
+            raise ValueError(f"x_host / x_stage must be [B, {self.x_shape()}]")
+        if x_host.is_cuda or not x_stage.is_cuda:
+            raise ValueError("x_host must be a CPU tensor and x_stage a CUDA tensor")
+        gs = grad[0].numel() if grad is not None else 0
+        vs = vals[0].numel() if vals is not None else 0
+        _check(lib().bsf_eval_all_batch_host(self._h, int(B), _hptr(x_host), x_host[0].numel(), _ptr(x_stage),
+                                             _ptr(params), _hptr(energy_host), _ptr(energy), _ptr(grad), gs,
+                                             _ptr(vals), vs, int(flags), int(chunk), _stream(stream)))
 
     def eval_all_batch_params(self, x, params, energy=None, grad=None, vals=None, flags=0, stream=None):
         """Batch of different affine sheets on this handle's grid: params [B, 9] (CUDA float64,

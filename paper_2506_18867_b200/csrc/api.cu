@@ -39,6 +39,8 @@ struct bsf_sheet {
   bsf::CoreTables ct;
   bool core_ok = false;
   bsf::FrameTables ft;
+  cudaStream_t copy_stream = nullptr;   // host-buffer calls: position uploads
+  cudaEvent_t ev_copy = nullptr, ev_start = nullptr;
   std::vector<void*> allocs;
   int last_launches = 0;
   bool host_only = false;
@@ -48,6 +50,9 @@ struct bsf_sheet {
     cudaGetDevice(&prev);
     cudaSetDevice(device);
     if (tt.side) cudaStreamDestroy(tt.side);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (ev_copy) cudaEventDestroy(ev_copy);
+    if (ev_start) cudaEventDestroy(ev_start);
     if (tt.ev_fork) cudaEventDestroy(tt.ev_fork);
     if (tt.ev_join) cudaEventDestroy(tt.ev_join);
     for (void* p : allocs) cudaFree(p);
@@ -364,6 +369,59 @@ bsf_status bsf_eval_all_batch_params(bsf_handle h, int nbatch, const double* d_x
   if (!d_params) return fail(BSF_E_INVALID_ARG, "null parameters");
   return eval_batch_impl(h, nbatch, d_x, x_stride, d_energy, d_grad, grad_stride, d_vals, vals_stride, flags, stream,
                          d_params);
+}
+
+bsf_status bsf_eval_all_batch_host(bsf_handle h, int nbatch, const double* h_x, int64_t x_stride, double* d_x_stage,
+                                   const double* d_params, double* h_energy, double* d_energy, double* d_grad,
+                                   int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags, int chunk,
+                                   bsf_stream stream) {
+  if (!h || !h_x || !d_x_stage || nbatch < 0) return fail(BSF_E_INVALID_ARG, "null argument / negative batch");
+  if (h_energy && !d_energy) return fail(BSF_E_INVALID_ARG, "h_energy needs the device energy buffer");
+  if (nbatch == 0) return BSF_OK;
+  if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
+  const int64_t xn = (int64_t)(h->sh.xhi - h->sh.xlo) * h->sh.n_u * 3;
+  if (nbatch > 1 && x_stride < xn) return fail(BSF_E_INVALID_ARG, "batch strides smaller than one item");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (!h->copy_stream) {
+    if (cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_copy, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming) != cudaSuccess) {
+      if (prev != h->device) cudaSetDevice(prev);
+      return fail(BSF_E_CUDA, "stream creation failed");
+    }
+  }
+  // chunk plan: fixed size if given, else geometric (nbatch/10, then doubling) so that each chunk's
+  // assembly covers the next, larger upload while the first exposed upload stays small
+  int ch = chunk > 0 ? chunk : std::max(1, (nbatch + 9) / 10);
+  // the uploads run on the copy stream, after the work already queued on `stream` (stage reuse)
+  bsf_status s = BSF_OK;
+  if (cudaEventRecord(h->ev_start, st) != cudaSuccess || cudaStreamWaitEvent(h->copy_stream, h->ev_start, 0) != cudaSuccess)
+    s = fail(BSF_E_CUDA, "event");
+  int launches = 0;
+  for (int b0 = 0, nb = 0; b0 < nbatch && s == BSF_OK; b0 += nb, ch = chunk > 0 ? ch : 2 * ch) {
+    nb = std::min(ch, nbatch - b0);
+    const size_t bytes = sizeof(double) * (size_t)((int64_t)(nb - 1) * x_stride + xn);
+    if (cudaMemcpyAsync(d_x_stage + b0 * x_stride, h_x + b0 * x_stride, bytes, cudaMemcpyHostToDevice,
+                        h->copy_stream) != cudaSuccess ||
+        cudaEventRecord(h->ev_copy, h->copy_stream) != cudaSuccess || cudaStreamWaitEvent(st, h->ev_copy, 0) != cudaSuccess) {
+      s = fail(BSF_E_CUDA, "position upload");
+      break;
+    }
+    s = eval_batch_impl(h, nb, d_x_stage + b0 * x_stride, x_stride, d_energy ? d_energy + b0 : nullptr,
+                        d_grad ? d_grad + b0 * grad_stride : nullptr, grad_stride,
+                        d_vals ? d_vals + b0 * vals_stride : nullptr, vals_stride, flags, stream,
+                        d_params ? d_params + 9 * (int64_t)b0 : nullptr);
+    launches += h->last_launches;
+  }
+  if (s == BSF_OK && h_energy &&
+      cudaMemcpyAsync(h_energy, d_energy, sizeof(double) * nbatch, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    s = fail(BSF_E_CUDA, "energy download");
+  h->last_launches = launches;
+  if (prev != h->device) cudaSetDevice(prev);
+  return s;
 }
 
 bsf_status bsf_eval_energy(bsf_handle h, const double* d_x, double* d_energy, int flags, bsf_stream stream) {

@@ -225,3 +225,32 @@ def test_c5_style_batch_of_different_sheets():
         va = o.eval(q.x, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
         assert_parity(float(E[k]), G[k].cpu().numpy(), V[k].cpu().numpy(), Er, gr, vr, what=f"C5 item {k}",
                       hdiag=diag_block_norms(vr, rp, ci, 0, q.n_u), cmax=np.abs(q.x).max(), vabs=va)
+
+
+def test_host_buffer_call_matches_device_call():
+    """bsf_eval_all_batch_host (chunked upload from pinned host memory, overlapped with the assembly)
+    gives the device call's gradient and Hessian bit for bit and its energies to rounding (the energy
+    partial sums follow the CTA partition, which depends on the launch size)."""
+    sheets = [W.make_c2(state=k) for k in range(7)]
+    s = B.Sheet.from_sheet(sheets[0])
+    Xh = torch.stack([torch.from_numpy(q.x) for q in sheets]).pin_memory()
+    X = Xh.cuda()
+    nb = len(sheets)
+    out = []
+    for host in (False, True):
+        E = torch.zeros(nb, dtype=torch.float64, device="cuda")
+        G = torch.zeros((nb,) + tuple(X.shape[1:]), dtype=torch.float64, device="cuda")
+        V = torch.zeros((nb, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+        Eh = torch.zeros(nb, dtype=torch.float64).pin_memory()
+        if host:
+            stage = torch.zeros_like(X)
+            s.eval_all_batch_host(Xh, stage, E, Eh, G, V, flags=B.PROJECT_PSD, chunk=3)
+            torch.cuda.synchronize()
+            assert torch.equal(stage, X)
+            assert torch.equal(Eh, E.cpu())
+        else:
+            s.eval_all_batch(X, E, G, V, B.PROJECT_PSD)
+            torch.cuda.synchronize()
+        out.append((E.cpu().numpy(), G, V))
+    assert torch.equal(out[0][1], out[1][1]) and torch.equal(out[0][2], out[1][2])
+    assert np.max(np.abs(out[0][0] - out[1][0]) / np.abs(out[0][0])) < 1e-13
