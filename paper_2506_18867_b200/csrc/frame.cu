@@ -46,7 +46,7 @@ struct FrameArgs {
   const double* params;
   int n_u, xlo, xhi, r0;
   int maxM, maxB;
-  int project, flags;
+  int project, flags, dbg;
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
   const int4* tile;
   const int32_t* tpm;
@@ -67,7 +67,10 @@ struct FrameArgs {
 };
 
 constexpr int kPosD = 8 * 8 * 3;    // (tw + 4) * (th + 4) * 3 for 4x4 tiles
-constexpr int kMRec = 28;           // 27 channels + pad (16-B aligned records)
+// record strides in doubles are odd so that lanes reading different points hit different banks
+constexpr int kMRec = 29;           // 27 channels + pad
+constexpr int kMCf = 19;            // 18 d-vector entries + pad
+constexpr int kBRec = 13;           // 12 bending channels + pad
 
 __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
   extern __shared__ __align__(16) double fsm[];
@@ -78,9 +81,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
   const int maxM = A.maxM, maxB = A.maxB;
   double* pos = fsm;                       // [(th+4)][(tw+4)][3]
   double* mch = pos + kPosD;               // [maxM][kMRec]  A~uu 6 | A~vv 6 | A~uv 9 | P~u 3 | P~v 3
-  double* mcf = mch + kMRec * maxM;        // [maxM][18]     (du, dv) per window entry
-  double* bch = mcf + kMCoef * maxM;       // [maxB][12]     sqrt(w mu) L_e 9 | sqrt(w mu) Lap phi 3
-  double* red = bch + kBChan * maxB;       // [16] energy reduction
+  double* mcf = mch + kMRec * maxM;        // [maxM][kMCf]   (du, dv) per window entry
+  double* bch = mcf + kMCf * maxM;         // [maxB][kBRec]  sqrt(w mu) L_e 9 | sqrt(w mu) Lap phi 3
+  double* red = bch + kBRec * maxB;        // [16] energy reduction
   double* kc = red + 16;                   // [16] per-item constants (kept out of registers)
   uint32_t* sent = reinterpret_cast<uint32_t*>(kc + 16);   // [tile entries]
   const double* __restrict__ x = A.x + item * A.xs;
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
   const int m0 = A.tpm[tile], M = A.tpm[tile + 1] - m0, b0 = A.tpb[tile], B = A.tpb[tile + 1] - b0;
   double e_acc = 0.0;
   // points on the threads at the end of the task order (the shortest gather lists)
-  for (int t = kThreads - 1 - tid; t < M + B; t += kThreads) {
+  for (int t = kThreads - 1 - tid; t < ((A.dbg & 16) ? 0 : M + B); t += kThreads) {
     if (t < M) {
       const int p = m0 + t;
       const int2 an = A.m_anc[p];
@@ -132,8 +135,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
 #pragma unroll
       for (int e = 0; e < 9; ++e) {
         const double du = cf[2 * e], dv = cf[2 * e + 1];
-        mcf[t * kMCoef + 2 * e] = du;
-        mcf[t * kMCoef + 2 * e + 1] = dv;
+        mcf[t * kMCf + 2 * e] = du;
+        mcf[t * kMCf + 2 * e + 1] = dv;
         const double* C = pos + ((an.y + e / 3 - (j0 - 2)) * PW + (an.x + e % 3 - (i0 - 2))) * 3;
 #pragma unroll
         for (int c = 0; c < 3; ++c) { Fu[c] = fma(C[c], du, Fu[c]); Fv[c] = fma(C[c], dv, Fv[c]); }
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
       const double* cf = A.b_coef + 27 * (int64_t)q;
       const double w = A.b_what[q] * kc[4];
       const double sw = sqrt(w * kc[8]);
-      double* rec = bch + tb * kBChan;
+      double* rec = bch + tb * kBRec;
       double lap[3] = {0, 0, 0};
 #pragma unroll
       for (int e = 0; e < 9; ++e) {
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
 
   // ---- 3. gather: tasks = (control point, block) or (control point, gradient), sorted by list length on
   // the host; thread tid takes tasks tid, tid + kThreads, ... (lanes of a warp run loops of similar length)
-  for (int tk = tid; tk < kTasks; tk += kThreads) {
+  for (int tk = tid; tk < ((A.dbg & 32) ? 0 : kTasks); tk += kThreads) {
   const uint4 task = A.lst[tile * kTasks + tk];
   const int first = task.x & 0xFFFFF, cnt = task.x >> 20;
   const int out = (int)task.y, outT = (int)task.z;
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
       const int pt = E & 1023, ea = (E >> 10) & 15, eb = (E >> 14) & 15;
       if (!(E >> 18)) {
         const double* rec = mch + pt * kMRec;
-        const double* cf = mcf + pt * kMCoef;
+        const double* cf = mcf + pt * kMCf;
         const double au = cf[2 * ea], av = cf[2 * ea + 1], bu = cf[2 * eb], bv = cf[2 * eb + 1];
         const double k11 = au * bu, k22 = av * bv, k12 = au * bv, k21 = av * bu;
 #pragma unroll
@@ -222,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
                                  fma(k21, rec[12 + 3 * c3 + r3], h[3 * r3 + c3]))));
           }
       } else {
-        const double* rec = bch + pt * kBChan;
+        const double* rec = bch + pt * kBRec;
         hb = fma(rec[ea], rec[eb], hb);
       }
     }
@@ -244,12 +247,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
       const int pt = E & 1023, ea = (E >> 10) & 15;
       if (!(E >> 18)) {
         const double* rec = mch + pt * kMRec;
-        const double au = mcf[pt * kMCoef + 2 * ea], av = mcf[pt * kMCoef + 2 * ea + 1];
+        const double au = mcf[pt * kMCf + 2 * ea], av = mcf[pt * kMCf + 2 * ea + 1];
         g0 = fma(au, rec[21], fma(av, rec[24], g0));
         g1 = fma(au, rec[22], fma(av, rec[25], g1));
         g2 = fma(au, rec[23], fma(av, rec[26], g2));
       } else {
-        const double* rec = bch + pt * kBChan;
+        const double* rec = bch + pt * kBRec;
         const double La = rec[ea];
         g0 = fma(La, rec[9], g0);
         g1 = fma(La, rec[10], g1);
@@ -436,7 +439,7 @@ int build_frame(const Sheet& sh, const CoreTables& ct, FrameTables& ft, std::str
   ft.ntiles = (int)tiles.size();
   ft.maxM = std::max(ft.maxM, 1);
   ft.maxB = std::max(ft.maxB, 1);
-  ft.smem = sizeof(double) * ((size_t)kPosD + (size_t)(kMRec + kMCoef) * ft.maxM + (size_t)kBChan * ft.maxB + 32) +
+  ft.smem = sizeof(double) * ((size_t)kPosD + (size_t)(kMRec + kMCf) * ft.maxM + (size_t)kBRec * ft.maxB + 32) +
             sizeof(uint32_t) * (size_t)max_te;
   if (ft.smem > 227 * 1024) { err = "frame: shared memory budget"; return 1; }
   const bool ok = upload(dalloc, &ft.tile, tinfo) && upload(dalloc, &ft.tpm, tpm) && upload(dalloc, &ft.tpb, tpb) &&
@@ -469,6 +472,10 @@ int frame_eval(const FrameTables& ft, const Sheet& sh, const double* d_x, int64_
   A.n_u = sh.n_u; A.xlo = sh.xlo; A.xhi = sh.xhi; A.r0 = sh.r0;
   A.maxM = ft.maxM; A.maxB = ft.maxB;
   A.project = (flags & 1) ? 1 : 0; A.flags = flags;
+  {
+    const char* e = getenv("BSF_CORE_DEBUG");   // profiling switches: 16 no points, 32 no gather
+    A.dbg = e ? atoi(e) : 0;
+  }
   A.G00 = G4[0]; A.G01 = G4[1]; A.G10 = G4[2]; A.G11 = G4[3]; A.detJ = detJ;
   A.mu1 = (flags & 2) ? 0.0 : mat.mu_st1;
   A.mu2 = (flags & 2) ? 0.0 : mat.mu_st2;
