@@ -276,50 +276,39 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
 #pragma unroll
     for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * cst[kCstP + 0] + Fv[c] * cst[kCstP + 2]; f2[c] = Fu[c] * cst[kCstP + 1] + Fv[c] * cst[kCstP + 3]; }
   }
-  FSpace o;
-  fbw_point(f1, f2, cst[kCstP + 5], cst[kCstP + 6], cst[kCstP + 7], P.project, o);
   double* rec = row + set * kSetD + k;
-  if (P.diagG) {   // A~uu = w G00^2 A11, A~vv = w G11^2 A22, A~uv = w G00 G11 A12, P~ = w (G00 P1, G11 P2)
-    const double su = wq * cst[kCstP + 0], sv = wq * cst[kCstP + 3];
-    const double auu = su * cst[kCstP + 0], avv = sv * cst[kCstP + 3], auv = su * cst[kCstP + 3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      rec[(21 + c) * kKH] = su * o.P1[c];
-      rec[(24 + c) * kKH] = sv * o.P2[c];
-    }
-#pragma unroll
-    for (int e6 = 0; e6 < 6; ++e6) {
-      rec[e6 * kKH] = auu * o.A11[e6];
-      rec[(6 + e6) * kKH] = avv * o.A22[e6];
-    }
-#pragma unroll
-    for (int e9 = 0; e9 < 9; ++e9) rec[(12 + e9) * kKH] = auv * o.A12[e9];
-    if (s >= P.i0 && s < P.i1 && tq >= P.ja && tq < P.jb) return wq * o.psi;
-    return 0.0;
-  }
-  // P~_mu = w sum_beta G_mu,beta P_beta
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {
-    rec[(21 + c) * kKH] = wq * (cst[kCstP + 0] * o.P1[c] + cst[kCstP + 1] * o.P2[c]);
-    rec[(24 + c) * kKH] = wq * (cst[kCstP + 2] * o.P1[c] + cst[kCstP + 3] * o.P2[c]);
-  }
-  // A~_mu,nu = w sum_{beta,gamma} G_mu,beta G_nu,gamma A_beta,gamma
-  const double a11 = wq * cst[kCstP + 0] * cst[kCstP + 0], a12 = wq * cst[kCstP + 0] * cst[kCstP + 1], a22 = wq * cst[kCstP + 1] * cst[kCstP + 1];
-  const double b11 = wq * cst[kCstP + 2] * cst[kCstP + 2], b12 = wq * cst[kCstP + 2] * cst[kCstP + 3], b22 = wq * cst[kCstP + 3] * cst[kCstP + 3];
-  const double c11 = wq * cst[kCstP + 0] * cst[kCstP + 2], c12 = wq * cst[kCstP + 0] * cst[kCstP + 3], c21 = wq * cst[kCstP + 1] * cst[kCstP + 2], c22 = wq * cst[kCstP + 1] * cst[kCstP + 3];
-#pragma unroll
-  for (int r3 = 0; r3 < 3; ++r3)
-#pragma unroll
-    for (int c3 = r3; c3 < 3; ++c3) {
+  double psi;
+  // P~_mu = w sum_beta G_mu,beta P_beta;  A~_mu,nu = w sum_{beta,gamma} G_mu,beta G_nu,gamma A_beta,gamma,
+  // streamed into the record as fbw_emit forms each F-space entry
+  const auto emit_p = [&](int c, double P1c, double P2c) {
+    rec[(21 + c) * kKH] = wq * (cst[kCstP + 0] * P1c + cst[kCstP + 1] * P2c);
+    rec[(24 + c) * kKH] = wq * (cst[kCstP + 2] * P1c + cst[kCstP + 3] * P2c);
+  };
+  if (P.diagG) {   // A~uu = w G00^2 A11, A~vv = w G11^2 A22, A~uv = w G00 G11 A12
+    const double auu = wq * cst[kCstP + 0] * cst[kCstP + 0], avv = wq * cst[kCstP + 3] * cst[kCstP + 3];
+    const double auv = wq * cst[kCstP + 0] * cst[kCstP + 3];
+    psi = fbw_emit(f1, f2, cst[kCstP + 5], cst[kCstP + 6], cst[kCstP + 7], P.project, emit_p,
+                   [&](int r3, int c3, double A11, double A22, double A12rc, double A12cr) {
       const int e6 = sym3(r3, c3);
-      const double A11 = o.A11[e6], A22 = o.A22[e6];
-      const double A12rc = o.A12[3 * r3 + c3], A12cr = o.A12[3 * c3 + r3];
-      rec[e6 * kKH] = a11 * A11 + a12 * (A12rc + A12cr) + a22 * A22;
-      rec[(6 + e6) * kKH] = b11 * A11 + b12 * (A12rc + A12cr) + b22 * A22;
-      rec[(12 + 3 * r3 + c3) * kKH] = c11 * A11 + c12 * A12rc + c21 * A12cr + c22 * A22;   // A~uv[r][c]
-      if (r3 != c3) rec[(12 + 3 * c3 + r3) * kKH] = c11 * A11 + c12 * A12cr + c21 * A12rc + c22 * A22;
-    }
-  if (s >= P.i0 && s < P.i1 && tq >= P.ja && tq < P.jb) return wq * o.psi;
+      rec[e6 * kKH] = auu * A11;
+      rec[(6 + e6) * kKH] = avv * A22;
+      rec[(12 + 3 * r3 + c3) * kKH] = auv * A12rc;
+      if (r3 != c3) rec[(12 + 3 * c3 + r3) * kKH] = auv * A12cr;
+    });
+  } else {
+    psi = fbw_emit(f1, f2, cst[kCstP + 5], cst[kCstP + 6], cst[kCstP + 7], P.project, emit_p,
+                   [&](int r3, int c3, double A11, double A22, double A12rc, double A12cr) {
+      const double G00 = cst[kCstP + 0], G01 = cst[kCstP + 1], G10 = cst[kCstP + 2], G11 = cst[kCstP + 3];
+      const int e6 = sym3(r3, c3);
+      const double sym12 = A12rc + A12cr;
+      rec[e6 * kKH] = wq * (G00 * G00 * A11 + G00 * G01 * sym12 + G01 * G01 * A22);
+      rec[(6 + e6) * kKH] = wq * (G10 * G10 * A11 + G10 * G11 * sym12 + G11 * G11 * A22);
+      rec[(12 + 3 * r3 + c3) * kKH] = wq * (G00 * G10 * A11 + G00 * G11 * A12rc + G01 * G10 * A12cr + G01 * G11 * A22);
+      if (r3 != c3)
+        rec[(12 + 3 * c3 + r3) * kKH] = wq * (G00 * G10 * A11 + G00 * G11 * A12cr + G01 * G10 * A12rc + G01 * G11 * A22);
+    });
+  }
+  if (s >= P.i0 && s < P.i1 && tq >= P.ja && tq < P.jb) return wq * psi;
   return 0.0;
 }
 
