@@ -76,6 +76,7 @@ __device__ __forceinline__ int ring_slot(int q) { return (unsigned)(q + 7 * kRin
 
 #ifdef BSF_PHASE_TIMERS
 __device__ unsigned long long g_core_t[16];
+__device__ unsigned long long g_warp_t[32];
 #define CT_MARK(v) const long long v = clock64()
 #define CT_ADD(i, d) atomicAdd(&g_core_t[i], (unsigned long long)(d))
 #else
@@ -115,6 +116,34 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
   return v;
 }
 
+// Gradient of one component r for the lanes' control points (parity PI): g_a[r] = sum_q d_a . P~(q)[r]
+// over the 12 incident membrane points + sum_q' w mu L_a(q') Lap phi(q')[r] over the 8 bending points.
+// base0/1: shared byte addresses of the knot rows (channel 0) for even / odd dp; bb0/1: bending arrays
+// at channel r.  Run by the point warps with spare time (the gather warps carry the blocks).
+template <int PI>
+__device__ __forceinline__ void gather_grad(const uint32_t (&base0)[4], const uint32_t (&base1)[4],
+                                            const double* const (&bb0)[3], const double* const (&bb1)[3],
+                                            uint32_t o_pu, uint32_t o_pv, const double* __restrict__ cst,
+                                            double* gdst) {
+  double g = 0.0;
+  static_for<0, make_template(PI).nslot>([&](auto SI) {
+    constexpr int s = decltype(SI)::value;
+    constexpr Template T = make_template(PI);
+    constexpr int dp = T.s_dp[s], dq = T.s_dq[s], set = T.s_set[s], ea = T.s_ea[s];
+    constexpr int imm = 8 * (set * kSetD + ((dp + 2) >> 1));
+    const uint32_t bu = (dp & 1) ? base1[dq + 2] : base0[dq + 2];
+    constexpr double dau = kSetTable.v[set][ea][0], dav = kSetTable.v[set][ea][1];
+    g = fma(dau, lds_f64<imm>(bu + o_pu), fma(dav, lds_f64<imm>(bu + o_pv), g));
+  });
+  static_for<0, kBSlots>([&](auto KI) {
+    constexpr int k = decltype(KI)::value;
+    constexpr int dp = bslot_dp(k), dq = bslot_dq(k);
+    const double* b = ((dp & 1) ? bb1[dq + 2] : bb0[dq + 2]) + ((dp + 2) >> 1);
+    g = fma(cst[kCstLw + k], b[0], g);
+  });
+  *gdst = g;
+}
+
 template <int PI>
 __device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
                                             const uint32_t (&base1)[4], const double* const (&bb0)[3],
@@ -125,7 +154,6 @@ __device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
   double acc[kNB];
 #pragma unroll
   for (int k = 0; k < kNB; ++k) acc[k] = 0.0;
-  double g = 0.0;
   static_for<0, make_template(PI).nslot>([&](auto SI) {
     constexpr int s = decltype(SI)::value;
     constexpr Template T = make_template(PI);
@@ -143,16 +171,8 @@ __device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
       constexpr double bu = kSetTable.v[set][eb][0], bv = kSetTable.v[set][eb][1];
       acc[k] = fma(bu, Yu, fma(bv, Yv, acc[k]));
     });
-    if (diag) g = fma(dau, lds_f64<imm>(bu + o_pu), fma(dav, lds_f64<imm>(bu + o_pv), g));
   });
   if (diag) {
-    static_for<0, kBSlots>([&](auto KI) {
-      constexpr int k = decltype(KI)::value;
-      constexpr int dp = bslot_dp(k), dq = bslot_dq(k);
-      const double* b = ((dp & 1) ? bb1[dq + 2] : bb0[dq + 2]) + ((dp + 2) >> 1);
-      g = fma(cst[kCstLw + k], b[0], g);
-    });
-    if (gdst && active) *gdst = g;
 #pragma unroll
     for (int k = 0; k < kNB; ++k) acc[k] += cst[kCstBeta + k];
   }
@@ -468,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
               const int pad = (int)(((uintptr_t)(vals + g0) >> 3) & 1);
               st_lane = stage + h * kStageRow + pad + (i - i0) * (kNB * 9) + 3 * rr + cc;
             }
-            double* gdst = (gout && diag) ? gout + ((int64_t)(jr - A.r0) * A.n_u + i) * 3 + rr : nullptr;
+            double* gdst = nullptr;
             const uint32_t par = k & 1;
             if (PI == 0)
               gather_role<0>(base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
@@ -481,6 +501,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
           }
         }
       }
+      // (c') gradient rows of step k: the last two point warps (bending-only point work) take the 6
+      // (parity, component) rounds
+      if (k >= 0 && gout && warp >= kThreads / 32 - 2 && !(A.dbg & 2)) {
+        const int PI = warp - (kThreads / 32 - 2);
+        const int jr = j + h;
+        const int sigma = (PI + jr + i0) & 1;
+        const int i = i0 + 2 * m + sigma;
+        if ((i < i1) && (jr < jb)) {
+          uint32_t gb0[4], gb1[4];
+          int sl = ring_slot(jr - 2);
+#pragma unroll
+          for (int d = 0; d < 4; ++d) {
+            gb0[d] = smem_u32(ring + sl * kRowD + m);
+            gb1[d] = gb0[d] + 8 * sigma;
+            sl = (sl == kRing - 1) ? 0 : sl + 1;
+          }
+#pragma unroll 1
+          for (int r = 0; r < 3; ++r) {
+            const double* bb0[3];
+            const double* bb1[3];
+            int s2 = ring_slot(jr - 2);
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+              const double* rb = ring + s2 * kRowD + 4 * kSetD + r * kKH + m;
+              bb0[d] = rb + sigma * kBendD;
+              bb1[d] = rb + (1 - sigma) * kBendD + sigma;
+              s2 = (s2 == kRing - 1) ? 0 : s2 + 1;
+            }
+            double* gdst = gout + ((int64_t)(jr - A.r0) * A.n_u + i) * 3 + r;
+            const uint32_t opu = 8 * (21 + r) * kKH, opv = 8 * (24 + r) * kKH;
+            if (PI == 0) gather_grad<0>(gb0, gb1, bb0, bb1, opu, opv, cst, gdst);
+            else gather_grad<1>(gb0, gb1, bb0, bb1, opu, opv, cst, gdst);
+          }
+        }
+      }
       CT_MARK(T2);
       asm volatile("cp.async.wait_all;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -488,6 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
       __syncthreads();
       CT_MARK(T4);
 #ifdef BSF_PHASE_TIMERS
+      if (k >= 0 && lane == 0) atomicAdd(&g_warp_t[warp], (unsigned long long)(T3 - T0));
       if (k >= 0 && lane == 0) {
         if (warp == kGatherWarps) { CT_ADD(0, T1 - T0); CT_ADD(7, T2 - T1); }
         if (warp == 0) { CT_ADD(1, T2 - T1); CT_ADD(3, T3 - T2); CT_ADD(4, T4 - T3); CT_ADD(5, T4 - T0); CT_ADD(6, 1); }
@@ -801,9 +857,14 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
 }
 
 #ifdef BSF_PHASE_TIMERS
-extern "C" int bsf_debug_core_timers(unsigned long long* out16, int reset) {
-  cudaMemcpyFromSymbol(out16, g_core_t, sizeof(unsigned long long) * 16);
-  if (reset) { unsigned long long z[16] = {}; cudaMemcpyToSymbol(g_core_t, z, sizeof(z)); }
+extern "C" int bsf_debug_core_timers(unsigned long long* out48, int reset) {
+  cudaMemcpyFromSymbol(out48, g_core_t, sizeof(unsigned long long) * 16);
+  cudaMemcpyFromSymbol(out48 + 16, g_warp_t, sizeof(unsigned long long) * 32);
+  if (reset) {
+    unsigned long long z[32] = {};
+    cudaMemcpyToSymbol(g_core_t, z, sizeof(unsigned long long) * 16);
+    cudaMemcpyToSymbol(g_warp_t, z, sizeof(z));
+  }
   return 0;
 }
 #endif

@@ -11,7 +11,7 @@ G = torch.zeros((nst,) + tuple(X.shape[1:]), dtype=torch.float64, device="cuda")
 V = torch.zeros((nst, h.nnzb, 3, 3), dtype=torch.float64, device="cuda")
 h.eval_all_batch(X, E, G, V, 1); torch.cuda.synchronize()
 L = B.lib()
-buf = (C.c_ulonglong * 16)()
+buf = (C.c_ulonglong * 48)()
 L.bsf_debug_core_timers(buf, 1)
 h.eval_all_batch(X, E, G, V, 1); torch.cuda.synchronize()
 L.bsf_debug_core_timers(buf, 1)
@@ -28,3 +28,4 @@ for _ in range(5): h.eval_all_batch(X, E, G, V, 1)
 t1.record(); torch.cuda.synchronize()
 print("call ms", t0.elapsed_time(t1) / 5)
 print("section (d): tid0 %.0f  tid32 %.0f" % (v[13] / n, v[14] / n))
+print("per-warp busy (T0->before barrier):", " ".join("w%d=%.0f" % (w, v[16 + w] / n) for w in range(16)))
