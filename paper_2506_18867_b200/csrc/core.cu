@@ -72,6 +72,8 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+constexpr int kTma = kThreads - 32;   // bulk-store issuer: lane 0 of the last (point / gradient) warp
+
 __device__ __forceinline__ int ring_slot(int q) { return (unsigned)(q + 7 * kRing) % kRing; }   // q >= -49
 
 #ifdef BSF_PHASE_TIMERS
@@ -444,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
       CT_MARK(T1);
       if (k >= 0) {
         // (b) the issuing thread releases the staging buffer once the previous bulk store has read it
-        if (tid == 0) {
+        if (tid == kTma) {
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(bar) : "memory");
         }
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
       }
 #endif
       // (d) bulk stores of the step's rows (head / tail doubles off the 16-B grid by plain stores)
-      if (k >= 0 && vals && tid < 5) {
+      if (k >= 0 && vals && tid >= kTma && tid < kTma + 5) {
         for (int hh = 0; hh < kRows; ++hh) {
           const int jr2 = j + hh;
           if (jr2 >= jb) break;
@@ -562,19 +564,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
           const int64_t nd = (int64_t)(i1 - i0) * (kNB * 9);
           const int head = pad;                                  // 1 double if gd is 8 mod 16
           const int tail = (int)((nd - head) & 1);               // 1 double if the end is 8 mod 16
-          if (tid == 0) {
+          if (tid == kTma) {
             const int64_t nb = (A.dbg & 8) ? 0 : nd - head - tail;
             if (nb > 0)
               asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gd + head),
                            "r"(smem_u32(sp + head)), "r"((uint32_t)(nb * 8))
                            : "memory");
-          } else if (tid == 1 + hh) {
+          } else if (tid == kTma + 1 + hh) {
             if (head) gd[0] = sp[0];
-          } else if (tid == 3 + hh) {
+          } else if (tid == kTma + 3 + hh) {
             if (tail) gd[nd - 1] = sp[nd - 1];
           }
         }
-        if (tid == 0) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (tid == kTma) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
 #ifdef BSF_PHASE_TIMERS
       if (k >= 0 && (tid == 0 || tid == 32)) { CT_MARK(T5); CT_ADD(tid ? 14 : 13, T5 - T4); }
@@ -582,7 +584,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
     }
   }
   CT_MARK(TK2);
-  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (tid == kTma) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #ifdef BSF_PHASE_TIMERS
   if (tid == 0) { CT_ADD(8, TK1 - TK0); CT_ADD(9, TK2 - TK1); CT_ADD(10, 1); CT_ADD(11, clock64() - TK0); }
 #endif
