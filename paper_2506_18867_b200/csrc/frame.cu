@@ -293,17 +293,38 @@ int build_frame(const Sheet& sh, const CoreTables& ct, FrameTables& ft, std::str
   ft = FrameTables();
   if (!ct.ok || !sh.affine) return 1;
   const int nu = sh.n_u, Su = sh.Su, Sv = sh.Sv, r0 = sh.r0, r1 = sh.r1;
-  // ---- frame rectangles of the owned rows and their 4x4 tiles
+  // ---- edge bands (band.cu); the rest of the frame (corners, bands that are not translation invariant)
+  // is cut into 4x4 tiles
+  {
+    const int brc = build_band(sh, ct, ft.band, err, dalloc);
+    if (brc < 0) return brc;
+  }
+  const int* cov = ft.band.covered;
   struct Rect { int i0, i1, j0, j1; };
-  std::vector<Rect> rects = {{0, nu, r0, ct.RJ0}, {0, nu, ct.RJ1, r1}, {0, ct.CI0, ct.RJ0, ct.RJ1},
-                             {ct.CI1, nu, ct.RJ0, ct.RJ1}};
+  std::vector<Rect> rects;
+  for (int side = 0; side < 2; ++side) {   // bottom, top (full width, or the two corners when banded)
+    const int j0 = side ? ct.RJ1 : r0, j1 = side ? r1 : ct.RJ0;
+    if (cov[side]) {
+      rects.push_back({0, ct.CI0, j0, j1});
+      rects.push_back({ct.CI1, nu, j0, j1});
+    } else {
+      rects.push_back({0, nu, j0, j1});
+    }
+  }
+  if (!cov[2]) rects.push_back({0, ct.CI0, ct.RJ0, ct.RJ1});
+  if (!cov[3]) rects.push_back({ct.CI1, nu, ct.RJ0, ct.RJ1});
   std::vector<Rect> tiles;
   for (const Rect& R : rects) {
     if (R.i1 <= R.i0 || R.j1 <= R.j0) continue;
     for (int j = R.j0; j < R.j1; j += 4)
       for (int i = R.i0; i < R.i1; i += 4) tiles.push_back({i, std::min(i + 4, R.i1), j, std::min(j + 4, R.j1)});
   }
-  if (tiles.empty()) return 1;
+  if (tiles.empty()) {   // the bands cover the whole frame
+    if (!ft.band.ok) return 1;
+    ft.ntiles = 0;
+    ft.ok = 1;
+    return 0;
+  }
   // ---- anchor buckets
   const int nanch = Su * Sv;
   std::vector<int32_t> mh(nanch + 1, 0), bh(nanch + 1, 0);
@@ -374,7 +395,8 @@ int build_frame(const Sheet& sh, const CoreTables& ct, FrameTables& ft, std::str
         if (k < kMaxNB) {   // frame-frame pairs: computed once, by the earlier control point
           const int32_t b = c0[k];
           const int bi = b % nu, bj = b / nu;
-          const bool bframe = bj >= r0 && bj < r1 && !(bi >= ct.CI0 && bi < ct.CI1 && bj >= ct.RJ0 && bj < ct.RJ1);
+          bool bframe = false;   // b's row is written by this kernel (a tile cp; not core, not band)
+          for (const Rect& R : rects) bframe = bframe || (bi >= R.i0 && bi < R.i1 && bj >= R.j0 && bj < R.j1);
           if (bframe && b < a_glob) continue;
           if (bframe && b > a_glob) {
             const int64_t bl = (int64_t)(bj - r0) * nu + bi;
@@ -465,6 +487,7 @@ int frame_eval(const FrameTables& ft, const Sheet& sh, const double* d_x, int64_
                int nbatch, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride, const int32_t* d_row_ptr,
                double* e_part, int64_t e_stride, int64_t e_off, const double* d_params, const double* G4, double detJ,
                cudaStream_t st) {
+  if (ft.ntiles == 0) return 0;
   FrameArgs A;
   A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride;
   A.epart = e_part; A.e_stride = e_stride; A.e_off = e_off;

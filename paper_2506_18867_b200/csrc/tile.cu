@@ -895,7 +895,8 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     // frame kernel (full frame rows) + core kernel (full core rows): disjoint rows, one energy array
     // [item][frame tiles | core CTAs]; every slot is written on every call
     const int core_nch = core_pick_chunks(*ct, nbatch);
-    const int64_t e_stride = ft->ntiles + core_ctas_per_item(*ct, core_nch);
+    const int64_t nfb = ft->ntiles + ft->band.nctas;   // energy slots: [frame tiles | band CTAs | core CTAs]
+    const int64_t e_stride = nfb + core_ctas_per_item(*ct, core_nch);
     const int64_t need = (int64_t)nbatch * e_stride;
     if (need > tt.e_cap) {
       void* p = dalloc(need * sizeof(double));
@@ -916,12 +917,15 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     int rc = frame_eval(*ft, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
                         tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, tt.side);
     if (rc) return rc;
+    rc = band_eval(ft->band, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
+                   tt.e_part, e_stride, ft->ntiles, d_params, ct->G, ct->detJ, tt.side);
+    if (rc) return rc;
     rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
-                   ft->ntiles, core_nch, d_params, tt.detJ_ref, st);
+                   nfb, core_nch, d_params, tt.detJ_ref, st);
     if (rc) return rc;
     if (cudaEventRecord(tt.ev_join, tt.side) != cudaSuccess || cudaStreamWaitEvent(st, tt.ev_join, 0) != cudaSuccess)
       return -6;
-    int nl = 2;
+    int nl = 1 + (ft->ntiles > 0) + (ft->band.ok && ft->band.nctas > 0);
     if (d_E) {
       k_energy_final<<<nbatch, 256, 0, st>>>(tt.e_part, (int)e_stride, d_E);
       ++nl;
