@@ -80,23 +80,22 @@ __device__ __forceinline__ void static_for(F&& f) {
 constexpr int kPA = kNA + 4;                       // staged along cps: [S0 - 2, S0 + kNA + 2)
 constexpr int kPosMax = (kMaxD + 4) * kPA * 3;     // staged depth rows: [od0, od1 + 1]
 
-// acc[slot(b)] += d_b,u Y_u + d_b,v Y_v over the 9 window entries b of a point in which a sits at EA
+// acc[slot(b)] += d_b,u Y_u + d_b,v Y_v over the 9 window entries b = (bi, bj) of a point in which a sits at
+// EA, with the tensor-product coefficients d_b,u = N'u[bi] Nv[bj], d_b,v = Nu[bi] N'v[bj] (masked entries
+// are zero in the 1D factors; checked at build time): per window row bj, Au = Nv[bj] Y_u, Av = N'v[bj] Y_v,
+// then acc += N'u[bi] Au + Nu[bi] Av.  cu[i] = (N'u[i], Nu[i]), cv[j] = (Nv[j], N'v[j]).
 template <int EA>
-__device__ __forceinline__ void upd_mem(double (&acc)[kSl], const double2* cb, double Yu, double Yv) {
+__device__ __forceinline__ void upd_mem(double (&acc)[kSl], const double2* cu, const double2* cv, double Yu,
+                                        double Yv) {
+  const double2 u0 = cu[0], u1 = cu[1], u2 = cu[2];
 #pragma unroll
-  for (int eb = 0; eb < 9; ++eb) {
-    const double2 b = cb[eb];
-    double& a = acc[(eb / 3 - EA / 3 + 2) * 5 + (eb % 3 - EA % 3 + 2)];
-    a = fma(b.x, Yu, fma(b.y, Yv, a));
-  }
-}
-
-template <int EA>
-__device__ __forceinline__ void upd_bend(double (&acc)[kSl], const double* __restrict__ lw, double la) {
-#pragma unroll
-  for (int eb = 0; eb < 9; ++eb) {
-    double& a = acc[(eb / 3 - EA / 3 + 2) * 5 + (eb % 3 - EA % 3 + 2)];
-    a = fma(la, lw[eb], a);
+  for (int bj = 0; bj < 3; ++bj) {
+    const double2 v = cv[bj];
+    const double au = v.x * Yu, av = v.y * Yv;
+    double* row = acc + (bj - EA / 3 + 2) * 5 + (2 - EA % 3);
+    row[0] = fma(u0.x, au, fma(u0.y, av, row[0]));
+    row[1] = fma(u1.x, au, fma(u1.y, av, row[1]));
+    row[2] = fma(u2.x, au, fma(u2.y, av, row[2]));
   }
 }
 
@@ -111,13 +110,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
   const int ncls = D.ncls, nbcls = D.nbcls;
   const int PD = od1 - od0 + 2;
   double* pos = bsm;                                   // [PD][kPA][3]
-  double2* cf = reinterpret_cast<double2*>(pos + kPosMax);   // [ncls][9]
-  double* lw = pos + kPosMax + 18 * ncls;              // [nbcls][9] sqrt(w mu) L_e (item constants)
+  double2* cf = reinterpret_cast<double2*>(pos + kPosMax);   // [ncls][6] 1D factors (N'u, Nu) x 3, (Nv, N'v) x 3
+  double* lw = pos + kPosMax + 12 * ncls;              // [nbcls][9] sqrt(w mu) L_e (item constants)
   double* rec = lw + ((9 * nbcls + 1) & ~1);           // [ncls][kChan][kMS]
   double* brec = rec + kChan * kMS * ncls;             // [nbcls][3][kMS] sqrt(w mu) Lap phi
   double* kc = brec + 3 * kMS * nbcls;                 // [16] per-item constants
-  double* red = kc + 16;                               // [8]
-  uint32_t* sent = reinterpret_cast<uint32_t*>(red + 8);   // [D.nent] template entries
+  double* red = kc + 16;                               // [32] per-warp energy partials
+  double* beta = red + 32;                             // [2][kMaxD][kSl] bending Hessian per block slot
+  uint32_t* sent = reinterpret_cast<uint32_t*>(beta + 2 * kMaxD * kSl);  // [D.nent] template entries
   const double* __restrict__ x = A.x + item * A.xs;
 
   if (tid == 0) {
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
     if (j >= A.xlo && j < A.xhi && i >= 0 && i < A.n_u) v = x[((int64_t)(j - A.xlo) * A.n_u + i) * 3 + c];
     pos[k] = v;
   }
-  for (int k = tid; k < 9 * ncls; k += kThreads) cf[k] = A.mcf[9 * D.cls0 + k];
+  for (int k = tid; k < 6 * ncls; k += kThreads) cf[k] = A.mcf[6 * D.cls0 + k];
   for (int k = tid; k < D.nent; k += kThreads) sent[k] = A.ent[D.ent0 + k];
   __syncthreads();
   for (int k = tid; k < 9 * nbcls; k += kThreads) {   // sqrt(w mu) L_e, L_e = G-contracted Laplacian coefficient
@@ -154,6 +154,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
     lw[k] = sqrt(A.bwhat[D.bcls0 + bc] * kc[4] * kc[8]) * L;
   }
   __syncthreads();
+
+  // beta[pi][td][slot] = sum over the bending entries of (pi, td) of w mu L_a L_b (position independent)
+  for (int k = tid; k < 2 * (t1 - t0) * kSl; k += kThreads) {
+    const int sl = k % kSl, pt = k / kSl, pi = pt & 1, td = pt >> 1;
+    const int di = sl % 5 - 2, dj = sl / 5 - 2;
+    const uint32_t* eb = sent + D.eoff[pi][td] + D.ment[pi][td];
+    double b = 0.0;
+    for (int q = 0; q < D.bent[pi][td]; ++q) {
+      const uint32_t E = eb[q];
+      const int ea = E >> 28, bi = ea % 3 + di, bj = ea / 3 + dj;   // b's window position
+      if (bi < 0 || bi > 2 || bj < 0 || bj > 2) continue;
+      const double* l9 = lw + ((E >> 16) & 0xFFF);
+      b = fma(l9[ea], l9[3 * bj + bi], b);
+    }
+    beta[(pi * kMaxD + td) * kSl + sl] = b;
+  }
 
   // ---- 2. points of the anchor window [max(S0, sa0) - 2, min(S0 + kNA, sa1)) x [od0, od1)
   const int olo = max(S0, sa0) - 2, ohi = min(S0 + kNA, sa1);
@@ -172,10 +188,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
     const int cb = 2 * m + ci.x, rb = od - od0;
     if (mem) {
       double Fu[3] = {0, 0, 0}, Fv[3] = {0, 0, 0};
-      const double2* c9 = cf + 9 * cls;
+      const double2* c6 = cf + 6 * cls;
 #pragma unroll
       for (int e = 0; e < 9; ++e) {
-        const double2 d = c9[e];
+        const double2 fu = c6[e % 3], fv = c6[3 + e / 3];
+        const double2 d = make_double2(fu.x * fv.x, fu.y * fv.y);   // (dN/du Nv, Nu dN/dv)
         const int ea = axis ? e / 3 : e % 3, ed = axis ? e % 3 : e / 3;
         const double* C = pos + ((rb + ed) * kPA + cb + ea) * 3;
 #pragma unroll
@@ -230,60 +247,69 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
     const bool valid = s >= sa0 && s < sa1;
     const int r3 = lc / 3, c3 = lc - 3 * (lc / 3);
     const bool hess = lc < 9;
-    const int o_uu = hess ? sym3(r3, c3) * kMS : (21 + lc - 9) * kMS;   // gradient: P~u, P~v channels
+    // record channels of this lane: Hessian lanes A~uu[rc], A~uv[cr], A~uv[rc], A~vv[rc]; gradient lanes
+    // P~u[c], P~v[c] (their Y_u is the gradient contribution; their block accumulators are not used)
+    const int o_uu = hess ? sym3(r3, c3) * kMS : (21 + lc - 9) * kMS;
     const int o_cr = hess ? (12 + 3 * c3 + r3) * kMS : (24 + lc - 9) * kMS;
-    const int o_rc = (12 + 3 * r3 + c3) * kMS, o_vv = (6 + sym3(r3, c3)) * kMS;
+    const int o_rc = hess ? (12 + 3 * r3 + c3) * kMS : o_uu, o_vv = hess ? (6 + sym3(r3, c3)) * kMS : o_cr;
     double acc[kSl];
 #pragma unroll
     for (int k = 0; k < kSl; ++k) acc[k] = 0.0;
-    // membrane entries; a switch on the warp-uniform ea picks compile-time accumulator indices
+    double gacc = 0.0;
+    // membrane entries, grouped by ea: compile-time accumulator indices, no divergence (every lane runs
+    // the same instructions)
     const uint32_t* ep = sent + D.eoff[pi][td];
-    const int nm = D.ment[pi][td], nb = D.bent[pi][td];
-    for (int e = 0; e < nm; ++e) {
-      const uint32_t E = ep[e];
-      const double* rb = rec + (E & 0xFFFF) + l;
-      const double2* c9 = cf + ((E >> 16) & 0xFFF);
-      const int ea = E >> 28;
-      const double2 da = c9[ea];
-      const double Yu = fma(da.x, rb[o_uu], da.y * rb[o_cr]);
-      if (hess) {
-        const double Yv = fma(da.x, rb[o_rc], da.y * rb[o_vv]);
-        switch (ea) {
-          case 0: upd_mem<0>(acc, c9, Yu, Yv); break;
-          case 1: upd_mem<1>(acc, c9, Yu, Yv); break;
-          case 2: upd_mem<2>(acc, c9, Yu, Yv); break;
-          case 3: upd_mem<3>(acc, c9, Yu, Yv); break;
-          case 4: upd_mem<4>(acc, c9, Yu, Yv); break;
-          case 5: upd_mem<5>(acc, c9, Yu, Yv); break;
-          case 6: upd_mem<6>(acc, c9, Yu, Yv); break;
-          case 7: upd_mem<7>(acc, c9, Yu, Yv); break;
-          default: upd_mem<8>(acc, c9, Yu, Yv); break;
-        }
-      } else {
-        acc[0] += Yu;
-      }
+    const unsigned char* mc = D.mcnt[pi][td];
+    // software pipeline across entries (and ea groups): the entry word two ahead, the record channels and
+    // the window factors of the next entry are loaded while the current one is accumulated
+    uint32_t E1 = ep[0], E2 = ep[1];
+    double p_uu, p_cr, p_rc, p_vv;
+    double2 p_fu, p_fv;
+    {
+      const double* rb = rec + (E1 & 0xFFFF) + l;
+      p_uu = rb[o_uu]; p_cr = rb[o_cr]; p_rc = rb[o_rc]; p_vv = rb[o_vv];
+      const double2* c6 = cf + ((E1 >> 16) & 0xFFF);
+      const int ea = E1 >> 28;
+      p_fu = c6[ea - 3 * (ea / 3)]; p_fv = c6[3 + ea / 3];
     }
-    // bending entries: sum_q' w mu L_a L_b on the diagonal entries, sqrt(w mu) L_a sqrt(w mu) Lap phi
-    const bool diag = hess && r3 == c3;
-    for (int e = nm; e < nm + nb; ++e) {
-      const uint32_t E = ep[e];
-      const double* l9 = lw + ((E >> 16) & 0xFFF);
-      const int ea = E >> 28;
-      const double la = l9[ea];
-      if (diag) {
-        switch (ea) {
-          case 0: upd_bend<0>(acc, l9, la); break;
-          case 1: upd_bend<1>(acc, l9, la); break;
-          case 2: upd_bend<2>(acc, l9, la); break;
-          case 3: upd_bend<3>(acc, l9, la); break;
-          case 4: upd_bend<4>(acc, l9, la); break;
-          case 5: upd_bend<5>(acc, l9, la); break;
-          case 6: upd_bend<6>(acc, l9, la); break;
-          case 7: upd_bend<7>(acc, l9, la); break;
-          default: upd_bend<8>(acc, l9, la); break;
+    int k = 0;
+    static_for<0, 9>([&](auto EA_) {
+      constexpr int EA = decltype(EA_)::value;
+      const int n = mc[EA];
+      for (int q = 0; q < n; ++q) {
+        const uint32_t E = E1;
+        const double ruu = p_uu, rcr = p_cr, rrc = p_rc, rvv = p_vv;
+        const double dau = p_fu.x * p_fv.x, dav = p_fu.y * p_fv.y;
+        E1 = E2;
+        E2 = ep[k + 2];
+        ++k;
+        {
+          const double* rb = rec + (E1 & 0xFFFF) + l;
+          p_uu = rb[o_uu]; p_cr = rb[o_cr]; p_rc = rb[o_rc]; p_vv = rb[o_vv];
+          const double2* c6 = cf + ((E1 >> 16) & 0xFFF);
+          const int ea = E1 >> 28;
+          p_fu = c6[ea - 3 * (ea / 3)]; p_fv = c6[3 + ea / 3];
         }
-      } else if (!hess) {
-        acc[0] = fma(la, brec[(E & 0xFFFF) + (lc - 9) * kMS + l], acc[0]);
+        const double2* c6 = cf + ((E >> 16) & 0xFFF);
+        const double Yu = fma(dau, ruu, dav * rcr);
+        const double Yv = fma(dau, rrc, dav * rvv);
+        upd_mem<EA>(acc, c6, c6 + 3, Yu, Yv);
+        gacc += Yu;
+      }
+    });
+    // bending: the Hessian part sum_q' w mu L_a L_b is position independent (beta table of the CTA,
+    // diagonal entries only); the gradient lanes gather sqrt(w mu) L_a sqrt(w mu) Lap phi
+    {
+      const double* bt = beta + (pi * kMaxD + td) * kSl;
+      const double dl = (hess && r3 == c3) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k2 = 0; k2 < kSl; ++k2) acc[k2] = fma(dl, bt[k2], acc[k2]);
+      const int go = (hess ? 0 : lc - 9) * kMS + l;
+      const int nb = D.bent[pi][td];
+      const uint32_t* eb = ep + D.ment[pi][td];
+      for (int q = 0; q < nb; ++q) {
+        const uint32_t E = eb[q];
+        gacc = fma(lw[((E >> 16) & 0xFFF) + (E >> 28)], brec[(E & 0xFFFF) + go], gacc);
       }
     }
     if (valid && !(A.dbg & 64)) {
@@ -298,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
           if (q != 255) dst[9 * q] = acc[k];
         }
       } else if (!hess && A.g) {
-        A.g[item * A.gs + 3 * aloc + (lc - 9)] = acc[0];
+        A.g[item * A.gs + 3 * aloc + (lc - 9)] = gacc;
       }
     }
   }
@@ -440,8 +466,11 @@ int build_band(const Sheet& sh, const CoreTables& ct, BandTables& bt, std::strin
               for (int e = 0; e < 9; ++e) {
                 const int iu = e % 3, jv = e / 3;
                 const bool in = (P.mask >> e) & 1;
-                mcf.push_back(make_double2(in ? P.bu.d1[iu] * P.bv.N[jv] : 0.0, in ? P.bu.N[iu] * P.bv.d1[jv] : 0.0));
+                // tensor-product form: a masked entry must have zero 1D products
+                if (!in && (P.bu.d1[iu] * P.bv.N[jv] != 0.0 || P.bu.N[iu] * P.bv.d1[jv] != 0.0)) okb = false;
               }
+              for (int i = 0; i < 3; ++i) mcf.push_back(make_double2(P.bu.d1[i], P.bu.N[i]));
+              for (int j = 0; j < 3; ++j) mcf.push_back(make_double2(P.bv.N[j], P.bv.d1[j]));
             } else {
               bcls.push_back(make_int2(par, od));
               bwhat.push_back(P.what);
@@ -504,7 +533,7 @@ int build_band(const Sheet& sh, const CoreTables& ct, BandTables& bt, std::strin
                 const int dm = (pi - (sr - oa) + 2) >> 1;
                 const uint32_t c = (uint32_t)(cbase + cl);
                 const uint32_t roff = (bend ? 3u * kMS : (uint32_t)(kChan * kMS)) * c + (uint32_t)dm;
-                grp[ea].push_back(roff | ((9u * c) << 16) | ((uint32_t)ea << 28));
+                grp[ea].push_back(roff | (((bend ? 9u : 6u) * c) << 16) | ((uint32_t)ea << 28));
               }
             }
           }
@@ -521,15 +550,16 @@ int build_band(const Sheet& sh, const CoreTables& ct, BandTables& bt, std::strin
     }
     if (!okb) {   // roll back this band's data
       if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "k_band: band %d rejected (templates / pattern)\n", b);
-      mcls.resize(d.cls0); mwhat.resize(d.cls0); mcf.resize(9 * (size_t)d.cls0);
+      mcls.resize(d.cls0); mwhat.resize(d.cls0); mcf.resize(6 * (size_t)d.cls0);
       bcls.resize(d.bcls0); bwhat.resize(d.bcls0); bcf.resize(27 * (size_t)d.bcls0);
       ent.resize(d.ent0);
       continue;
     }
-    ent.push_back(0u);   // padding: the membrane loop prefetches one entry ahead
+    ent.push_back(0u);   // padding: the membrane loop prefetches two entries ahead
+    ent.push_back(0u);
     d.nent = (int)ent.size() - d.ent0;
-    const size_t smem = sizeof(double) * ((size_t)kPosMax + 18 * d.ncls + ((9 * d.nbcls + 1) & ~1) +
-                                          (size_t)kChan * kMS * d.ncls + 3 * kMS * d.nbcls + 24) +
+    const size_t smem = sizeof(double) * ((size_t)kPosMax + 12 * d.ncls + ((9 * d.nbcls + 1) & ~1) +
+                                          (size_t)kChan * kMS * d.ncls + 3 * kMS * d.nbcls + 48 + 2 * kMaxD * kSl) +
                         sizeof(uint32_t) * (size_t)d.nent;
     smem_max = std::max(smem_max, smem);
     bt.h_cfirst.push_back((int)ctas.size());
