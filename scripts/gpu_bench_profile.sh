@@ -8,5 +8,5 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --csv --log-file
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo launches=$?
 # full capture of the two assembly kernels of one call (20 C2 states): k_frame and k_core
 python scripts/prof_tile.py 20 > gpurun_out/prof_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_core|k_frame" -s 4 -c 2 -o gpurun_out/core_full \
+ncu --set full --clock-control none --import-source on -k regex:"k_core|k_frame|k_band" -s 6 -c 3 -o gpurun_out/core_full \
     python scripts/prof_tile.py 20 > gpurun_out/ncu_full.log 2>&1; echo full=$?
