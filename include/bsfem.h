@@ -66,7 +66,11 @@ enum {
   BSF_NO_MEMBRANE = 2,   /* debug: drop the membrane terms                                       */
   BSF_NO_BENDING = 4,    /* debug: drop the bending terms                                        */
   BSF_GENERIC_PATH = 8,  /* force the generic point/gather kernels instead of the fused tile path */
-  BSF_TILE_ONLY = 16     /* debug: the tile kernel on the whole sheet, without the interior core kernel */
+  BSF_TILE_ONLY = 16,    /* debug: the tile kernel on the whole sheet, without the interior core kernel */
+  BSF_ASYNC_STAGE = 32   /* bsf_eval_all_batch_host only: the upload into d_x_stage waits only for the previous
+                            host-buffer call on this handle that read the same d_x_stage (not for all work
+                            queued on `stream`), so alternating two staging buffers overlaps one call's
+                            upload with the previous call's assembly */
 };
 
 /* Stiffness symbols of Eq. `eq: FBW stretching and shearing energy` and
@@ -135,6 +139,10 @@ bsf_status bsf_eval_all_batch_params(bsf_handle h, int nbatch, const double* d_x
  * uploaded into the caller's device buffer d_x_stage (same layout) in chunks of `chunk` items (0: batch/10,
  * then doubling each chunk)
  * on an internal copy stream, each chunk's assembly starting as soon as its positions have arrived.
+ * By default the upload starts after all work already queued on `stream`; with BSF_ASYNC_STAGE in flags
+ * it waits only for the last host-buffer call on this handle that read the same d_x_stage (the caller
+ * must not use d_x_stage for anything else meanwhile), and chunk 0 means one chunk (the previous call's
+ * assembly hides this call's upload).
  * d_params: optional per-item parameters (as bsf_eval_all_batch_params; device).  Energies go to d_energy
  * (device, nbatch doubles; required if h_energy is given) and, if h_energy is not NULL, are copied back to
  * the host buffer h_energy at the end of `stream` (valid after the stream synchronises).  Gradient and

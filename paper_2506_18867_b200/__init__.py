@@ -20,6 +20,7 @@ __all__ = ["Sheet", "Material", "material_from_young", "affine_params", "lib", "
 
 RULE_REDUCED, RULE_G2_INTERIOR, RULE_G3_FULL = 0, 1, 2
 PROJECT_PSD, NO_MEMBRANE, NO_BENDING, GENERIC_PATH, TILE_ONLY = 1, 2, 4, 8, 16
+ASYNC_STAGE = 32   # eval_all_batch_host: upload waits only for the last call that read the same stage
 
 _STATUS = {0: "OK", -1: "INVALID_ARG", -2: "KNOTS", -3: "TOO_SMALL", -4: "DEGENERATE_GEOMETRY",
            -5: "SINGULAR_STRETCH", -6: "CUDA", -7: "OOM", -8: "NCCL", -9: "NO_DEVICE"}

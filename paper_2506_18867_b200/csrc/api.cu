@@ -41,6 +41,8 @@ struct bsf_sheet {
   bsf::FrameTables ft;
   cudaStream_t copy_stream = nullptr;   // host-buffer calls: position uploads
   cudaEvent_t ev_copy = nullptr, ev_start = nullptr;
+  struct StageUse { const void* ptr; cudaEvent_t done; };   // BSF_ASYNC_STAGE: last reader of each stage
+  std::vector<StageUse> stage_uses;
   std::vector<void*> allocs;
   int last_launches = 0;
   bool host_only = false;
@@ -55,6 +57,7 @@ struct bsf_sheet {
     if (ev_start) cudaEventDestroy(ev_start);
     if (tt.ev_fork) cudaEventDestroy(tt.ev_fork);
     if (tt.ev_join) cudaEventDestroy(tt.ev_join);
+    for (StageUse& u : stage_uses) cudaEventDestroy(u.done);
     for (void* p : allocs) cudaFree(p);
     cudaSetDevice(prev);
   }
@@ -377,6 +380,8 @@ bsf_status bsf_eval_all_batch_host(bsf_handle h, int nbatch, const double* h_x, 
                                    bsf_stream stream) {
   if (!h || !h_x || !d_x_stage || nbatch < 0) return fail(BSF_E_INVALID_ARG, "null argument / negative batch");
   if (h_energy && !d_energy) return fail(BSF_E_INVALID_ARG, "h_energy needs the device energy buffer");
+  const bool async_stage = (flags & BSF_ASYNC_STAGE) != 0;
+  flags &= ~BSF_ASYNC_STAGE;
   if (nbatch == 0) return BSF_OK;
   if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
   const int64_t xn = (int64_t)(h->sh.xhi - h->sh.xlo) * h->sh.n_u * 3;
@@ -395,11 +400,34 @@ bsf_status bsf_eval_all_batch_host(bsf_handle h, int nbatch, const double* h_x, 
   }
   // chunk plan: fixed size if given, else geometric (nbatch/10, then doubling) so that each chunk's
   // assembly covers the next, larger upload while the first exposed upload stays small
-  int ch = chunk > 0 ? chunk : std::max(1, (nbatch + 9) / 10);
+  // (BSF_ASYNC_STAGE: one chunk by default, the previous call's assembly already covers this upload)
+  int ch = chunk > 0 ? chunk : (async_stage ? nbatch : std::max(1, (nbatch + 9) / 10));
   // the uploads run on the copy stream, after the work already queued on `stream` (stage reuse)
   bsf_status s = BSF_OK;
-  if (cudaEventRecord(h->ev_start, st) != cudaSuccess || cudaStreamWaitEvent(h->copy_stream, h->ev_start, 0) != cudaSuccess)
+  bsf_sheet::StageUse* use = nullptr;
+  if (async_stage) {
+    for (bsf_sheet::StageUse& u : h->stage_uses)
+      if (u.ptr == d_x_stage) use = &u;
+    if (!use) {
+      if (h->stage_uses.size() >= 8) {   // bounded: forget the oldest stage (its event is released on completion)
+        cudaEventDestroy(h->stage_uses.front().done);
+        h->stage_uses.erase(h->stage_uses.begin());
+      }
+      bsf_sheet::StageUse u{d_x_stage, nullptr};
+      if (cudaEventCreateWithFlags(&u.done, cudaEventDisableTiming) != cudaSuccess) {
+        if (prev != h->device) cudaSetDevice(prev);
+        return fail(BSF_E_CUDA, "event creation failed");
+      }
+      // first use of this stage: order after everything queued so far (as without the flag)
+      if (cudaEventRecord(u.done, st) != cudaSuccess) s = fail(BSF_E_CUDA, "event");
+      h->stage_uses.push_back(u);
+      use = &h->stage_uses.back();
+    }
+    if (s == BSF_OK && cudaStreamWaitEvent(h->copy_stream, use->done, 0) != cudaSuccess) s = fail(BSF_E_CUDA, "event");
+  } else if (cudaEventRecord(h->ev_start, st) != cudaSuccess ||
+             cudaStreamWaitEvent(h->copy_stream, h->ev_start, 0) != cudaSuccess) {
     s = fail(BSF_E_CUDA, "event");
+  }
   int launches = 0;
   for (int b0 = 0, nb = 0; b0 < nbatch && s == BSF_OK; b0 += nb, ch = chunk > 0 ? ch : 2 * ch) {
     nb = std::min(ch, nbatch - b0);
@@ -416,6 +444,7 @@ bsf_status bsf_eval_all_batch_host(bsf_handle h, int nbatch, const double* h_x, 
                         d_params ? d_params + 9 * (int64_t)b0 : nullptr);
     launches += h->last_launches;
   }
+  if (s == BSF_OK && use && cudaEventRecord(use->done, st) != cudaSuccess) s = fail(BSF_E_CUDA, "event");
   if (s == BSF_OK && h_energy &&
       cudaMemcpyAsync(h_energy, d_energy, sizeof(double) * nbatch, cudaMemcpyDeviceToHost, st) != cudaSuccess)
     s = fail(BSF_E_CUDA, "energy download");

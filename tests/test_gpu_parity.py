@@ -266,3 +266,28 @@ def test_band_kernel_and_frame_fallback(no_band, monkeypatch):
     _gpu(s, W.make_c2(state=2).x, B.PROJECT_PSD)
     assert s.last_launch_count() == (3 if no_band else 4)
     _check(W.make_sheet(40, 1.0, 9, n_modes=4, amp=5e-3, lam=0.2, rigid=True), flags=0)
+
+
+def test_async_stage_pipelined_host_calls():
+    """BSF_ASYNC_STAGE: consecutive host-buffer calls alternating two staging buffers (each upload waits
+    only for the last call that read its stage) give the same outputs as plain device calls, per call."""
+    sheets = [W.make_c2(state=k) for k in range(6)]
+    s = B.Sheet.from_sheet(sheets[0])
+    Xh = [torch.stack([torch.from_numpy(q.x) for q in sheets[i:i + 3]]).pin_memory() for i in (0, 3)]
+    stages = [torch.zeros_like(Xh[0]).cuda() for _ in range(2)]
+    outs = []
+    for rep in range(4):   # calls 0..3 alternate inputs and stages; each result copied out in stream order
+        i = rep & 1
+        E = torch.zeros(3, dtype=torch.float64, device="cuda")
+        G = torch.zeros((3,) + tuple(Xh[0].shape[1:]), dtype=torch.float64, device="cuda")
+        V = torch.zeros((3, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+        Eh = torch.zeros(3, dtype=torch.float64).pin_memory()
+        s.eval_all_batch_host(Xh[i], stages[i], E, Eh, G, V, flags=B.PROJECT_PSD | B.ASYNC_STAGE)
+        outs.append((i, E, G.clone(), V.clone(), Eh))
+    torch.cuda.synchronize()
+    for i, E, G, V, Eh in outs:
+        E2 = torch.zeros_like(E); G2 = torch.zeros_like(G); V2 = torch.zeros_like(V)
+        s.eval_all_batch(Xh[i].cuda(), E2, G2, V2, B.PROJECT_PSD)
+        torch.cuda.synchronize()
+        assert torch.equal(G, G2) and torch.equal(V, V2) and torch.equal(E, E2)
+        assert torch.equal(Eh, E.cpu())
