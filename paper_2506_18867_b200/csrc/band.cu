@@ -67,6 +67,7 @@ struct BandArgs {
   int cfirst[5];                  // first CTA (blockIdx.x) of each band
   BandDesc desc[4];
   const uint32_t* ent;            // template entries of all bands
+  const double2* entd;            // per entry (d_a,u, d_a,v) at its window position (membrane; 0 for bending)
 };
 
 template <int B, int E, class F>
@@ -74,6 +75,22 @@ __device__ __forceinline__ void static_for(F&& f) {
   if constexpr (B < E) {
     f(std::integral_constant<int, B>{});
     static_for<B + 1, E>(f);
+  }
+}
+
+// Membrane records are anchor-pair major: rec[class][m][kRecP], channel ch at kRecPos[ch]. A gather load
+// instruction reads 4 channels (one per lane group) x 8 consecutive anchor pairs; this permutation (found
+// by exhaustive search over the 12 (channel group, load) combinations and both pair offsets) puts every
+// such load at the 2-wavefront minimum (no bank conflicts).
+constexpr int kRecP = 30, kRecC = kMS * kRecP;
+__host__ __device__ __forceinline__ constexpr int rec_pos(int ch) {
+  switch (ch) {
+    case 0: return 5;   case 1: return 15;  case 2: return 0;   case 3: return 27;  case 4: return 23;
+    case 5: return 24;  case 6: return 9;   case 7: return 14;  case 8: return 19;  case 9: return 2;
+    case 10: return 26; case 11: return 8;  case 12: return 1;  case 13: return 20; case 14: return 13;
+    case 15: return 4;  case 16: return 16; case 17: return 21; case 18: return 7;  case 19: return 18;
+    case 20: return 12; case 21: return 25; case 22: return 29; case 23: return 28; case 24: return 11;
+    case 25: return 3;  default: return 10;
   }
 }
 
@@ -112,12 +129,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
   double* pos = bsm;                                   // [PD][kPA][3]
   double2* cf = reinterpret_cast<double2*>(pos + kPosMax);   // [ncls][6] 1D factors (N'u, Nu) x 3, (Nv, N'v) x 3
   double* lw = pos + kPosMax + 12 * ncls;              // [nbcls][9] sqrt(w mu) L_e (item constants)
-  double* rec = lw + ((9 * nbcls + 1) & ~1);           // [ncls][kChan][kMS]
-  double* brec = rec + kChan * kMS * ncls;             // [nbcls][3][kMS] sqrt(w mu) Lap phi
+  double* rec = lw + ((9 * nbcls + 1) & ~1);           // [ncls][kMS][kRecP] (channel ch at rec_pos(ch))
+  double* brec = rec + kRecC * ncls;                   // [nbcls][3][kMS] sqrt(w mu) Lap phi
   double* kc = brec + 3 * kMS * nbcls;                 // [16] per-item constants
   double* red = kc + 16;                               // [32] per-warp energy partials
   double* beta = red + 32;                             // [2][kMaxD][kSl] bending Hessian per block slot
-  uint32_t* sent = reinterpret_cast<uint32_t*>(beta + 2 * kMaxD * kSl);  // [D.nent] template entries
+  double2* sda = reinterpret_cast<double2*>(beta + 2 * kMaxD * kSl);     // [D.nent] entry window coefficients
+  uint32_t* sent = reinterpret_cast<uint32_t*>(sda + D.nent);             // [D.nent] template entries
   const double* __restrict__ x = A.x + item * A.xs;
 
   if (tid == 0) {
@@ -145,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
     pos[k] = v;
   }
   for (int k = tid; k < 6 * ncls; k += kThreads) cf[k] = A.mcf[6 * D.cls0 + k];
-  for (int k = tid; k < D.nent; k += kThreads) sent[k] = A.ent[D.ent0 + k];
+  for (int k = tid; k < D.nent; k += kThreads) { sent[k] = A.ent[D.ent0 + k]; sda[k] = A.entd[D.ent0 + k]; }
   __syncthreads();
   for (int k = tid; k < 9 * nbcls; k += kThreads) {   // sqrt(w mu) L_e, L_e = G-contracted Laplacian coefficient
     const int bc = k / 9, e = k - bc * 9;
@@ -202,10 +220,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
       double f1[3], f2[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * kc[0] + Fv[c] * kc[2]; f2[c] = Fu[c] * kc[1] + Fv[c] * kc[3]; }
-      double* r = rec + kChan * kMS * cls + m;
+      double* r = rec + kRecC * cls + kRecP * m;
       const auto emit_p = [&](int c, double P1c, double P2c) {   // P~_mu = w sum_beta G_mu,beta P_beta
-        r[(21 + c) * kMS] = wq * (kc[0] * P1c + kc[1] * P2c);
-        r[(24 + c) * kMS] = wq * (kc[2] * P1c + kc[3] * P2c);
+        r[rec_pos(21 + c)] = wq * (kc[0] * P1c + kc[1] * P2c);
+        r[rec_pos(24 + c)] = wq * (kc[2] * P1c + kc[3] * P2c);
       };
       const double wG00 = wq * kc[0], wG01 = wq * kc[1], wG10 = wq * kc[2], wG11 = wq * kc[3];
       const double a11 = wG00 * kc[0], a12 = wG00 * kc[1], a22 = wG01 * kc[1];
@@ -214,10 +232,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
       const double psi = fbw_emit(f1, f2, kc[5], kc[6], kc[7], A.project != 0, emit_p,
                                   [&](int r3, int c3, double A11, double A22, double A12rc, double A12cr) {
         const int e6 = sym3(r3, c3);
-        r[e6 * kMS] = a11 * A11 + a12 * (A12rc + A12cr) + a22 * A22;
-        r[(6 + e6) * kMS] = b11 * A11 + b12 * (A12rc + A12cr) + b22 * A22;
-        r[(12 + 3 * r3 + c3) * kMS] = c11 * A11 + c12 * A12rc + c21 * A12cr + c22 * A22;
-        if (r3 != c3) r[(12 + 3 * c3 + r3) * kMS] = c11 * A11 + c12 * A12cr + c21 * A12rc + c22 * A22;
+        r[rec_pos(e6)] = a11 * A11 + a12 * (A12rc + A12cr) + a22 * A22;
+        r[rec_pos(6 + e6)] = b11 * A11 + b12 * (A12rc + A12cr) + b22 * A22;
+        r[rec_pos(12 + 3 * r3 + c3)] = c11 * A11 + c12 * A12rc + c21 * A12cr + c22 * A22;
+        if (r3 != c3) r[rec_pos(12 + 3 * c3 + r3)] = c11 * A11 + c12 * A12cr + c21 * A12rc + c22 * A22;
       });
       if (own) e_acc += wq * psi;
     } else {
@@ -249,9 +267,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
     const bool hess = lc < 9;
     // record channels of this lane: Hessian lanes A~uu[rc], A~uv[cr], A~uv[rc], A~vv[rc]; gradient lanes
     // P~u[c], P~v[c] (their Y_u is the gradient contribution; their block accumulators are not used)
-    const int o_uu = hess ? sym3(r3, c3) * kMS : (21 + lc - 9) * kMS;
-    const int o_cr = hess ? (12 + 3 * c3 + r3) * kMS : (24 + lc - 9) * kMS;
-    const int o_rc = hess ? (12 + 3 * r3 + c3) * kMS : o_uu, o_vv = hess ? (6 + sym3(r3, c3)) * kMS : o_cr;
+    const int o_uu = rec_pos(hess ? sym3(r3, c3) : 21 + lc - 9) + kRecP * l;
+    const int o_cr = rec_pos(hess ? 12 + 3 * c3 + r3 : 24 + lc - 9) + kRecP * l;
+    const int o_rc = hess ? rec_pos(12 + 3 * r3 + c3) + kRecP * l : o_uu;
+    const int o_vv = hess ? rec_pos(6 + sym3(r3, c3)) + kRecP * l : o_cr;
     double acc[kSl];
 #pragma unroll
     for (int k = 0; k < kSl; ++k) acc[k] = 0.0;
@@ -262,15 +281,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
     const unsigned char* mc = D.mcnt[pi][td];
     // software pipeline across entries (and ea groups): the entry word two ahead, the record channels and
     // the window factors of the next entry are loaded while the current one is accumulated
+    const double2* dp = sda + D.eoff[pi][td];   // (d_a,u, d_a,v) of each entry
     uint32_t E1 = ep[0], E2 = ep[1];
     double p_uu, p_cr, p_rc, p_vv;
-    double2 p_fu, p_fv;
+    double2 p_da;
     {
-      const double* rb = rec + (E1 & 0xFFFF) + l;
+      const double* rb = rec + (E1 & 0xFFFF);
       p_uu = rb[o_uu]; p_cr = rb[o_cr]; p_rc = rb[o_rc]; p_vv = rb[o_vv];
-      const double2* c6 = cf + ((E1 >> 16) & 0xFFF);
-      const int ea = E1 >> 28;
-      p_fu = c6[ea - 3 * (ea / 3)]; p_fv = c6[3 + ea / 3];
+      p_da = dp[0];
     }
     int k = 0;
     static_for<0, 9>([&](auto EA_) {
@@ -279,16 +297,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
       for (int q = 0; q < n; ++q) {
         const uint32_t E = E1;
         const double ruu = p_uu, rcr = p_cr, rrc = p_rc, rvv = p_vv;
-        const double dau = p_fu.x * p_fv.x, dav = p_fu.y * p_fv.y;
+        const double dau = p_da.x, dav = p_da.y;
         E1 = E2;
         E2 = ep[k + 2];
         ++k;
         {
-          const double* rb = rec + (E1 & 0xFFFF) + l;
+          const double* rb = rec + (E1 & 0xFFFF);
           p_uu = rb[o_uu]; p_cr = rb[o_cr]; p_rc = rb[o_rc]; p_vv = rb[o_vv];
-          const double2* c6 = cf + ((E1 >> 16) & 0xFFF);
-          const int ea = E1 >> 28;
-          p_fu = c6[ea - 3 * (ea / 3)]; p_fv = c6[3 + ea / 3];
+          p_da = dp[k];
         }
         const double2* c6 = cf + ((E >> 16) & 0xFFF);
         const double Yu = fma(dau, ruu, dav * rcr);
@@ -392,6 +408,7 @@ int build_band(const Sheet& sh, const CoreTables& ct, BandTables& bt, std::strin
   std::vector<double2> mcf;
   std::vector<double> mwhat, bcf, bwhat;
   std::vector<uint32_t> ent;
+  std::vector<double2> entd;
   size_t smem_max = 0;
   for (int b = 0; b < 4; ++b) {
     const Geo& G = geos[b];
@@ -443,7 +460,7 @@ int build_band(const Sheet& sh, const CoreTables& ct, BandTables& bt, std::strin
           }
         }
     }
-    if (!okb || ccount[0] > 255 || ccount[1] > 255 || 9 * ccount[0] > 4095 || kChan * kMS * ccount[0] > 65535) {
+    if (!okb || ccount[0] > 255 || ccount[1] > 255 || 9 * ccount[0] > 4095 || kRecC * ccount[0] > 65535) {
       if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "k_band: band %d rejected (point classes)\n", b);
       continue;
     }
@@ -532,7 +549,7 @@ int build_band(const Sheet& sh, const CoreTables& ct, BandTables& bt, std::strin
                 if (cl < 0) { okb = false; break; }
                 const int dm = (pi - (sr - oa) + 2) >> 1;
                 const uint32_t c = (uint32_t)(cbase + cl);
-                const uint32_t roff = (bend ? 3u * kMS : (uint32_t)(kChan * kMS)) * c + (uint32_t)dm;
+                const uint32_t roff = bend ? 3u * kMS * c + (uint32_t)dm : (uint32_t)(kRecC * c + kRecP * dm);
                 grp[ea].push_back(roff | (((bend ? 9u : 6u) * c) << 16) | ((uint32_t)ea << 28));
               }
             }
@@ -542,6 +559,12 @@ int build_band(const Sheet& sh, const CoreTables& ct, BandTables& bt, std::strin
             if (grp[ea].size() > 255) okb = false;
             (bend ? d.bcnt : d.mcnt)[pi][td][ea] = (unsigned char)grp[ea].size();
             ent.insert(ent.end(), grp[ea].begin(), grp[ea].end());
+            for (uint32_t E : grp[ea]) {   // the entry's window coefficients (membrane; bending: unused)
+              const size_t f = 6 * (size_t)d.cls0 + ((E >> 16) & 0xFFF);
+              entd.push_back(bend ? make_double2(0.0, 0.0)
+                                  : make_double2(mcf[f + ea % 3].x * mcf[f + 3 + ea / 3].x,
+                                                 mcf[f + ea % 3].y * mcf[f + 3 + ea / 3].y));
+            }
             cnt += (int)grp[ea].size();
           }
           (bend ? d.bent : d.ment)[pi][td] = cnt;
@@ -553,14 +576,17 @@ int build_band(const Sheet& sh, const CoreTables& ct, BandTables& bt, std::strin
       mcls.resize(d.cls0); mwhat.resize(d.cls0); mcf.resize(6 * (size_t)d.cls0);
       bcls.resize(d.bcls0); bwhat.resize(d.bcls0); bcf.resize(27 * (size_t)d.bcls0);
       ent.resize(d.ent0);
+      entd.resize(d.ent0);
       continue;
     }
     ent.push_back(0u);   // padding: the membrane loop prefetches two entries ahead
     ent.push_back(0u);
+    entd.push_back(make_double2(0.0, 0.0));
+    entd.push_back(make_double2(0.0, 0.0));
     d.nent = (int)ent.size() - d.ent0;
     const size_t smem = sizeof(double) * ((size_t)kPosMax + 12 * d.ncls + ((9 * d.nbcls + 1) & ~1) +
-                                          (size_t)kChan * kMS * d.ncls + 3 * kMS * d.nbcls + 48 + 2 * kMaxD * kSl) +
-                        sizeof(uint32_t) * (size_t)d.nent;
+                                          (size_t)kRecC * d.ncls + 3 * kMS * d.nbcls + 48 + 2 * kMaxD * kSl) +
+                        (sizeof(double2) + sizeof(uint32_t)) * (size_t)d.nent;
     smem_max = std::max(smem_max, smem);
     bt.h_cfirst.push_back((int)ctas.size());
     for (int S0 = G.sa0 & ~1; S0 < G.sa1; S0 += kNA) ctas.push_back(make_int2((int)descs.size(), S0));
@@ -578,7 +604,7 @@ int build_band(const Sheet& sh, const CoreTables& ct, BandTables& bt, std::strin
   const bool ok = upload_v(dalloc, &bt.mcf, mcf) && upload_v(dalloc, &bt.mcls, mcls) &&
                   upload_v(dalloc, &bt.mwhat, mwhat) && upload_v(dalloc, &bt.bcf, bcf) &&
                   upload_v(dalloc, &bt.bcls, bcls) && upload_v(dalloc, &bt.bwhat, bwhat) &&
-                  upload_v(dalloc, &bt.ent, ent);
+                  upload_v(dalloc, &bt.ent, ent) && upload_v(dalloc, &bt.entd, entd);
   if (!ok) { err = "band: device allocation failed"; return -7; }
   if (cudaFuncSetAttribute(k_band, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max) != cudaSuccess) {
     cudaGetLastError();
@@ -624,7 +650,7 @@ int band_eval(const BandTables& bt, const Sheet& sh, const double* d_x, int64_t 
   A.nbands = bt.nbands;
   for (int b = 0; b <= bt.nbands; ++b) A.cfirst[b] = bt.h_cfirst[b];
   std::memcpy(A.desc, bt.h_desc.data(), sizeof(BandDesc) * bt.h_desc.size());
-  A.ent = bt.ent;
+  A.ent = bt.ent; A.entd = bt.entd;
   dim3 grid(bt.nctas, nbatch);
   k_band<<<grid, kThreads, bt.smem, st>>>(A);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;

@@ -77,6 +77,7 @@ struct BandTables {
   std::vector<BandDesc> h_desc;
   std::vector<int> h_cfirst;
   uint32_t* ent = nullptr;        // record offset (16 bits) | coefficient offset << 16 (12 bits) | ea << 28
+  double2* entd = nullptr;        // per entry: (d_a,u, d_a,v) at its window position (membrane)
 };
 
 struct FrameTables {
