@@ -60,6 +60,9 @@ def lib():
             L.oracle_energy_cplx.argtypes = [vp, dp, dp, C.c_int, dp, dp]
             L.oracle_gradient_cplx.argtypes = [vp, dp, dp, C.c_int, dp, dp]
             L.oracle_membrane_A.argtypes = [dp, dp, C.c_int, dp]
+            L.oracle_lumped_mass.argtypes = [vp, C.c_double, dp]
+            L.oracle_eval_ip.argtypes = [vp, dp, dp, dp, C.c_double, dp, C.POINTER(C.c_uint8), C.c_int, dp, dp, dp,
+                                         C.c_int]
             _lib = L
     return _lib
 
@@ -186,6 +189,32 @@ class Oracle:
         threads = max_threads() if threads is None else threads
         lib().oracle_eval(self._h, _p(x), flags, _p(E) if energy else None,
                           _p(g) if gradient else None, _p(vals) if hessian else None, threads)
+        return (float(E[0]) if energy else None), g, vals
+
+    def lumped_mass(self, R0):
+        """Lumped mass of the owned control points [owned rows, n_u]: consistent M by 3x3 Gauss per span,
+        row sums."""
+        m = np.zeros((self.r1 - self.r0, self.n_u))
+        _check(lib().oracle_lumped_mass(self._h, float(R0), _p(m)))
+        return m
+
+    def eval_ip(self, x, xhat, m, dt, gravity=(0.0, 0.0, 0.0), pinned=None, flags=0, energy=True, gradient=True,
+                hessian=True, threads=None):
+        """Incremental potential: elastic + sum m/(2dt^2)|x-xhat|^2 - sum m g.x, with
+        pinned control points masked (pinned: bool [n_v, n_u] over all rows, or None)."""
+        x = self._xslab(x)
+        xhat = np.ascontiguousarray(xhat, dtype=np.float64).reshape(self.r1 - self.r0, self.n_u, 3)
+        m = np.ascontiguousarray(m, dtype=np.float64).reshape(self.r1 - self.r0, self.n_u)
+        grav = np.ascontiguousarray(gravity, dtype=np.float64)
+        pin = None if pinned is None else np.ascontiguousarray(pinned, dtype=np.uint8).reshape(self.n_v, self.n_u)
+        E = np.zeros(1)
+        g = np.zeros((self.r1 - self.r0, self.n_u, 3)) if gradient else None
+        vals = np.zeros((self.nnzb, 3, 3)) if hessian else None
+        threads = max_threads() if threads is None else threads
+        _check(lib().oracle_eval_ip(self._h, _p(x), _p(xhat), _p(m), float(dt), _p(grav),
+                                    None if pin is None else pin.ctypes.data_as(C.POINTER(C.c_uint8)), flags,
+                                    _p(E) if energy else None, _p(g) if gradient else None,
+                                    _p(vals) if hessian else None, threads))
         return (float(E[0]) if energy else None), g, vals
 
     def energy_cplx(self, x_re, x_im, flags=0):

@@ -752,6 +752,103 @@ int oracle_gradient_cplx(void* h, const double* x_re, const double* x_im, int fl
   return 0;
 }
 
+// ------------------------------------------------------------------ incremental potential
+// Lumped mass of the owned control points, step by step as the paper states it:
+//   consistent mass  M_ab = int_Omega0 R0 N_a N_b dX
+//   quadrature       3x3 Gauss per knot span (exact for N_a N_b per span)
+//   lumping          m_a = sum_b M_ab, off-diagonals dropped     (Eq. lumped mass)
+// R0 = areal (reference) density, dX = det J du dv.  m: [owned rows][n_u].
+int oracle_lumped_mass(void* h, double R0, double* m) {
+  auto* o = static_cast<Oracle*>(h);
+  const int nu = o->n_u, nv = o->n_v;
+  std::vector<double> Nu(nu), dNu(nu), ddNu(nu), Nv(nv), dNv(nv), ddNv(nv);
+  std::fill(m, m + (size_t)(o->r1 - o->r0) * nu, 0.0);
+  double gx[3], gw[3], hx[3], hw[3];
+  for (int t = 0; t < o->Sv; ++t)
+    for (int s = 0; s < o->Su; ++s) {
+      // bases active on span (s, t): i in [s, s+2], j in [t, t+2]
+      if (t + 2 < o->r0 || t >= o->r1) continue;
+      gauss(3, s, s + 1, gx, gw);
+      gauss(3, t, t + 1, hx, hw);
+      double Mloc[9][9] = {};
+      for (int b = 0; b < 3; ++b)
+        for (int a = 0; a < 3; ++a) {
+          cox_de_boor(o->ku.data(), nu + 3, gx[a], Nu.data(), dNu.data(), ddNu.data());
+          cox_de_boor(o->kv.data(), nv + 3, hx[b], Nv.data(), dNv.data(), ddNv.data());
+          double J[2][2] = {{0, 0}, {0, 0}};
+          for (int j = t; j <= t + 2; ++j)
+            for (int i = s; i <= s + 2; ++i) {
+              const double* X = &o->rest[2 * ((size_t)j * nu + i)];
+              for (int c = 0; c < 2; ++c) { J[c][0] += dNu[i] * Nv[j] * X[c]; J[c][1] += Nu[i] * dNv[j] * X[c]; }
+            }
+          const double det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+          if (!(det > 0.0)) return fail("degenerate geometry: det J <= 0 at a mass quadrature point", -4);
+          const double wq = gw[a] * hw[b] * det * R0;
+          for (int e = 0; e < 9; ++e)
+            for (int f = 0; f < 9; ++f)
+              Mloc[e][f] += wq * Nu[s + e % 3] * Nv[t + e / 3] * Nu[s + f % 3] * Nv[t + f / 3];
+        }
+      for (int e = 0; e < 9; ++e) {
+        const int j = t + e / 3, i = s + e % 3;
+        if (j < o->r0 || j >= o->r1) continue;
+        for (int f = 0; f < 9; ++f) m[(size_t)(j - o->r0) * nu + i] += Mloc[e][f];   // row sum
+      }
+    }
+  return 0;
+}
+
+// Incremental potential (Eq. `eq:incremental_potential`) with the lumped mass and a
+// uniform gravity field ("handled similarly to standard FEM"; Q13):
+//   E = E_elastic(x) + sum_a m_a/(2 dt^2) |x_a - xhat_a|^2 - sum_a m_a g.x_a
+//   g_a += m_a/dt^2 (x_a - xhat_a) - m_a g,   H_aa += m_a/dt^2 I3.
+// Pinned control points (Dirichlet, Q14): gradient row zeroed; Hessian rows and columns zeroed
+// and the diagonal block set to I3 (energy unchanged).  x: rows [lo, hi); xhat, m, pinned: owned rows
+// (pinned over ALL rows [n_v][n_u], since columns of other slabs' rows are masked too).
+int oracle_eval_ip(void* h, const double* x, const double* xhat, const double* m, double dt, const double* grav,
+                   const uint8_t* pinned, int flags, double* E, double* g, double* vals, int nthreads) {
+  auto* o = static_cast<Oracle*>(h);
+  const int rc = oracle_eval(h, x, flags, E, g, vals, nthreads);
+  if (rc) return rc;
+  const int nu = o->n_u;
+  const double k = 1.0 / (dt * dt);
+  for (int j = o->r0; j < o->r1; ++j)
+    for (int i = 0; i < nu; ++i) {
+      const size_t a = (size_t)(j - o->r0) * nu + i;
+      const double* xa = x + 3 * ((size_t)(j - o->lo) * nu + i);
+      const double* ha = xhat + 3 * a;
+      double d2 = 0, gx = 0;
+      for (int c = 0; c < 3; ++c) { d2 += (xa[c] - ha[c]) * (xa[c] - ha[c]); gx += grav[c] * xa[c]; }
+      if (E) *E += 0.5 * k * m[a] * d2 - m[a] * gx;
+      if (g)
+        for (int c = 0; c < 3; ++c) g[3 * a + c] += k * m[a] * (xa[c] - ha[c]) - m[a] * grav[c];
+      if (vals) {
+        const int32_t* c0 = o->col_idx.data() + o->row_ptr[a];
+        const int32_t* c1 = o->col_idx.data() + o->row_ptr[a + 1];
+        double* blk = vals + 9 * (size_t)(std::lower_bound(c0, c1, (int32_t)(j * nu + i)) - o->col_idx.data());
+        for (int c = 0; c < 3; ++c) blk[4 * c] += k * m[a];
+      }
+    }
+  if (pinned) {
+    for (int j = o->r0; j < o->r1; ++j)
+      for (int i = 0; i < nu; ++i) {
+        const size_t a = (size_t)(j - o->r0) * nu + i;
+        const bool pa = pinned[(size_t)j * nu + i] != 0;
+        if (g && pa)
+          for (int c = 0; c < 3; ++c) g[3 * a + c] = 0.0;
+        if (!vals) continue;
+        for (int32_t q = o->row_ptr[a]; q < o->row_ptr[a + 1]; ++q) {
+          const int b = o->col_idx[q];
+          if (!pa && !pinned[b]) continue;
+          double* blk = vals + 9 * (size_t)q;
+          for (int e = 0; e < 9; ++e) blk[e] = 0.0;
+          if (b == j * nu + i)
+            for (int c = 0; c < 3; ++c) blk[4 * c] = 1.0;
+        }
+      }
+  }
+  return 0;
+}
+
 // Exposed for the projection pins: the 6x6 F-space Hessian of the FBW density at F = (f1, f2).
 int oracle_membrane_A(const double* mu4, const double* f6, int project, double* A36) {
   Oracle o;
