@@ -152,6 +152,28 @@ bsf_status bsf_eval_all_batch_host(bsf_handle h, int nbatch, const double* h_x, 
                                    int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags, int chunk,
                                    bsf_stream stream);
 
+/* ---- Incremental potential (Q13/Q14) ------------------------------------
+ * E(x) = E_elastic(x) + sum_a m_a/(2 dt^2) |x_a - xhat_a|^2 - sum_a m_a g.x_a
+ * with the lumped mass m_a = sum_b M_ab, M_ab = int R0 N_a N_b dX (3x3 Gauss per
+ * knot span), the minimised objective of one implicit-Euler step; its Hessian adds m_a/dt^2 I3 to the
+ * diagonal blocks.  Pinned control points are eliminated: gradient rows 0, Hessian rows and columns 0 and
+ * the diagonal block I3 (the energy is unchanged).
+ *
+ * bsf_set_inertia: areal_density R0 (mass per rest area, >= 0), time step dt (> 0), gravity: host, 3 doubles
+ * (NULL = none), pinned: host, [n_v][n_u] bytes over ALL rows (nonzero = pinned; NULL = none).  Computes the
+ * lumped masses of the owned control points (host) and uploads them with the pinned lists; may be called
+ * again to change any of them.  Works on a host-only handle (masses only).
+ * bsf_get_lumped_mass: host m[owned rows][n_u] of the last bsf_set_inertia.
+ * bsf_eval_ip_batch: as bsf_eval_all_batch plus the terms above; d_xhat: device, the predicted positions
+ * x^ = x^n + dt v^n of the owned control points, [owned rows][n_u][3] per item, item stride xhat_stride
+ * (doubles).  BSF_E_INVALID_ARG before bsf_set_inertia. */
+bsf_status bsf_set_inertia(bsf_handle h, double areal_density, double dt, const double* gravity,
+                           const uint8_t* pinned);
+bsf_status bsf_get_lumped_mass(bsf_handle h, double* m);
+bsf_status bsf_eval_ip_batch(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride, const double* d_xhat,
+                             int64_t xhat_stride, double* d_energy, double* d_grad, int64_t grad_stride,
+                             double* d_vals, int64_t vals_stride, int flags, bsf_stream stream);
+
 /* Energy only (the line-search call). d_energy: device, 1 double (overwritten). */
 bsf_status bsf_eval_energy(bsf_handle h, const double* d_x, double* d_energy, int flags,
                            bsf_stream stream);

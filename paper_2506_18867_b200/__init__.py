@@ -28,7 +28,8 @@ _STATUS = {0: "OK", -1: "INVALID_ARG", -2: "KNOTS", -3: "TOO_SMALL", -4: "DEGENE
 SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_material", "bsf_get_sizes",
            "bsf_get_pattern", "bsf_eval_all_batch", "bsf_eval_all_batch_params", "bsf_eval_energy", "bsf_eval_gradient", "bsf_assemble_hessian", "bsf_eval_all",
            "bsf_halo_exchange", "bsf_nccl_get_unique_id", "bsf_nccl_comm_init", "bsf_nccl_comm_destroy",
-           "bsf_allreduce_sum", "bsf_get_core_rect", "bsf_eval_all_batch_host", "bsf_last_launch_count", "bsf_last_error"]
+           "bsf_allreduce_sum", "bsf_get_core_rect", "bsf_eval_all_batch_host", "bsf_set_inertia",
+           "bsf_get_lumped_mass", "bsf_eval_ip_batch", "bsf_last_launch_count", "bsf_last_error"]
 
 
 class BsfError(RuntimeError):
@@ -81,6 +82,10 @@ def lib():
         L.bsf_get_core_rect.argtypes = [vp, ip]
         L.bsf_eval_all_batch_host.argtypes = [vp, C.c_int, vp, C.c_int64, vp, vp, vp, vp, vp, C.c_int64, vp,
                                               C.c_int64, C.c_int, C.c_int, vp]
+        L.bsf_set_inertia.argtypes = [vp, C.c_double, C.c_double, dp, C.POINTER(C.c_uint8)]
+        L.bsf_get_lumped_mass.argtypes = [vp, dp]
+        L.bsf_eval_ip_batch.argtypes = [vp, C.c_int, vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, vp, C.c_int64,
+                                        C.c_int, vp]
         for s in SYMBOLS:
             getattr(L, s).restype = C.c_int if s not in ("bsf_last_error",) else C.c_char_p
         _lib = L
@@ -225,6 +230,33 @@ class Sheet:
         vs = vals[0].numel() if vals is not None else 0
         _check(lib().bsf_eval_all_batch(self._h, int(B), _ptr(x), x[0].numel(), _ptr(energy), _ptr(grad), gs,
                                         _ptr(vals), vs, int(flags), _stream(stream)))
+
+    def set_inertia(self, areal_density, dt, gravity=None, pinned=None):
+        """Incremental-potential terms (Q13/Q14): areal density R0, time step dt, gravity (3,)
+        and an optional pinned mask (bool [n_v, n_u] over all rows).  Works on host-only handles."""
+        g = None if gravity is None else np.ascontiguousarray(gravity, dtype=np.float64)
+        pin = None if pinned is None else np.ascontiguousarray(pinned, dtype=np.uint8).reshape(self.n_v, self.n_u)
+        _check(lib().bsf_set_inertia(self._h, float(areal_density), float(dt),
+                                     None if g is None else g.ctypes.data_as(C.POINTER(C.c_double)),
+                                     None if pin is None else pin.ctypes.data_as(C.POINTER(C.c_uint8))))
+        self._ip_keep = (g, pin)
+
+    def lumped_mass(self):
+        """Lumped masses of the owned control points (numpy [rows, n_u]) of the last set_inertia."""
+        m = np.zeros((self.row_end - self.row_begin, self.n_u))
+        _check(lib().bsf_get_lumped_mass(self._h, m.ctypes.data_as(C.POINTER(C.c_double))))
+        return m
+
+    def eval_ip_batch(self, x, xhat, energy=None, grad=None, vals=None, flags=0, stream=None):
+        """Incremental potential for a batch: x [B, *x_shape()], xhat [B, rows, n_u, 3] (CUDA float64);
+        outputs as eval_all_batch."""
+        B = x.shape[0]
+        if tuple(x.shape[1:]) != self.x_shape() or tuple(xhat.shape) != (B, self.row_end - self.row_begin, self.n_u, 3):
+            raise ValueError("x must be [B, *x_shape()] and xhat [B, rows, n_u, 3]")
+        gs = grad[0].numel() if grad is not None else 0
+        vs = vals[0].numel() if vals is not None else 0
+        _check(lib().bsf_eval_ip_batch(self._h, int(B), _ptr(x), x[0].numel(), _ptr(xhat), xhat[0].numel(),
+                                       _ptr(energy), _ptr(grad), gs, _ptr(vals), vs, int(flags), _stream(stream)))
 
     def eval_all_batch_host(self, x_host, x_stage, energy=None, energy_host=None, grad=None, vals=None, params=None,
                             flags=0, chunk=0, stream=None):

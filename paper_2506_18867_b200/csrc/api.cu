@@ -15,6 +15,7 @@
 #include "core.hpp"
 #include "frame.hpp"
 #include "tile.hpp"
+#include "ip.hpp"
 
 namespace bsf {
 int generic_eval(const GenericTables& t, const double* d_x, const Mat& mat, int flags, int64_t nnzb, int64_t nrows,
@@ -43,6 +44,15 @@ struct bsf_sheet {
   cudaEvent_t ev_copy = nullptr, ev_start = nullptr;
   struct StageUse { const void* ptr; cudaEvent_t done; };   // BSF_ASYNC_STAGE: last reader of each stage
   std::vector<StageUse> stage_uses;
+  // incremental potential (bsf_set_inertia)
+  bool ip_set = false;
+  double ip_k = 0.0, ip_g[3] = {0.0, 0.0, 0.0};
+  std::vector<double> h_mass;
+  double* d_mass = nullptr;
+  int32_t *d_diag = nullptr, *d_zero = nullptr, *d_pin = nullptr;
+  int nzero = 0, npin = 0;
+  double* d_ip_epart = nullptr;
+  int64_t ip_epart_cap = 0;
   std::vector<void*> allocs;
   int last_launches = 0;
   bool host_only = false;
@@ -319,7 +329,7 @@ bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, doubl
 
 static bsf_status eval_batch_impl(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride, double* d_energy,
                                   double* d_grad, int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags,
-                                  bsf_stream stream, const double* d_params) {
+                                  bsf_stream stream, const double* d_params, const bsf::IpFused* ip = nullptr) {
   if (!h || !d_x || nbatch < 0) return fail(BSF_E_INVALID_ARG, "null argument / negative batch");
   if (nbatch == 0) return BSF_OK;
   if (flags & ~31) return fail(BSF_E_INVALID_ARG, "unknown flag bits");
@@ -342,7 +352,7 @@ static bsf_status eval_batch_impl(bsf_handle h, int nbatch, const double* d_x, i
   if (h->tile_ok && !(flags & BSF_GENERIC_PATH)) {
     rc = bsf::tile_eval(h->tt, h->sh, d_x, x_stride, h->mat, flags, nbatch, d_energy, d_grad, grad_stride, d_vals,
                         vals_stride, st, &nl, h->dalloc(), d_params,
-                        (h->core_ok && !(flags & BSF_TILE_ONLY)) ? &h->ct : nullptr, &h->ft);
+                        (h->core_ok && !(flags & BSF_TILE_ONLY)) ? &h->ct : nullptr, &h->ft, ip);
   } else {
     const int64_t nrows = (int64_t)(h->sh.r1 - h->sh.r0) * h->sh.n_u, nnzb = (int64_t)h->sh.col_idx.size();
     for (int b = 0; b < nbatch && rc == 0; ++b) {
@@ -372,6 +382,102 @@ bsf_status bsf_eval_all_batch_params(bsf_handle h, int nbatch, const double* d_x
   if (!d_params) return fail(BSF_E_INVALID_ARG, "null parameters");
   return eval_batch_impl(h, nbatch, d_x, x_stride, d_energy, d_grad, grad_stride, d_vals, vals_stride, flags, stream,
                          d_params);
+}
+
+bsf_status bsf_set_inertia(bsf_handle h, double areal_density, double dt, const double* gravity,
+                           const uint8_t* pinned) {
+  if (!h) return fail(BSF_E_INVALID_ARG, "null handle");
+  if (!(dt > 0.0) || !(areal_density >= 0.0)) return fail(BSF_E_INVALID_ARG, "need dt > 0 and areal_density >= 0");
+  const bsf::Sheet& sh = h->sh;
+  std::vector<double> m;
+  std::string err;
+  const int rc = bsf::lumped_mass(sh, areal_density, m, err);
+  if (rc) return fail(BSF_E_DEGENERATE_GEOMETRY, err);
+  const int nu = sh.n_u, nrows = (sh.r1 - sh.r0) * nu;
+  std::vector<int32_t> diag(nrows), zero, pin;
+  for (int a = 0; a < nrows; ++a) {
+    const int32_t ga = sh.r0 * nu + a;
+    const int32_t* c0 = sh.col_idx.data() + sh.row_ptr[a];
+    const int32_t* c1 = sh.col_idx.data() + sh.row_ptr[a + 1];
+    const int32_t* it = std::lower_bound(c0, c1, ga);
+    if (it == c1 || *it != ga) return fail(BSF_E_INVALID_ARG, "pattern without a diagonal block");
+    diag[a] = (int32_t)(it - sh.col_idx.data());
+    if (!pinned) continue;
+    const bool pa = pinned[ga] != 0;
+    if (pa) pin.push_back(a);
+    for (const int32_t* q = c0; q < c1; ++q)
+      if ((pa || pinned[*q]) && !(pa && *q == ga)) zero.push_back((int32_t)(q - sh.col_idx.data()));
+  }
+  if (!h->host_only) {   // a host-only handle keeps the masses (bsf_get_lumped_mass) but cannot evaluate
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != h->device) cudaSetDevice(h->device);
+    bsf_status s = h->upload(&h->d_mass, m);
+    if (s == BSF_OK) s = h->upload(&h->d_diag, diag);
+    if (s == BSF_OK) s = h->upload(&h->d_zero, zero);
+    if (s == BSF_OK) s = h->upload(&h->d_pin, pin);
+    if (prev != h->device) cudaSetDevice(prev);
+    if (s != BSF_OK) return s;
+  }
+  h->h_mass = m;
+  h->nzero = (int)zero.size();
+  h->npin = (int)pin.size();
+  h->ip_k = 1.0 / (dt * dt);
+  for (int c = 0; c < 3; ++c) h->ip_g[c] = gravity ? gravity[c] : 0.0;
+  h->ip_set = true;
+  return BSF_OK;
+}
+
+bsf_status bsf_get_lumped_mass(bsf_handle h, double* m) {
+  if (!h || !m) return fail(BSF_E_INVALID_ARG, "null argument");
+  if (!h->ip_set) return fail(BSF_E_INVALID_ARG, "bsf_set_inertia has not been called");
+  std::memcpy(m, h->h_mass.data(), h->h_mass.size() * sizeof(double));
+  return BSF_OK;
+}
+
+bsf_status bsf_eval_ip_batch(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride, const double* d_xhat,
+                             int64_t xhat_stride, double* d_energy, double* d_grad, int64_t grad_stride, double* d_vals,
+                             int64_t vals_stride, int flags, bsf_stream stream) {
+  if (!h || !d_x || !d_xhat || nbatch < 0) return fail(BSF_E_INVALID_ARG, "null argument / negative batch");
+  if (!h->ip_set) return fail(BSF_E_INVALID_ARG, "bsf_set_inertia has not been called");
+  if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
+  const int64_t ncp = (int64_t)(h->sh.r1 - h->sh.r0) * h->sh.n_u;
+  if (nbatch > 1 && xhat_stride < 3 * ncp) return fail(BSF_E_INVALID_ARG, "batch strides smaller than one item");
+  // fused into the core / band / corner kernels when that path runs (every affine REDUCED sheet), else an
+  // epilogue pass after the assembly; the pinned elimination always runs after
+  const bool fused = h->tile_ok && h->core_ok && h->ft.ok && !(flags & (BSF_TILE_ONLY | BSF_GENERIC_PATH)) &&
+                     !getenv("BSF_IP_EPILOGUE");
+  bsf::IpFused ipf;
+  ipf.xhat = d_xhat; ipf.xhs = xhat_stride; ipf.mass = h->d_mass; ipf.k = h->ip_k;
+  for (int c = 0; c < 3; ++c) ipf.grav[c] = h->ip_g[c];
+  bsf_status s = eval_batch_impl(h, nbatch, d_x, x_stride, d_energy, d_grad, grad_stride, d_vals, vals_stride, flags,
+                                 stream, nullptr, fused ? &ipf : nullptr);
+  if (s != BSF_OK || nbatch == 0) return s;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  const int64_t need = (int64_t)nbatch * bsf::ip_partials((int)ncp);
+  if (!fused && d_energy && need > h->ip_epart_cap) {
+    s = h->alloc(&h->d_ip_epart, (size_t)need);
+    if (s == BSF_OK) h->ip_epart_cap = need;
+  }
+  if (s == BSF_OK) {
+    bsf::IpArgs A;
+    A.x = d_x; A.xs = x_stride; A.xhat = d_xhat; A.xhs = xhat_stride;
+    A.g = d_grad; A.gs = grad_stride; A.vals = d_vals; A.vs = vals_stride;
+    A.epart = h->d_ip_epart; A.mass = h->d_mass; A.diag = h->d_diag; A.zero_blk = h->d_zero; A.pin_cp = h->d_pin;
+    A.nzero = h->nzero; A.npin = h->npin;
+    A.ncp = (int)ncp; A.n_u = h->sh.n_u; A.r0 = h->sh.r0; A.xlo = h->sh.xlo;
+    A.k = h->ip_k;
+    for (int c = 0; c < 3; ++c) A.grav[c] = h->ip_g[c];
+    int nl = 0;
+    if (fused ? bsf::ip_pin(A, nbatch, static_cast<cudaStream_t>(stream), &nl)
+              : bsf::ip_eval(A, nbatch, d_energy, static_cast<cudaStream_t>(stream), &nl))
+      s = check_cuda("kernel launch") == BSF_OK ? fail(BSF_E_CUDA, "launch failed") : BSF_E_CUDA;
+    h->last_launches += nl;
+  }
+  if (prev != h->device) cudaSetDevice(prev);
+  return s;
 }
 
 bsf_status bsf_eval_all_batch_host(bsf_handle h, int nbatch, const double* h_x, int64_t x_stride, double* d_x_stage,

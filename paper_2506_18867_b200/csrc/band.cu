@@ -36,6 +36,7 @@
 #include "core.hpp"
 #include "fbw.cuh"
 #include "frame.hpp"
+#include "ip.hpp"
 
 namespace bsf {
 
@@ -68,6 +69,11 @@ struct BandArgs {
   BandDesc desc[4];
   const uint32_t* ent;            // template entries of all bands
   const double2* entd;            // per entry (d_a,u, d_a,v) at its window position (membrane; 0 for bending)
+  // incremental-potential terms (Q13; xhat == nullptr: elastic only)
+  const double* xhat;
+  int64_t xhs;
+  const double* mass;
+  double ipk, grav[3];
 };
 
 template <int B, int E, class F>
@@ -326,6 +332,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
       for (int q = 0; q < nb; ++q) {
         const uint32_t E = eb[q];
         gacc = fma(lw[((E >> 16) & 0xFFF) + (E >> 28)], brec[(E & 0xFFFF) + go], gacc);
+      }
+    }
+    if (valid && A.xhat) {   // incremental potential: diagonal m/dt^2, gradient and energy (gradient lanes)
+      const int ai = axis ? t : s, aj = axis ? s : t;
+      const int64_t aloc = (int64_t)(aj - A.r0) * A.n_u + ai;
+      const double mm = A.mass[aloc];
+      if (hess) {
+        if (r3 == c3) acc[12] += A.ipk * mm;
+      } else {
+        const int c = lc - 9;
+        const double xa = pos[((t - od0) * kPA + (s - S0 + 2)) * 3 + c];
+        const double d = xa - A.xhat[item * A.xhs + aloc * 3 + c];
+        gacc += A.ipk * mm * d - mm * A.grav[c];
+        e_acc += 0.5 * A.ipk * mm * d * d - mm * A.grav[c] * xa;
       }
     }
     if (valid && !(A.dbg & 64)) {
@@ -627,7 +647,7 @@ int build_band(const Sheet& sh, const CoreTables& ct, BandTables& bt, std::strin
 int band_eval(const BandTables& bt, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride, const int32_t* d_row_ptr,
               double* e_part, int64_t e_stride, int64_t e_off, const double* d_params, const double* G4, double detJ,
-              cudaStream_t st) {
+              cudaStream_t st, const IpFused* ip) {
   if (!bt.ok || bt.nctas == 0) return 0;
   static_assert(sizeof(BandArgs) <= 32000, "kernel parameter budget");
   BandArgs A;
@@ -651,6 +671,9 @@ int band_eval(const BandTables& bt, const Sheet& sh, const double* d_x, int64_t 
   for (int b = 0; b <= bt.nbands; ++b) A.cfirst[b] = bt.h_cfirst[b];
   std::memcpy(A.desc, bt.h_desc.data(), sizeof(BandDesc) * bt.h_desc.size());
   A.ent = bt.ent; A.entd = bt.entd;
+  A.xhat = ip ? ip->xhat : nullptr; A.xhs = ip ? ip->xhs : 0; A.mass = ip ? ip->mass : nullptr;
+  A.ipk = ip ? ip->k : 0.0;
+  for (int c = 0; c < 3; ++c) A.grav[c] = ip ? ip->grav[c] : 0.0;
   dim3 grid(bt.nctas, nbatch);
   k_band<<<grid, kThreads, bt.smem, st>>>(A);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;

@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "core.hpp"
+#include "ip.hpp"
 #include "fbw.cuh"
 
 namespace bsf {
@@ -56,6 +57,11 @@ struct CoreArgs {
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
   const double* tabs;      // device [104]: S[4][9][2] | LA[9] | LB[9] | LC[9] | what[5]
   double what[5];
+  // incremental-potential terms (Q13; xhat == nullptr: elastic only)
+  const double* xhat;
+  int64_t xhs;
+  const double* mass;
+  double ipk, grav[3];
 };
 
 // shared constants block (doubles)
@@ -126,8 +132,8 @@ template <int PI>
 __device__ __forceinline__ void gather_grad(const uint32_t (&base0)[4], const uint32_t (&base1)[4],
                                             const double* const (&bb0)[3], const double* const (&bb1)[3],
                                             uint32_t o_pu, uint32_t o_pv, const double* __restrict__ cst,
-                                            double* gdst) {
-  double g = 0.0;
+                                            double* gdst, double g0) {
+  double g = g0;
   static_for<0, make_template(PI).nslot>([&](auto SI) {
     constexpr int s = decltype(SI)::value;
     constexpr Template T = make_template(PI);
@@ -143,7 +149,7 @@ __device__ __forceinline__ void gather_grad(const uint32_t (&base0)[4], const ui
     const double* b = ((dp & 1) ? bb1[dq + 2] : bb0[dq + 2]) + ((dp + 2) >> 1);
     g = fma(cst[kCstLw + k], b[0], g);
   });
-  *gdst = g;
+  if (gdst) *gdst = g;
 }
 
 template <int PI>
@@ -152,7 +158,7 @@ __device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
                                             const double* const (&bb1)[3], int o_rc, int o_cr,
                                             int o_pu, int o_pv, bool diag, const double* __restrict__ cst,
                                             double* st_lane, double* gdst, bool active, uint32_t bar,
-                                            uint32_t parity) {
+                                            uint32_t parity, double dshift) {
   double acc[kNB];
 #pragma unroll
   for (int k = 0; k < kNB; ++k) acc[k] = 0.0;
@@ -177,6 +183,7 @@ __device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
   if (diag) {
 #pragma unroll
     for (int k = 0; k < kNB; ++k) acc[k] += cst[kCstBeta + k];
+    acc[block_index(0, 0)] += dshift;   // inertia m_a/dt^2 (0 without the incremental potential)
   }
   if (!st_lane) return;
   mbar_wait(bar, parity);
@@ -492,20 +499,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
             }
             double* gdst = nullptr;
             const uint32_t par = k & 1;
+            const double dshift = (diag && A.xhat && active) ? A.ipk * A.mass[(int64_t)(jr - A.r0) * A.n_u + i] : 0.0;
             if (PI == 0)
               gather_role<0>(base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
                              8 * (o_pv - o_uu), diag, cst, st_lane,
-                             gdst, active, bar, par);
+                             gdst, active, bar, par, dshift);
             else
               gather_role<1>(base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
                              8 * (o_pv - o_uu), diag, cst, st_lane,
-                             gdst, active, bar, par);
+                             gdst, active, bar, par, dshift);
           }
         }
       }
       // (c') gradient rows of step k: the last two point warps (bending-only point work) take the 6
       // (parity, component) rounds
-      if (k >= 0 && gout && warp >= kThreads / 32 - 2 && !(A.dbg & 2)) {
+      if (k >= 0 && (gout || A.xhat) && warp >= kThreads / 32 - 2 && !(A.dbg & 2)) {
         const int PI = warp - (kThreads / 32 - 2);
         const int jr = j + h;
         const int sigma = (PI + jr + i0) & 1;
@@ -531,10 +539,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
               bb1[d] = rb + (1 - sigma) * kBendD + sigma;
               s2 = (s2 == kRing - 1) ? 0 : s2 + 1;
             }
-            double* gdst = gout + ((int64_t)(jr - A.r0) * A.n_u + i) * 3 + r;
-            const uint32_t opu = 8 * (21 + r) * kKH, opv = 8 * (24 + r) * kKH;
-            if (PI == 0) gather_grad<0>(gb0, gb1, bb0, bb1, opu, opv, cst, gdst);
-            else gather_grad<1>(gb0, gb1, bb0, bb1, opu, opv, cst, gdst);
+            const int64_t al = (int64_t)(jr - A.r0) * A.n_u + i;
+            double* gdst = gout ? gout + al * 3 + r : nullptr;
+            // incremental potential: m/dt^2 (x - xhat) - m g on the gradient, its energy on this lane
+            double g0 = 0.0;
+            if (A.xhat) {
+              const double mm = A.mass[al], xa = x[((int64_t)(jr - A.xlo) * A.n_u + i) * 3 + r];
+              const double d = xa - A.xhat[item * A.xhs + al * 3 + r], gr = A.grav[r];
+              g0 = A.ipk * mm * d - mm * gr;
+              e_acc += 0.5 * A.ipk * mm * d * d - mm * gr * xa;
+            }
+            if (gout) {
+              const uint32_t opu = 8 * (21 + r) * kKH, opv = 8 * (24 + r) * kKH;
+              if (PI == 0) gather_grad<0>(gb0, gb1, bb0, bb1, opu, opv, cst, gdst, g0);
+              else gather_grad<1>(gb0, gb1, bb0, bb1, opu, opv, cst, gdst, g0);
+            }
           }
         }
       }
@@ -832,9 +851,12 @@ int core_pick_chunks(const CoreTables& ct, int nbatch) {
 int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride, double* e_part,
               int64_t e_stride, int64_t e_off, int nchunks, const double* d_params, double detJ_ref,
-              cudaStream_t st) {
+              cudaStream_t st, const IpFused* ip) {
   (void)detJ_ref;
   CoreArgs A;
+  A.xhat = ip ? ip->xhat : nullptr; A.xhs = ip ? ip->xhs : 0; A.mass = ip ? ip->mass : nullptr;
+  A.ipk = ip ? ip->k : 0.0;
+  for (int c = 0; c < 3; ++c) A.grav[c] = ip ? ip->grav[c] : 0.0;
   A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride;
   A.epart = e_part; A.e_stride = e_stride; A.e_off = e_off;
   A.row_ptr = ct.row_ptr; A.rp_base = ct.rp_base; A.rp_stride = ct.rp_stride; A.params = d_params;

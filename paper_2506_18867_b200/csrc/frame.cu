@@ -27,6 +27,7 @@
 #include "core.hpp"
 #include "fbw.cuh"
 #include "frame.hpp"
+#include "ip.hpp"
 
 namespace bsf {
 
@@ -64,6 +65,11 @@ struct FrameArgs {
                           // transposed output = block of H_ab^T in row b (frame pairs computed once) or -1
   const uint32_t* ent;    // tile-relative contribution entries
   const int32_t* tent;    // [ntiles+1]
+  // incremental-potential terms (Q13; xhat == nullptr: elastic only)
+  const double* xhat;
+  int64_t xhs;
+  const double* mass;
+  double ipk, grav[3];
 };
 
 constexpr int kPosD = 8 * 8 * 3;    // (tw + 4) * (th + 4) * 3 for 4x4 tiles
@@ -72,7 +78,7 @@ constexpr int kMRec = 29;           // 27 channels + pad
 constexpr int kMCf = 19;            // 18 d-vector entries + pad
 constexpr int kBRec = 13;           // 12 bending channels + pad
 
-__global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
+__global__ void __launch_bounds__(kThreads, 3) k_frame(const FrameArgs A) {
   extern __shared__ __align__(16) double fsm[];
   const int tile = blockIdx.x, item = blockIdx.y, tid = threadIdx.x;
   const int4 ti = A.tile[tile];
@@ -229,6 +235,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
         hb = fma(rec[ea], rec[eb], hb);
       }
     }
+    if (A.xhat && task.w) hb += A.ipk * A.mass[task.w - 1];   // diagonal block: inertia m_a/dt^2
     h[0] += hb; h[4] += hb; h[8] += hb;
     if (A.vals) {
       double* dst = A.vals + item * A.vs + (int64_t)out * 9;
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
         for (int k = 0; k < 9; ++k) dt[k] = h[3 * (k % 3) + k / 3];
       }
     }
-  } else if (out < 0 && A.g) {
+  } else if (out < 0 && (A.g || A.xhat)) {
     double g0 = 0.0, g1 = 0.0, g2 = 0.0;
     for (int e = 0; e < cnt; ++e) {
       const uint32_t E = sent[first + e];
@@ -259,8 +266,25 @@ __global__ void __launch_bounds__(kThreads, 4) k_frame(const FrameArgs A) {
         g2 = fma(La, rec[11], g2);
       }
     }
-    double* gd = A.g + item * A.gs + 3 * (int64_t)(~out);
-    gd[0] = g0; gd[1] = g1; gd[2] = g2;
+    const int64_t al = ~out;
+    if (A.xhat) {   // incremental potential: m/dt^2 (x - xhat) - m g and its energy
+      const int aj = (int)(al / A.n_u) + A.r0, ai = (int)(al % A.n_u);
+      const double* xa = pos + ((aj - (j0 - 2)) * PW + (ai - (i0 - 2))) * 3;
+      const double* xh = A.xhat + item * A.xhs + 3 * al;
+      const double mm = A.mass[al];
+      double gi[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double d = xa[c] - xh[c];
+        gi[c] = A.ipk * mm * d - mm * A.grav[c];
+        e_acc += 0.5 * A.ipk * mm * d * d - mm * A.grav[c] * xa[c];
+      }
+      g0 += gi[0]; g1 += gi[1]; g2 += gi[2];
+    }
+    if (A.g) {
+      double* gd = A.g + item * A.gs + 3 * al;
+      gd[0] = g0; gd[1] = g1; gd[2] = g2;
+    }
   }
   }
   // ---- energy partial of this CTA
@@ -410,7 +434,8 @@ int build_frame(const Sheet& sh, const CoreTables& ct, FrameTables& ft, std::str
         const size_t f = ent.size() - tbase;
         if (f >= (1u << 20) || per[k].size() >= 4096) { err = "frame: program too long"; return -1; }
         const int32_t outi = (k == kSlots - 1) ? ~(int32_t)al : sh.row_ptr[al] + k;
-        ttask.push_back(make_uint4((uint32_t)f | ((uint32_t)per[k].size() << 20), (uint32_t)outi, (uint32_t)outT, 0u));
+        const uint32_t dg = (k < kMaxNB && c0[k] == a_glob) ? (uint32_t)al + 1u : 0u;   // diagonal block: a_loc + 1
+        ttask.push_back(make_uint4((uint32_t)f | ((uint32_t)per[k].size() << 20), (uint32_t)outi, (uint32_t)outT, dg));
         ent.insert(ent.end(), per[k].begin(), per[k].end());
       }
     }
@@ -486,9 +511,12 @@ int build_frame(const Sheet& sh, const CoreTables& ct, FrameTables& ft, std::str
 int frame_eval(const FrameTables& ft, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
                int nbatch, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride, const int32_t* d_row_ptr,
                double* e_part, int64_t e_stride, int64_t e_off, const double* d_params, const double* G4, double detJ,
-               cudaStream_t st) {
+               cudaStream_t st, const IpFused* ip) {
   if (ft.ntiles == 0) return 0;
   FrameArgs A;
+  A.xhat = ip ? ip->xhat : nullptr; A.xhs = ip ? ip->xhs : 0; A.mass = ip ? ip->mass : nullptr;
+  A.ipk = ip ? ip->k : 0.0;
+  for (int c = 0; c < 3; ++c) A.grav[c] = ip ? ip->grav[c] : 0.0;
   A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride;
   A.epart = e_part; A.e_stride = e_stride; A.e_off = e_off;
   A.row_ptr = d_row_ptr; A.params = d_params;

@@ -114,11 +114,11 @@ int build_band(const Sheet& sh, const CoreTables& ct, BandTables& bt, std::strin
 int band_eval(const BandTables& bt, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride, const int32_t* d_row_ptr,
               double* e_part, int64_t e_stride, int64_t e_off, const double* d_params, const double* G4, double detJ,
-              cudaStream_t st);
+              cudaStream_t st, const struct IpFused* ip = nullptr);
 
 int frame_eval(const FrameTables& ft, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
                int nbatch, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride, const int32_t* d_row_ptr,
                double* e_part, int64_t e_stride, int64_t e_off, const double* d_params, const double* G4, double detJ,
-               cudaStream_t st);
+               cudaStream_t st, const struct IpFused* ip = nullptr);
 
 }  // namespace bsf

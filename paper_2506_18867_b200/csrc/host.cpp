@@ -216,6 +216,42 @@ static int eval_point(const Sheet& sh, const RulePoint& q, bool bending, Point& 
   return 0;
 }
 
+int lumped_mass(const Sheet& sh, double R0, std::vector<double>& m, std::string& err) {
+  const int nu = sh.n_u;
+  m.assign((size_t)(sh.r1 - sh.r0) * nu, 0.0);
+  double xu[3], wu[3], xv[3], wv[3];
+  for (int t = std::max(0, sh.r0 - 2); t < std::min(sh.Sv, sh.r1); ++t) {   // spans touching owned rows
+    g3(t, t + 1, xv, wv);
+    for (int s = 0; s < sh.Su; ++s) {
+      g3(s, s + 1, xu, wu);
+      for (int b = 0; b < 3; ++b)
+        for (int a = 0; a < 3; ++a) {
+          Basis1 bu, bv;
+          basis1(sh.Su, xu[a], bu);
+          basis1(sh.Sv, xv[b], bv);
+          double Xu[2] = {0, 0}, Xv[2] = {0, 0};
+          for (int jv = 0; jv < 3; ++jv)
+            for (int iu = 0; iu < 3; ++iu) {
+              const double* X = &sh.rest[2 * ((size_t)(bv.span + jv) * nu + (bu.span + iu))];
+              for (int c = 0; c < 2; ++c) {
+                Xu[c] += bu.d1[iu] * bv.N[jv] * X[c];
+                Xv[c] += bu.N[iu] * bv.d1[jv] * X[c];
+              }
+            }
+          const double det = Xu[0] * Xv[1] - Xv[0] * Xu[1];
+          if (!(det > 0.0)) { err = "degenerate rest geometry at a mass quadrature point"; return -4; }
+          const double w = wu[a] * wv[b] * det * R0;
+          for (int jv = 0; jv < 3; ++jv) {
+            const int j = bv.span + jv;
+            if (j < sh.r0 || j >= sh.r1) continue;
+            for (int iu = 0; iu < 3; ++iu) m[(size_t)(j - sh.r0) * nu + bu.span + iu] += w * bu.N[iu] * bv.N[jv];
+          }
+        }
+    }
+  }
+  return 0;
+}
+
 int build_sheet(int n_u, int n_v, const double* ku, const double* kv, const double* rest_xy, int mrule,
                 int brule, int r0, int r1, Sheet& sh, std::string& err) {
   if (n_u < 3 || n_v < 3) { err = "need at least 3 control points per direction"; return -3; }

@@ -67,6 +67,11 @@ struct Sheet {
 int build_sheet(int n_u, int n_v, const double* ku, const double* kv, const double* rest_xy,
                 int mrule, int brule, int r0, int r1, Sheet& sh, std::string& err);
 
+// Lumped mass of the owned control points (Q13): m_a = int R0 N_a dX (the row
+// sum of the consistent mass matrix) by 3x3 Gauss per knot span.
+// m: [owned rows][n_u].  Returns 0 or -4 (det J <= 0 at a mass point, message in err).
+int lumped_mass(const Sheet& sh, double R0, std::vector<double>& m, std::string& err);
+
 // Index helpers
 inline int win_entry(int iu, int jv) { return 3 * jv + iu; }
 

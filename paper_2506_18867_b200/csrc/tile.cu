@@ -29,6 +29,7 @@
 #include "fbw.cuh"
 #include "frame.hpp"
 #include "tile.hpp"
+#include "ip.hpp"
 
 namespace bsf {
 
@@ -889,8 +890,9 @@ int tile_set_core(TileTables& tt, const Sheet& sh, const CoreTables& ct, const s
 int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_E, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride,
               cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc, const double* d_params,
-              const CoreTables* ct, const FrameTables* ft) {
+              const CoreTables* ct, const FrameTables* ft, const IpFused* ip) {
   const bool core = ct && tt.core && ct->ok;
+  if (ip && !(core && ft && ft->ok)) return -1;   // the fused incremental potential needs core + band + corners
   if (core && ft && ft->ok) {
     // frame kernel (full frame rows) + core kernel (full core rows): disjoint rows, one energy array
     // [item][frame tiles | core CTAs]; every slot is written on every call
@@ -915,13 +917,13 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     if (cudaEventRecord(tt.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(tt.side, tt.ev_fork, 0) != cudaSuccess)
       return -6;
     int rc = frame_eval(*ft, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
-                        tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, tt.side);
+                        tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, tt.side, ip);
     if (rc) return rc;
     rc = band_eval(ft->band, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
-                   tt.e_part, e_stride, ft->ntiles, d_params, ct->G, ct->detJ, tt.side);
+                   tt.e_part, e_stride, ft->ntiles, d_params, ct->G, ct->detJ, tt.side, ip);
     if (rc) return rc;
     rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
-                   nfb, core_nch, d_params, tt.detJ_ref, st);
+                   nfb, core_nch, d_params, tt.detJ_ref, st, ip);
     if (rc) return rc;
     if (cudaEventRecord(tt.ev_join, tt.side) != cudaSuccess || cudaStreamWaitEvent(st, tt.ev_join, 0) != cudaSuccess)
       return -6;

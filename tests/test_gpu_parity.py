@@ -291,3 +291,41 @@ def test_async_stage_pipelined_host_calls():
         torch.cuda.synchronize()
         assert torch.equal(G, G2) and torch.equal(V, V2) and torch.equal(E, E2)
         assert torch.equal(Eh, E.cpu())
+
+
+@pytest.mark.parametrize("case", ["c1", "c2_pinned", "slab"])
+def test_incremental_potential_matches_oracle(case):
+    """bsf_eval_ip_batch (elastic assembly + lumped-mass inertia, gravity, pinned elimination) against the
+    oracle's eval_ip, every path, a batch of 2 items with different predicted positions."""
+    sh = W.make_c1() if case == "c1" else W.make_c2(state=4)
+    r0, r1 = (40, 90) if case == "slab" else (0, sh.n_v)
+    R0, dt, grav = 0.15, 4e-3, np.array([0.0, -9.81, 0.5])
+    pinned = None
+    if case == "c2_pinned":
+        pinned = np.zeros((sh.n_v, sh.n_u), bool)
+        pinned[-1, :] = True
+        pinned[0, :3] = True
+    o = O.Oracle.from_sheet(sh, r0=r0, r1=r1)
+    m = o.lumped_mass(R0)
+    rng = np.random.default_rng(17)
+    s = B.Sheet.from_sheet(sh, row_begin=r0, row_end=r1)
+    s.set_inertia(R0, dt, gravity=grav, pinned=pinned)
+    assert np.max(np.abs(s.lumped_mass() - m)) < 1e-14 * m.max()
+    xs = [sh.x, sh.x + rng.normal(0, 1e-3, sh.x.shape)]
+    xh = [x[r0:r1] + rng.normal(0, 2e-3, x[r0:r1].shape) for x in xs]
+    X = torch.stack([torch.from_numpy(np.ascontiguousarray(x[s.x_row_begin:s.x_row_end])) for x in xs]).cuda()
+    XH = torch.from_numpy(np.stack(xh)).cuda()
+    for path in PATHS:
+        E = torch.zeros(2, dtype=torch.float64, device="cuda")
+        G = torch.zeros((2, r1 - r0, sh.n_u, 3), dtype=torch.float64, device="cuda")
+        V = torch.zeros((2, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+        s.eval_ip_batch(X, XH, E, G, V, flags=B.PROJECT_PSD | path)
+        torch.cuda.synchronize()
+        for b in range(2):
+            Er, gr, vr = o.eval_ip(xs[b], xh[b], m, dt, grav, pinned, flags=O.FLAG_PROJECT)
+            rp, ci = o.pattern()
+            hd = diag_block_norms(vr, rp, ci, r0, sh.n_u)
+            va = o.eval_ip(xs[b], xh[b], m, dt, grav, pinned, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM,
+                           energy=False, gradient=False)[2]
+            assert_parity(E[b].item(), G[b].cpu().numpy(), V[b].cpu().numpy(), Er, gr, vr,
+                          what=f"ip case={case} path={path} item={b}", hdiag=hd, cmax=np.abs(xs[b]).max(), vabs=va)

@@ -158,3 +158,20 @@ def test_ip_pinned_masking():
                 assert np.array_equal(vp[k], np.eye(3) if a == b else np.zeros((3, 3)))
             else:
                 assert np.array_equal(vp[k], v[k])
+
+
+@pytest.mark.parametrize("case", ["c1", "slab", "curved"])
+def test_library_host_lumped_mass_matches_oracle(case):
+    """bsf_set_inertia computes the masses on the host (also for a host-only handle, device = -1); they
+    equal the oracle's row-summed consistent mass to rounding."""
+    import paper_2506_18867_b200 as B
+    sh = W.make_c1()
+    r0, r1 = (3, 9) if case == "slab" else (0, sh.n_v)
+    if case == "curved":
+        sh = W.Sheet(sh.n_u, sh.n_v, sh.knots_u, sh.knots_v, W.make_curved_rest(sh.n_u, sh.n_v, 2), sh.x, sh.E,
+                     sh.nu, sh.h)
+    s = B.Sheet.from_sheet(sh, row_begin=r0, row_end=r1, device=-1)
+    s.set_inertia(0.7, 1e-3, gravity=(0, 0, -9.81))
+    m = s.lumped_mass()
+    ref = O.Oracle.from_sheet(sh, r0=r0, r1=r1).lumped_mass(0.7)
+    assert np.max(np.abs(m - ref)) < 1e-14 * ref.max()
