@@ -174,6 +174,22 @@ bsf_status bsf_eval_ip_batch(bsf_handle h, int nbatch, const double* d_x, int64_
                              int64_t xhat_stride, double* d_energy, double* d_grad, int64_t grad_stride,
                              double* d_vals, int64_t vals_stride, int flags, bsf_stream stream);
 
+/* ---- Linear algebra on the assembled Hessian (solve.cu) --------------------------------
+ * The projected Newton step solves (H_inertia + H_elasticity) dC = -g; the paper
+ * factorises (CHOLMOD), this library offers device block-Jacobi PCG on the BSR values it assembled.
+ * bsf_bsr_spmv: d_y[owned rows][n_u][3] = H d_x, d_x in the position layout (owned rows plus the 2-row halo
+ *   of a slab, like bsf_eval_all's d_x); d_vals: the handle's pattern.  Asynchronous.
+ * bsf_gershgorin: host lo / hi with spec(H) within [lo, hi] (union of the scalar rows' Gershgorin discs,
+ *   the bound PAPER.md:884-888 gates its Neumann split with).  Synchronises `stream`.
+ * bsf_pcg: whole-sheet handles only; solves H x = b for SPD H (e.g. the PSD-projected Hessian plus inertia),
+ *   d_b / d_x: device [n_v][n_u][3], d_x holds the initial guess on entry and the solution on return;
+ *   stops at |b - Hx| <= rtol |b| or after max_iter iterations (check *relres); *iters, *relres: host (may
+ *   be NULL).  BSF_E_INVALID_ARG if H is found not SPD.  Synchronises `stream` every 16 iterations. */
+bsf_status bsf_bsr_spmv(bsf_handle h, const double* d_vals, const double* d_x, double* d_y, bsf_stream stream);
+bsf_status bsf_gershgorin(bsf_handle h, const double* d_vals, double* lo, double* hi, bsf_stream stream);
+bsf_status bsf_pcg(bsf_handle h, const double* d_vals, const double* d_b, double* d_x, int max_iter, double rtol,
+                   int* iters, double* relres, bsf_stream stream);
+
 /* Energy only (the line-search call). d_energy: device, 1 double (overwritten). */
 bsf_status bsf_eval_energy(bsf_handle h, const double* d_x, double* d_energy, int flags,
                            bsf_stream stream);

@@ -29,7 +29,8 @@ SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_mate
            "bsf_get_pattern", "bsf_eval_all_batch", "bsf_eval_all_batch_params", "bsf_eval_energy", "bsf_eval_gradient", "bsf_assemble_hessian", "bsf_eval_all",
            "bsf_halo_exchange", "bsf_nccl_get_unique_id", "bsf_nccl_comm_init", "bsf_nccl_comm_destroy",
            "bsf_allreduce_sum", "bsf_get_core_rect", "bsf_eval_all_batch_host", "bsf_set_inertia",
-           "bsf_get_lumped_mass", "bsf_eval_ip_batch", "bsf_last_launch_count", "bsf_last_error"]
+           "bsf_get_lumped_mass", "bsf_eval_ip_batch", "bsf_bsr_spmv", "bsf_gershgorin", "bsf_pcg",
+           "bsf_last_launch_count", "bsf_last_error"]
 
 
 class BsfError(RuntimeError):
@@ -86,6 +87,9 @@ def lib():
         L.bsf_get_lumped_mass.argtypes = [vp, dp]
         L.bsf_eval_ip_batch.argtypes = [vp, C.c_int, vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, vp, C.c_int64,
                                         C.c_int, vp]
+        L.bsf_bsr_spmv.argtypes = [vp, vp, vp, vp, vp]
+        L.bsf_gershgorin.argtypes = [vp, vp, dp, dp, vp]
+        L.bsf_pcg.argtypes = [vp, vp, vp, vp, C.c_int, C.c_double, C.POINTER(C.c_int), dp, vp]
         for s in SYMBOLS:
             getattr(L, s).restype = C.c_int if s not in ("bsf_last_error",) else C.c_char_p
         _lib = L
@@ -257,6 +261,29 @@ class Sheet:
         vs = vals[0].numel() if vals is not None else 0
         _check(lib().bsf_eval_ip_batch(self._h, int(B), _ptr(x), x[0].numel(), _ptr(xhat), xhat[0].numel(),
                                        _ptr(energy), _ptr(grad), gs, _ptr(vals), vs, int(flags), _stream(stream)))
+
+    def spmv(self, vals, x, y=None, stream=None):
+        """y = H x with the BSR values `vals` [nnzb, 3, 3]; x in the position layout (x_shape()), y [rows, n_u, 3]."""
+        import torch
+        if y is None:
+            y = torch.empty((self.row_end - self.row_begin, self.n_u, 3), dtype=torch.float64, device=x.device)
+        _check(lib().bsf_bsr_spmv(self._h, _ptr(vals), _ptr(x), _ptr(y), _stream(stream)))
+        return y
+
+    def gershgorin(self, vals, stream=None):
+        """(lo, hi): the spectrum of H lies in [lo, hi] (Gershgorin discs of the scalar rows)."""
+        lo, hi = C.c_double(), C.c_double()
+        _check(lib().bsf_gershgorin(self._h, _ptr(vals), C.byref(lo), C.byref(hi), _stream(stream)))
+        return lo.value, hi.value
+
+    def pcg(self, vals, b, x=None, max_iter=1000, rtol=1e-10, stream=None):
+        """Block-Jacobi PCG for H x = b (whole-sheet handle, SPD H); returns (x, iterations, relative residual)."""
+        import torch
+        x = torch.zeros_like(b) if x is None else x
+        it, rr = C.c_int(), C.c_double()
+        _check(lib().bsf_pcg(self._h, _ptr(vals), _ptr(b), _ptr(x), int(max_iter), float(rtol), C.byref(it),
+                             C.byref(rr), _stream(stream)))
+        return x, it.value, rr.value
 
     def eval_all_batch_host(self, x_host, x_stage, energy=None, energy_host=None, grad=None, vals=None, params=None,
                             flags=0, chunk=0, stream=None):

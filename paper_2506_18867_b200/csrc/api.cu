@@ -16,6 +16,7 @@
 #include "frame.hpp"
 #include "tile.hpp"
 #include "ip.hpp"
+#include "solve.hpp"
 
 namespace bsf {
 int generic_eval(const GenericTables& t, const double* d_x, const Mat& mat, int flags, int64_t nnzb, int64_t nrows,
@@ -53,6 +54,10 @@ struct bsf_sheet {
   int nzero = 0, npin = 0;
   double* d_ip_epart = nullptr;
   int64_t ip_epart_cap = 0;
+  // linear algebra on the assembled Hessian (solve.cu)
+  int32_t *d_rp = nullptr, *d_ci = nullptr, *d_sdiag = nullptr;
+  bsf::CgWork cg{};
+  bool solve_ready = false, cg_ready = false;
   std::vector<void*> allocs;
   int last_launches = 0;
   bool host_only = false;
@@ -478,6 +483,93 @@ bsf_status bsf_eval_ip_batch(bsf_handle h, int nbatch, const double* d_x, int64_
   }
   if (prev != h->device) cudaSetDevice(prev);
   return s;
+}
+
+static bsf_status solve_setup(bsf_handle h, bool cg, bsf::SolveArgs& A) {
+  const bsf::Sheet& sh = h->sh;
+  const int nu = sh.n_u, nrows = (sh.r1 - sh.r0) * nu;
+  if (!h->solve_ready) {
+    std::vector<int32_t> diag(nrows);
+    for (int a = 0; a < nrows; ++a) {
+      const int32_t ga = sh.r0 * nu + a;
+      const int32_t* c0 = sh.col_idx.data() + sh.row_ptr[a];
+      const int32_t* c1 = sh.col_idx.data() + sh.row_ptr[a + 1];
+      diag[a] = (int32_t)(std::lower_bound(c0, c1, ga) - sh.col_idx.data());
+    }
+    bsf_status s = h->upload(&h->d_rp, sh.row_ptr);
+    if (s == BSF_OK) s = h->upload(&h->d_ci, sh.col_idx);
+    if (s == BSF_OK) s = h->upload(&h->d_sdiag, diag);
+    if (s == BSF_OK) s = h->alloc(&h->cg.part, (size_t)bsf::solve_parts(nrows));
+    if (s != BSF_OK) return s;
+    h->solve_ready = true;
+  }
+  if (cg && !h->cg_ready) {
+    const size_t n3 = 3 * (size_t)nrows;
+    bsf_status s = h->alloc(&h->cg.r, n3);
+    if (s == BSF_OK) s = h->alloc(&h->cg.z, n3);
+    if (s == BSF_OK) s = h->alloc(&h->cg.p, n3);
+    if (s == BSF_OK) s = h->alloc(&h->cg.q, n3);
+    if (s == BSF_OK) s = h->alloc(&h->cg.dinv, 9 * (size_t)nrows);
+    if (s == BSF_OK) s = h->alloc(&h->cg.S, (size_t)bsf::kSN);
+    if (s == BSF_OK) s = h->alloc(&h->cg.bad, 1);
+    if (s != BSF_OK) return s;
+    h->cg_ready = true;
+  }
+  A.row_ptr = h->d_rp; A.col_idx = h->d_ci; A.diag = h->d_sdiag;
+  A.nrows = nrows; A.n_u = nu; A.r0 = sh.r0; A.xlo = sh.xlo;
+  return BSF_OK;
+}
+
+bsf_status bsf_bsr_spmv(bsf_handle h, const double* d_vals, const double* d_x, double* d_y, bsf_stream stream) {
+  if (!h || !d_vals || !d_x || !d_y) return fail(BSF_E_INVALID_ARG, "null argument");
+  if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  bsf::SolveArgs A;
+  bsf_status s = solve_setup(h, false, A);
+  if (s == BSF_OK && bsf::spmv(A, d_vals, d_x, d_y, nullptr, static_cast<cudaStream_t>(stream)))
+    s = fail(BSF_E_CUDA, "spmv launch failed");
+  if (prev != h->device) cudaSetDevice(prev);
+  return s;
+}
+
+bsf_status bsf_gershgorin(bsf_handle h, const double* d_vals, double* lo, double* hi, bsf_stream stream) {
+  if (!h || !d_vals || !lo || !hi) return fail(BSF_E_INVALID_ARG, "null argument");
+  if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  bsf::SolveArgs A;
+  bsf_status s = solve_setup(h, false, A);
+  if (s == BSF_OK && bsf::gershgorin(A, d_vals, h->cg.part, lo, hi, static_cast<cudaStream_t>(stream)))
+    s = fail(BSF_E_CUDA, "gershgorin failed");
+  if (prev != h->device) cudaSetDevice(prev);
+  return s;
+}
+
+bsf_status bsf_pcg(bsf_handle h, const double* d_vals, const double* d_b, double* d_x, int max_iter, double rtol,
+                   int* iters, double* relres, bsf_stream stream) {
+  if (!h || !d_vals || !d_b || !d_x) return fail(BSF_E_INVALID_ARG, "null argument");
+  if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
+  if (h->sh.r0 != 0 || h->sh.r1 != h->sh.n_v) return fail(BSF_E_INVALID_ARG, "bsf_pcg needs a whole-sheet handle");
+  if (max_iter < 0 || !(rtol > 0.0)) return fail(BSF_E_INVALID_ARG, "need max_iter >= 0 and rtol > 0");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  bsf::SolveArgs A;
+  bsf_status s = solve_setup(h, true, A);
+  int it = 0, status = 0;
+  double rr = 0.0;
+  if (s == BSF_OK && bsf::pcg(A, d_vals, d_b, d_x, h->cg, max_iter, rtol, 16, &it, &rr, &status,
+                              static_cast<cudaStream_t>(stream)))
+    s = fail(BSF_E_CUDA, "pcg failed");
+  if (prev != h->device) cudaSetDevice(prev);
+  if (s != BSF_OK) return s;
+  if (iters) *iters = it;
+  if (relres) *relres = rr;
+  if (status == 2) return fail(BSF_E_INVALID_ARG, "matrix not SPD (p.Hp <= 0 or a diagonal block not positive definite)");
+  return BSF_OK;
 }
 
 bsf_status bsf_eval_all_batch_host(bsf_handle h, int nbatch, const double* h_x, int64_t x_stride, double* d_x_stage,

@@ -1,0 +1,92 @@
+"""GPU: linear algebra on the assembled Hessian against the oracle's matrix.
+
+  bsf_bsr_spmv    vs scipy.sparse BSR product of the oracle's values (same pattern), 1e-13 relative
+  bsf_gershgorin  contains numpy's eigenvalues of the oracle's dense matrix (small sheet)
+  bsf_pcg         Newton step of the incremental potential: |b - Hx| <= rtol |b| re-measured on the host with
+                  the oracle's matrix, and the solution vs scipy's sparse direct solve
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+import oracle as O
+import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2506_18867_b200 as B  # noqa: E402
+
+
+def _bsr(o, vals, n_cols):
+    rp, ci = o.pattern()
+    return sp.bsr_matrix((np.asarray(vals), ci, rp), shape=(3 * (len(rp) - 1), 3 * n_cols)).tocsr()
+
+
+def _ip_system(sh, R0=0.15, dt=2e-3):
+    o = O.Oracle.from_sheet(sh)
+    m = o.lumped_mass(R0)
+    rng = np.random.default_rng(3)
+    xhat = sh.x + rng.normal(0, 1e-3, sh.x.shape)
+    E, g, v = o.eval_ip(sh.x, xhat, m, dt, (0, 0, -9.81), flags=O.FLAG_PROJECT)
+    return o, m, xhat, g, v
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "slab"])
+def test_spmv_matches_scipy(case):
+    sh = W.make_c1() if case == "c1" else W.make_c2(state=1)
+    r0, r1 = (30, 70) if case == "slab" else (0, sh.n_v)
+    o = O.Oracle.from_sheet(sh, r0=r0, r1=r1)
+    _, _, v = o.eval(sh.x, flags=O.FLAG_PROJECT)
+    s = B.Sheet.from_sheet(sh, row_begin=r0, row_end=r1)
+    rng = np.random.default_rng(9)
+    xv = rng.normal(size=(sh.n_v, sh.n_u, 3))
+    y = s.spmv(torch.from_numpy(v).cuda(), torch.from_numpy(np.ascontiguousarray(xv[s.x_row_begin:s.x_row_end])).cuda())
+    torch.cuda.synchronize()
+    ref = (_bsr(o, v, sh.n_u * sh.n_v) @ xv.reshape(-1)).reshape(r1 - r0, sh.n_u, 3)
+    assert np.max(np.abs(y.cpu().numpy() - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+def test_gershgorin_contains_spectrum():
+    sh = W.make_c1()
+    o, m, xhat, g, v = _ip_system(sh)
+    s = B.Sheet.from_sheet(sh)
+    lo, hi = s.gershgorin(torch.from_numpy(v).cuda())
+    lam = np.linalg.eigvalsh(_bsr(o, v, sh.n_u * sh.n_v).toarray())
+    assert lo <= lam.min() * (1 + 1e-12) and lam.max() <= hi * (1 + 1e-12)
+    # and the bound is a real Gershgorin bound (tight up to the disc radii): lo <= min diagonal entry
+    assert lo <= np.min(np.diag(_bsr(o, v, sh.n_u * sh.n_v).toarray()))
+
+
+@pytest.mark.parametrize("case", ["c1", "c2"])
+def test_pcg_newton_step(case):
+    sh = W.make_c1() if case == "c1" else W.make_c2(state=2)
+    o, m, xhat, g, v = _ip_system(sh)
+    s = B.Sheet.from_sheet(sh)
+    V = torch.from_numpy(v).cuda()
+    b = torch.from_numpy(-g).cuda()
+    x, it, rr = s.pcg(V, b, max_iter=2000, rtol=1e-11)
+    torch.cuda.synchronize()
+    A = _bsr(o, v, sh.n_u * sh.n_v)
+    xs = x.cpu().numpy().reshape(-1)
+    res = np.linalg.norm(-g.reshape(-1) - A @ xs) / np.linalg.norm(g)
+    assert rr <= 1e-11 and res <= 2e-11, (it, rr, res)
+    ref = spla.spsolve(A.tocsc(), -g.reshape(-1))
+    assert np.linalg.norm(xs - ref) <= 1e-8 * np.linalg.norm(ref), (it, np.linalg.norm(xs - ref) / np.linalg.norm(ref))
+    assert 0 < it < 2000
+
+
+def test_pcg_rejects_indefinite():
+    sh = W.make_c1()
+    o = O.Oracle.from_sheet(sh)
+    _, g, v = o.eval(sh.x)        # no projection, no inertia: singular / indefinite
+    v = v.copy()
+    rp, ci = o.pattern()
+    for a in range(len(rp) - 1):  # flip the sign of the diagonal blocks: certainly not SPD
+        for k in range(rp[a], rp[a + 1]):
+            if ci[k] == a:
+                v[k] = -np.eye(3)
+    s = B.Sheet.from_sheet(sh)
+    with pytest.raises(B.BsfError):
+        s.pcg(torch.from_numpy(v).cuda(), torch.from_numpy(np.ones_like(g)).cuda(), max_iter=50, rtol=1e-10)
