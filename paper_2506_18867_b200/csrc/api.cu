@@ -332,6 +332,11 @@ bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, doubl
   return BSF_OK;
 }
 
+static bool ip_epilogue_forced() {   // debug / comparison switch, read once
+  static const bool v = getenv("BSF_IP_EPILOGUE") != nullptr;
+  return v;
+}
+
 static bsf_status eval_batch_impl(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride, double* d_energy,
                                   double* d_grad, int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags,
                                   bsf_stream stream, const double* d_params, const bsf::IpFused* ip = nullptr) {
@@ -451,7 +456,7 @@ bsf_status bsf_eval_ip_batch(bsf_handle h, int nbatch, const double* d_x, int64_
   // fused into the core / band / corner kernels when that path runs (every affine REDUCED sheet), else an
   // epilogue pass after the assembly; the pinned elimination always runs after
   const bool fused = h->tile_ok && h->core_ok && h->ft.ok && !(flags & (BSF_TILE_ONLY | BSF_GENERIC_PATH)) &&
-                     !getenv("BSF_IP_EPILOGUE");
+                     !ip_epilogue_forced();
   bsf::IpFused ipf;
   ipf.xhat = d_xhat; ipf.xhs = xhat_stride; ipf.mass = h->d_mass; ipf.k = h->ip_k;
   for (int c = 0; c < 3; ++c) ipf.grav[c] = h->ip_g[c];

@@ -656,9 +656,9 @@ int band_eval(const BandTables& bt, const Sheet& sh, const double* d_x, int64_t 
   A.row_ptr = d_row_ptr; A.params = d_params;
   A.n_u = sh.n_u; A.xlo = sh.xlo; A.xhi = sh.xhi; A.r0 = sh.r0;
   A.project = (flags & 1) ? 1 : 0; A.flags = flags;
-  {
-    const char* e = getenv("BSF_CORE_DEBUG");   // profiling switches: 16 no points, 32 no gather
-    A.dbg = e ? atoi(e) : 0;
+  {   // profiling switches (read once per process): 16 no points, 32 no gather
+    static const int dbg = getenv("BSF_CORE_DEBUG") ? atoi(getenv("BSF_CORE_DEBUG")) : 0;
+    A.dbg = dbg;
   }
   A.G00 = G4[0]; A.G01 = G4[1]; A.G10 = G4[2]; A.G11 = G4[3]; A.detJ = detJ;
   A.mu1 = (flags & 2) ? 0.0 : mat.mu_st1;

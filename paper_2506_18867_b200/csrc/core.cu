@@ -863,9 +863,9 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
   A.n_u = sh.n_u; A.xlo = sh.xlo; A.xhi = sh.xhi; A.r0 = sh.r0;
   A.CI0 = ct.CI0; A.CI1 = ct.CI1; A.RJ0 = ct.RJ0; A.RJ1 = ct.RJ1; A.nstrips = ct.nstrips; A.nchunks = nchunks;
   A.project = (flags & 1) ? 1 : 0; A.flags = flags;
-  {
-    const char* e = getenv("BSF_CORE_DEBUG");   // profiling switches: 1 no points, 2 no gather, 4 no stores
-    A.dbg = e ? atoi(e) : 0;
+  {   // profiling switches (read once per process): 1 no points, 2 no gather, 4 no stores
+    static const int dbg = getenv("BSF_CORE_DEBUG") ? atoi(getenv("BSF_CORE_DEBUG")) : 0;
+    A.dbg = dbg;
   }
   A.G00 = ct.G[0]; A.G01 = ct.G[1]; A.G10 = ct.G[2]; A.G11 = ct.G[3]; A.detJ = ct.detJ;
   A.mu1 = (flags & 2) ? 0.0 : mat.mu_st1;

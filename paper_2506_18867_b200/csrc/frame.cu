@@ -523,9 +523,9 @@ int frame_eval(const FrameTables& ft, const Sheet& sh, const double* d_x, int64_
   A.n_u = sh.n_u; A.xlo = sh.xlo; A.xhi = sh.xhi; A.r0 = sh.r0;
   A.maxM = ft.maxM; A.maxB = ft.maxB;
   A.project = (flags & 1) ? 1 : 0; A.flags = flags;
-  {
-    const char* e = getenv("BSF_CORE_DEBUG");   // profiling switches: 16 no points, 32 no gather
-    A.dbg = e ? atoi(e) : 0;
+  {   // profiling switches (read once per process): 16 no points, 32 no gather
+    static const int dbg = getenv("BSF_CORE_DEBUG") ? atoi(getenv("BSF_CORE_DEBUG")) : 0;
+    A.dbg = dbg;
   }
   A.G00 = G4[0]; A.G01 = G4[1]; A.G10 = G4[2]; A.G11 = G4[3]; A.detJ = detJ;
   A.mu1 = (flags & 2) ? 0.0 : mat.mu_st1;
