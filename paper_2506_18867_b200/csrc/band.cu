@@ -264,7 +264,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
   // ---- 3. gather: warp task = (depth row, parity, channel group); lane = (channel k, along l)
   const int nd = t1 - t0, ntw = (A.dbg & 32) ? 0 : nd * 6;
   const int k4 = lane >> 3, l = lane & 7;
-  for (int wt = warp; wt < ntw; wt += kThreads / 32) {
+  for (int kt = 0; kt < 6 && ntw > 0; ++kt) {
+    const int wt = D.wtask[warp][kt];
+    if (wt == 255) break;
     const int td = wt / 6, pi = (wt / 3) & 1, grp = wt % 3;
     const int lc = grp * kLC + k4;                   // 0..8: block entry (r, c); 9..11: gradient component
     const int s = S0 + pi + 2 * l, t = t0 + td;
@@ -598,6 +600,24 @@ int build_band(const Sheet& sh, const CoreTables& ct, BandTables& bt, std::strin
       ent.resize(d.ent0);
       entd.resize(d.ent0);
       continue;
+    }
+    {   // gather tasks to warps: longest first onto the least loaded warp (cost ~ membrane entries + 1/3 bending)
+      const int nt = 6 * D;
+      std::vector<int> order(nt);
+      for (int k = 0; k < nt; ++k) order[k] = k;
+      auto cost = [&](int wt) { const int td = wt / 6, pi = (wt / 3) & 1; return 3 * d.ment[pi][td] + d.bent[pi][td]; };
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return cost(x) > cost(y); });
+      constexpr int nw = kThreads / 32;
+      int load[nw] = {}, cnt[nw] = {};
+      std::memset(d.wtask, 255, sizeof d.wtask);
+      for (int wt : order) {
+        int best = -1;
+        for (int w = 0; w < nw; ++w)
+          if (cnt[w] < 6 && (best < 0 || load[w] < load[best])) best = w;
+        if (best < 0) { okb = false; break; }
+        d.wtask[best][cnt[best]++] = (unsigned char)wt;
+        load[best] += cost(wt);
+      }
     }
     ent.push_back(0u);   // padding: the membrane loop prefetches two entries ahead
     ent.push_back(0u);

@@ -341,6 +341,7 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
   return 0.0;
 }
 
+template <bool IP>   // IP: the incremental-potential terms (compiled out of the elastic kernel)
 __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);   // [kRing][kRowD]
@@ -499,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
             }
             double* gdst = nullptr;
             const uint32_t par = k & 1;
-            const double dshift = (diag && A.xhat && active) ? A.ipk * A.mass[(int64_t)(jr - A.r0) * A.n_u + i] : 0.0;
+            const double dshift = (IP && diag && active) ? A.ipk * A.mass[(int64_t)(jr - A.r0) * A.n_u + i] : 0.0;
             if (PI == 0)
               gather_role<0>(base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
                              8 * (o_pv - o_uu), diag, cst, st_lane,
@@ -513,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
       }
       // (c') gradient rows of step k: the last two point warps (bending-only point work) take the 6
       // (parity, component) rounds
-      if (k >= 0 && (gout || A.xhat) && warp >= kThreads / 32 - 2 && !(A.dbg & 2)) {
+      if (k >= 0 && (gout || IP) && warp >= kThreads / 32 - 2 && !(A.dbg & 2)) {
         const int PI = warp - (kThreads / 32 - 2);
         const int jr = j + h;
         const int sigma = (PI + jr + i0) & 1;
@@ -543,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
             double* gdst = gout ? gout + al * 3 + r : nullptr;
             // incremental potential: m/dt^2 (x - xhat) - m g on the gradient, its energy on this lane
             double g0 = 0.0;
-            if (A.xhat) {
+            if constexpr (IP) {
               const double mm = A.mass[al], xa = x[((int64_t)(jr - A.xlo) * A.n_u + i) * 3 + r];
               const double d = xa - A.xhat[item * A.xhs + al * 3 + r], gr = A.grav[r];
               g0 = A.ipk * mm * d - mm * gr;
@@ -820,15 +821,16 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
   }
   ct.smem = sizeof(double) * ((size_t)kRing * kRowD + 2 * kStageRow + kPosD + kCstN) + 16;
   if (ct.smem > 227 * 1024) { err = "core: shared memory budget"; return -1; }
-  if (cudaFuncSetAttribute(k_core, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess) {
+  if (cudaFuncSetAttribute(k_core<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_core<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess) {
     cudaGetLastError();
     { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
   }
   if (getenv("BSF_CORE_DEBUG")) {
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k_core);
+    cudaFuncGetAttributes(&fa, k_core<false>);
     int nb = -1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_core, kThreads, ct.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_core<false>, kThreads, ct.smem);
     fprintf(stderr, "k_core: regs %d maxthreads %d local %zu static smem %zu dyn %zu maxdyn %d occ %d\n", fa.numRegs,
             fa.maxThreadsPerBlock, fa.localSizeBytes, fa.sharedSizeBytes, ct.smem, fa.maxDynamicSharedSizeBytes, nb);
   }
@@ -876,7 +878,8 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
   std::memcpy(A.what, ct.what, sizeof(A.what));
 
   dim3 grid(ct.nstrips, nchunks, nbatch);
-  k_core<<<grid, kThreads, ct.smem, st>>>(A);
+  if (A.xhat) k_core<true><<<grid, kThreads, ct.smem, st>>>(A);
+  else k_core<false><<<grid, kThreads, ct.smem, st>>>(A);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
 }
 

@@ -60,6 +60,8 @@ struct BandDesc {
   int ment[2][band::kMaxD], bent[2][band::kMaxD];   // entry counts
   unsigned char mcnt[2][band::kMaxD][9], bcnt[2][band::kMaxD][9];
   unsigned char rank[band::kMaxD][band::kSl];   // block rank of offset slot in the row, 255 = not in the pattern
+  unsigned char wtask[band::kThreads / 32][6];  // gather tasks (depth row * 6 + parity * 3 + group) of each warp,
+                                                // balanced by entry count on the host; 255 = none
 };
 
 struct BandTables {
