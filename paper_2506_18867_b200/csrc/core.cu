@@ -842,12 +842,21 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
 int core_ctas_per_item(const CoreTables& ct, int nchunks) { return ct.nstrips * nchunks; }
 
 int core_pick_chunks(const CoreTables& ct, int nbatch) {
-  // enough CTAs for ~4 waves of 148 SMs (1 CTA / SM), chunks of >= 16 rows
+  // row chunks per (strip, item): minimise (waves of 1 CTA per SM) x (rows per chunk + the 6-row prologue
+  // of a chunk); chunks of >= 16 rows.  The band / corner kernels run beside k_core and fill a partial
+  // last wave, so large batches prefer few long chunks and small ones many.
   const int rows = ct.RJ1 - ct.RJ0;
   const int per = std::max(1, ct.nstrips * std::max(1, nbatch));
-  int nch = (4 * 148 + per - 1) / per;
-  nch = std::min(nch, std::max(1, rows / 16));
-  return std::max(1, nch);
+  const int maxch = std::max(1, rows / 16);
+  int best = 1;
+  double bcost = 1e300;
+  for (int nch = 1; nch <= maxch; ++nch) {
+    const long long nctas = (long long)per * nch;
+    const long long waves = (nctas + 147) / 148;
+    const double cost = (double)waves * ((double)rows / nch + 6.0);
+    if (cost < bcost - 1e-9) { bcost = cost; best = nch; }
+  }
+  return best;
 }
 
 int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
