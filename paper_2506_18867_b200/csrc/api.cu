@@ -57,6 +57,7 @@ struct bsf_sheet {
   // linear algebra on the assembled Hessian (solve.cu)
   int32_t *d_rp = nullptr, *d_ci = nullptr, *d_sdiag = nullptr;
   bsf::CgWork cg{};
+  bsf::CgGraph cg_graph;
   bool solve_ready = false, cg_ready = false;
   std::vector<void*> allocs;
   int last_launches = 0;
@@ -72,6 +73,10 @@ struct bsf_sheet {
     if (ev_start) cudaEventDestroy(ev_start);
     if (tt.ev_fork) cudaEventDestroy(tt.ev_fork);
     if (tt.ev_join) cudaEventDestroy(tt.ev_join);
+    if (cg_graph.exec) cudaGraphExecDestroy(cg_graph.exec);
+    if (cg_graph.cs) cudaStreamDestroy(cg_graph.cs);
+    if (cg_graph.e0) cudaEventDestroy(cg_graph.e0);
+    if (cg_graph.e1) cudaEventDestroy(cg_graph.e1);
     for (StageUse& u : stage_uses) cudaEventDestroy(u.done);
     for (void* p : allocs) cudaFree(p);
     cudaSetDevice(prev);
@@ -518,6 +523,7 @@ static bsf_status solve_setup(bsf_handle h, bool cg, bsf::SolveArgs& A) {
     if (s == BSF_OK) s = h->alloc(&h->cg.S, (size_t)bsf::kSN);
     if (s == BSF_OK) s = h->alloc(&h->cg.bad, 1);
     if (s != BSF_OK) return s;
+    h->cg.graph = &h->cg_graph;
     h->cg_ready = true;
   }
   A.row_ptr = h->d_rp; A.col_idx = h->d_ci; A.diag = h->d_sdiag;

@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(kRedThreads) k_cg_scalar(int which, double* __
   S[kSRr] = rr;
   S[kSIter] += 1.0;
   if (rr <= rtol2 * S[kSBnorm2]) S[kSDone] = 1.0;
+  else if (S[kSIter] >= S[kSMaxIt]) S[kSDone] = 3.0;   // iteration budget spent
 }
 
 __global__ void __launch_bounds__(kVecThreads) k_dot(const double* __restrict__ u, const double* __restrict__ v, int64_t n,
@@ -211,10 +212,10 @@ __global__ void __launch_bounds__(kVecThreads) k_dot(const double* __restrict__ 
 }
 
 __global__ void __launch_bounds__(kRedThreads) k_set_bnorm(double* __restrict__ S, const double* __restrict__ part,
-                                                           int nparts) {
+                                                           int nparts, double max_iter) {
   __shared__ double sh[kRedThreads];
   const double s = block_sum(part, nparts, 1, 0, sh);
-  if (threadIdx.x == 0) S[kSBnorm2] = s;
+  if (threadIdx.x == 0) { S[kSBnorm2] = s; S[kSMaxIt] = max_iter; }
 }
 
 // r = b - r (r holds A x)
@@ -303,35 +304,66 @@ int pcg(const SolveArgs& A, const double* d_vals, const double* d_b, double* d_x
   k_diag_inv<<<(A.nrows + 127) / 128, 128, 0, st>>>(A.diag, d_vals, W.dinv, A.nrows, W.bad);
   // |b|^2
   k_dot<<<nbv, kVecThreads, 0, st>>>(d_b, d_b, n3, W.part);
-  k_set_bnorm<<<1, kRedThreads, 0, st>>>(W.S, W.part, nbv);
+  k_set_bnorm<<<1, kRedThreads, 0, st>>>(W.S, W.part, nbv, (double)max_iter);
   // r = b - A x, z = D^-1 r, p = z
   if (spmv(A, d_vals, d_x, W.r, nullptr, st)) return -6;
   k_residual<<<nbn, kVecThreads, 0, st>>>(d_b, W.r, n3);
   k_cg_update<<<nbv, kVecThreads, 0, st>>>(0, W.S, d_x, W.p, W.q, W.r, W.z, W.dinv, A.nrows, W.part);
   k_cg_scalar<<<1, kRedThreads, 0, st>>>(2, W.S, W.part, nbv, rtol * rtol);
   k_cg_dir<<<nbn, kVecThreads, 0, st>>>(0, W.S, W.z, W.p, n3);
-  double hs[kSN];
-  int it = 0;
-  *status = 0;
-  while (true) {
-    for (int k = 0; k < check_every && it < max_iter; ++k, ++it) {
-      if (spmv(A, d_vals, W.p, W.q, W.part, st)) return -6;   // q = A p, partials of p.q
-      k_cg_scalar<<<1, kRedThreads, 0, st>>>(0, W.S, W.part, nbs, rtol * rtol);
-      k_cg_update<<<nbv, kVecThreads, 0, st>>>(1, W.S, d_x, W.p, W.q, W.r, W.z, W.dinv, A.nrows, W.part);
-      k_cg_scalar<<<1, kRedThreads, 0, st>>>(1, W.S, W.part, nbv, rtol * rtol);
-      k_cg_dir<<<nbn, kVecThreads, 0, st>>>(1, W.S, W.z, W.p, n3);
+  // iterations in chunks of check_every, recorded once as a CUDA graph on an internal stream (one launch
+  // per chunk instead of 5 per iteration; after convergence or the budget the kernels return at once)
+  auto chunk = [&](cudaStream_t s) {
+    for (int k = 0; k < check_every; ++k) {
+      spmv(A, d_vals, W.p, W.q, W.part, s);   // q = A p, partials of p.q
+      k_cg_scalar<<<1, kRedThreads, 0, s>>>(0, W.S, W.part, nbs, rtol * rtol);
+      k_cg_update<<<nbv, kVecThreads, 0, s>>>(1, W.S, d_x, W.p, W.q, W.r, W.z, W.dinv, A.nrows, W.part);
+      k_cg_scalar<<<1, kRedThreads, 0, s>>>(1, W.S, W.part, nbv, rtol * rtol);
+      k_cg_dir<<<nbn, kVecThreads, 0, s>>>(1, W.S, W.z, W.p, n3);
     }
-    if (cudaPeekAtLastError() != cudaSuccess) return -6;
-    if (cudaMemcpyAsync(hs, W.S, sizeof(hs), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
-        cudaStreamSynchronize(st) != cudaSuccess)
+  };
+  CgGraph* Gr = W.graph;
+  cudaStream_t run = st;
+  if (Gr) {
+    if (!Gr->cs && (cudaStreamCreateWithFlags(&Gr->cs, cudaStreamNonBlocking) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&Gr->e0, cudaEventDisableTiming) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&Gr->e1, cudaEventDisableTiming) != cudaSuccess))
       return -6;
-    if (hs[kSDone] != 0.0 || it >= max_iter) break;
+    const bool same = Gr->exec && Gr->key[0] == d_vals && Gr->key[1] == d_b && Gr->key[2] == d_x &&
+                      Gr->key_rtol == rtol && Gr->key_max == check_every;
+    if (!same) {
+      if (Gr->exec) { cudaGraphExecDestroy(Gr->exec); Gr->exec = nullptr; }
+      cudaGraph_t g = nullptr;
+      if (cudaStreamBeginCapture(Gr->cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return -6;
+      chunk(Gr->cs);
+      if (cudaStreamEndCapture(Gr->cs, &g) != cudaSuccess) return -6;
+      const cudaError_t ie = cudaGraphInstantiate(&Gr->exec, g, 0);
+      cudaGraphDestroy(g);
+      if (ie != cudaSuccess) { Gr->exec = nullptr; return -6; }
+      Gr->key[0] = d_vals; Gr->key[1] = d_b; Gr->key[2] = d_x; Gr->key_rtol = rtol; Gr->key_max = check_every;
+    }
+    if (cudaEventRecord(Gr->e0, st) != cudaSuccess || cudaStreamWaitEvent(Gr->cs, Gr->e0, 0) != cudaSuccess) return -6;
+    run = Gr->cs;
   }
+  double hs[kSN];
+  *status = 0;
+  for (int it = 0;; it += check_every) {
+    if (Gr) { if (cudaGraphLaunch(Gr->exec, run) != cudaSuccess) return -6; }
+    else chunk(run);
+    if (cudaPeekAtLastError() != cudaSuccess) return -6;
+    if (cudaMemcpyAsync(hs, W.S, sizeof(hs), cudaMemcpyDeviceToHost, run) != cudaSuccess ||
+        cudaStreamSynchronize(run) != cudaSuccess)
+      return -6;
+    if (hs[kSDone] != 0.0 || it + check_every >= max_iter) break;
+  }
+  if (Gr && (cudaEventRecord(Gr->e1, run) != cudaSuccess || cudaStreamWaitEvent(st, Gr->e1, 0) != cudaSuccess))
+    return -6;
   int bad = 0;
   cudaMemcpy(&bad, W.bad, sizeof(int), cudaMemcpyDeviceToHost);
   *iters = (int)hs[kSIter];
   *relres = hs[kSBnorm2] > 0.0 ? std::sqrt(hs[kSRr] / hs[kSBnorm2]) : 0.0;
-  *status = hs[kSDone] == 1.0 ? 0 : (hs[kSDone] == 2.0 || bad ? 2 : 1);   // 0 converged, 1 max_iter, 2 not SPD
+  // 0 converged, 1 iteration budget spent, 2 not SPD
+  *status = hs[kSDone] == 1.0 ? 0 : ((hs[kSDone] == 2.0 || bad) ? 2 : 1);
   return 0;
 }
 

@@ -15,9 +15,20 @@ struct SolveArgs {
 };
 
 // device scalar slots of the PCG
-enum { kSRz = 0, kSRr, kSRr0, kSAlpha, kSBeta, kSDone, kSIter, kSBnorm2, kSN };
+enum { kSRz = 0, kSRr, kSRr0, kSAlpha, kSBeta, kSDone, kSIter, kSBnorm2, kSMaxIt, kSN };
+
+// CUDA graph of a chunk of PCG iterations (replayed until convergence; rebuilt when the operands change)
+struct CgGraph {
+  cudaStream_t cs = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  const void* key[3] = {nullptr, nullptr, nullptr};
+  double key_rtol = 0.0;
+  int key_max = 0;
+};
 
 struct CgWork {
+  CgGraph* graph = nullptr;   // owned by the handle
   double *r, *z, *p, *q;   // [3 nrows] each
   double* dinv;            // [nrows][9]
   double* part;            // [solve_parts(nrows)] partial sums
