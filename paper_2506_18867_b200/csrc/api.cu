@@ -51,6 +51,7 @@ struct bsf_sheet {
   std::vector<double> h_mass;
   double* d_mass = nullptr;
   int32_t *d_diag = nullptr, *d_zero = nullptr, *d_pin = nullptr;
+  size_t cap_mass = 0, cap_diag = 0, cap_zero = 0, cap_pin = 0;
   int nzero = 0, npin = 0;
   double* d_ip_epart = nullptr;
   int64_t ip_epart_cap = 0;
@@ -91,6 +92,19 @@ struct bsf_sheet {
     if (cudaMemcpy(p, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
       return fail(BSF_E_CUDA, "cudaMemcpy failed");
     *dst = static_cast<T*>(p);
+    return BSF_OK;
+  }
+  // upload into an existing allocation when it is large enough (set_inertia may be called every step)
+  template <class T>
+  bsf_status upload_reuse(T** dst, size_t* cap, const std::vector<T>& src) {
+    if (src.empty()) return BSF_OK;
+    if (!*dst || *cap < src.size()) {
+      bsf_status s = upload(dst, src);
+      if (s == BSF_OK) *cap = src.size();
+      return s;
+    }
+    if (cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(BSF_E_CUDA, "cudaMemcpy failed");
     return BSF_OK;
   }
   std::function<void*(size_t)> dalloc() {
@@ -427,10 +441,15 @@ bsf_status bsf_set_inertia(bsf_handle h, double areal_density, double dt, const 
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != h->device) cudaSetDevice(h->device);
-    bsf_status s = h->upload(&h->d_mass, m);
-    if (s == BSF_OK) s = h->upload(&h->d_diag, diag);
-    if (s == BSF_OK) s = h->upload(&h->d_zero, zero);
-    if (s == BSF_OK) s = h->upload(&h->d_pin, pin);
+    // in-flight calls may still read the previous tables: finish them before overwriting in place
+    if (h->ip_set && cudaDeviceSynchronize() != cudaSuccess) {
+      if (prev != h->device) cudaSetDevice(prev);
+      return fail(BSF_E_CUDA, "device synchronisation failed");
+    }
+    bsf_status s = h->upload_reuse(&h->d_mass, &h->cap_mass, m);
+    if (s == BSF_OK) s = h->upload_reuse(&h->d_diag, &h->cap_diag, diag);
+    if (s == BSF_OK) s = h->upload_reuse(&h->d_zero, &h->cap_zero, zero);
+    if (s == BSF_OK) s = h->upload_reuse(&h->d_pin, &h->cap_pin, pin);
     if (prev != h->device) cudaSetDevice(prev);
     if (s != BSF_OK) return s;
   }

@@ -354,3 +354,30 @@ def test_cuda_graph_capture_and_replay():
     s.eval_all_batch(X, E2, G2, V2, B.PROJECT_PSD)
     torch.cuda.synchronize()
     assert torch.equal(G, G2) and torch.equal(V, V2) and torch.equal(E, E2)
+
+
+def test_set_inertia_repeated_reuses_tables():
+    """bsf_set_inertia called again (new dt, gravity, pinned set) updates the tables in place; results follow
+    the latest settings."""
+    sh = W.make_c1()
+    s = B.Sheet.from_sheet(sh)
+    o = O.Oracle.from_sheet(sh)
+    X = torch.from_numpy(sh.x).cuda().unsqueeze(0)
+    XH = X + 1e-3
+    for dt, pin_rows in [(1e-2, [15]), (3e-3, []), (5e-3, [0, 15])]:
+        pinned = np.zeros((sh.n_v, sh.n_u), bool)
+        pinned[pin_rows, :] = True
+        s.set_inertia(0.3, dt, gravity=(0, -1.0, 0), pinned=pinned if pin_rows else None)
+        E = torch.zeros(1, dtype=torch.float64, device="cuda")
+        G = torch.zeros_like(X)
+        V = torch.zeros((1, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+        s.eval_ip_batch(X, XH, E, G, V, flags=B.PROJECT_PSD)
+        torch.cuda.synchronize()
+        m = o.lumped_mass(0.3)
+        Er, gr, vr = o.eval_ip(sh.x, XH[0].cpu().numpy(), m, dt, (0, -1.0, 0), pinned if pin_rows else None,
+                               flags=O.FLAG_PROJECT)
+        rp, ci = o.pattern()
+        assert_parity(E.item(), G[0].cpu().numpy(), V[0].cpu().numpy(), Er, gr, vr, what=f"dt={dt}",
+                      hdiag=diag_block_norms(vr, rp, ci, 0, sh.n_u), cmax=np.abs(sh.x).max(),
+                      vabs=o.eval_ip(sh.x, XH[0].cpu().numpy(), m, dt, (0, -1.0, 0), pinned if pin_rows else None,
+                                     flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2])
