@@ -223,6 +223,14 @@ bsf_status bsf_nccl_comm_destroy(void* comm);
 bsf_status bsf_halo_exchange(bsf_handle h, double* d_x, void* nccl_comm, int rank, int nranks,
                              bsf_stream stream);
 
+/* Halo exchange overlapped with the assembly (SURVEY §8(e) "Overlap"): the exchange runs on an internal
+ * stream while the core kernel assembles the rows [r0+4, r1-4) that need no halo (a row's gather reads
+ * control-point rows j-4 .. j+3); the remaining core rows, the bands and the corners wait for it.  Outputs
+ * as bsf_eval_all (the slab's energy; sum it over ranks with bsf_allreduce_sum).  nranks == 1: no exchange
+ * (nccl_comm may be NULL).  Falls back to exchange-then-assemble when the core path does not apply. */
+bsf_status bsf_eval_all_slab(bsf_handle h, double* d_x, void* nccl_comm, int rank, int nranks, double* d_energy,
+                             double* d_grad, double* d_vals, int flags, bsf_stream stream);
+
 /* In-place sum all-reduce of n doubles (the slab energies) over the communicator. */
 bsf_status bsf_allreduce_sum(double* d_buf, int64_t n, void* nccl_comm, bsf_stream stream);
 

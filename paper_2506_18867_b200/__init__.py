@@ -30,6 +30,7 @@ SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_mate
            "bsf_halo_exchange", "bsf_nccl_get_unique_id", "bsf_nccl_comm_init", "bsf_nccl_comm_destroy",
            "bsf_allreduce_sum", "bsf_get_core_rect", "bsf_eval_all_batch_host", "bsf_set_inertia",
            "bsf_get_lumped_mass", "bsf_eval_ip_batch", "bsf_bsr_spmv", "bsf_gershgorin", "bsf_pcg",
+           "bsf_eval_all_slab",
            "bsf_last_launch_count", "bsf_last_error"]
 
 
@@ -87,6 +88,7 @@ def lib():
         L.bsf_get_lumped_mass.argtypes = [vp, dp]
         L.bsf_eval_ip_batch.argtypes = [vp, C.c_int, vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, vp, C.c_int64,
                                         C.c_int, vp]
+        L.bsf_eval_all_slab.argtypes = [vp, vp, vp, C.c_int, C.c_int, vp, vp, vp, C.c_int, vp]
         L.bsf_bsr_spmv.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_gershgorin.argtypes = [vp, vp, dp, dp, vp]
         L.bsf_pcg.argtypes = [vp, vp, vp, vp, C.c_int, C.c_double, C.POINTER(C.c_int), dp, vp]
@@ -261,6 +263,12 @@ class Sheet:
         vs = vals[0].numel() if vals is not None else 0
         _check(lib().bsf_eval_ip_batch(self._h, int(B), _ptr(x), x[0].numel(), _ptr(xhat), xhat[0].numel(),
                                        _ptr(energy), _ptr(grad), gs, _ptr(vals), vs, int(flags), _stream(stream)))
+
+    def eval_all_slab(self, x, energy=None, grad=None, vals=None, comm=None, rank=0, nranks=1, flags=0, stream=None):
+        """Halo exchange (NCCL communicator handle `comm`, nranks > 1) overlapped with the assembly of the
+        interior rows; outputs as eval_all."""
+        _check(lib().bsf_eval_all_slab(self._h, _ptr(x), comm, int(rank), int(nranks), _ptr(energy), _ptr(grad),
+                                       _ptr(vals), int(flags), _stream(stream)))
 
     def spmv(self, vals, x, y=None, stream=None):
         """y = H x with the BSR values `vals` [nnzb, 3, 3]; x in the position layout (x_shape()), y [rows, n_u, 3]."""

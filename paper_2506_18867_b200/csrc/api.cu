@@ -59,6 +59,8 @@ struct bsf_sheet {
   int32_t *d_rp = nullptr, *d_ci = nullptr, *d_sdiag = nullptr;
   bsf::CgWork cg{};
   bsf::CgGraph cg_graph;
+  cudaStream_t comm_stream = nullptr;   // bsf_eval_all_slab: halo exchange
+  cudaEvent_t ev_halo0 = nullptr, ev_halo = nullptr;
   bool solve_ready = false, cg_ready = false;
   std::vector<void*> allocs;
   int last_launches = 0;
@@ -74,6 +76,9 @@ struct bsf_sheet {
     if (ev_start) cudaEventDestroy(ev_start);
     if (tt.ev_fork) cudaEventDestroy(tt.ev_fork);
     if (tt.ev_join) cudaEventDestroy(tt.ev_join);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
+    if (ev_halo0) cudaEventDestroy(ev_halo0);
+    if (ev_halo) cudaEventDestroy(ev_halo);
     if (cg_graph.exec) cudaGraphExecDestroy(cg_graph.exec);
     if (cg_graph.cs) cudaStreamDestroy(cg_graph.cs);
     if (cg_graph.e0) cudaEventDestroy(cg_graph.e0);
@@ -750,6 +755,73 @@ extern "C" bsf_status bsf_halo_exchange(bsf_handle h, double* d_x, void* nccl_co
   std::string err;
   const int rc = bsf::nccl_halo_exchange(d_x, sh.n_u, sh.r0, sh.r1, sh.xlo, sh.xhi, rank, nranks, nccl_comm, stream, err);
   return rc ? fail(BSF_E_NCCL, err) : BSF_OK;
+}
+
+extern "C" bsf_status bsf_eval_all_slab(bsf_handle h, double* d_x, void* nccl_comm, int rank, int nranks,
+                                        double* d_energy, double* d_grad, double* d_vals, int flags,
+                                        bsf_stream stream) {
+  if (!h || !d_x || rank < 0 || rank >= nranks) return fail(BSF_E_INVALID_ARG, "bad slab arguments");
+  if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle");
+  if (flags & ~31) return fail(BSF_E_INVALID_ARG, "unknown flag bits");
+  const bsf::Sheet& sh = h->sh;
+  const bool exchange = nranks > 1;
+  if (exchange && !nccl_comm) return fail(BSF_E_INVALID_ARG, "null communicator");
+  if (exchange && sh.r1 - sh.r0 < 2) return fail(BSF_E_INVALID_ARG, "every slab must own at least 2 rows");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  auto st = static_cast<cudaStream_t>(stream);
+  bsf_status s = BSF_OK;
+  const bool fused = h->tile_ok && h->core_ok && h->ft.ok && !(flags & (BSF_TILE_ONLY | BSF_GENERIC_PATH));
+  // interior core rows: the gather of row j reads control-point rows j-4 .. j+3 (knot-row pairs of the
+  // prologue), so rows [r0+4, r1-4) need no halo; the boundary rows wait for the exchange
+  bsf::HaloOverlap ov{0, 0, nullptr};
+  static const bool force_split = getenv("BSF_SLAB_SPLIT") != nullptr;   // test switch: split without exchange
+  if (fused && (exchange || force_split)) {
+    ov.ja = std::max(h->ct.RJ0, rank > 0 ? sh.r0 + 4 : h->ct.RJ0);
+    ov.jb = std::min(h->ct.RJ1, rank < nranks - 1 ? sh.r1 - 4 : h->ct.RJ1);
+  }
+  if (!exchange && ov.jb > ov.ja) {   // forced split on one rank: `ready` is an already-reached point of st
+    if (!h->ev_halo && cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming) != cudaSuccess)
+      s = fail(BSF_E_CUDA, "event");
+    if (s == BSF_OK && cudaEventRecord(h->ev_halo, st) != cudaSuccess) s = fail(BSF_E_CUDA, "event");
+    ov.ready = h->ev_halo;
+    ov.ja = std::max(h->ct.RJ0, sh.r0 + 4);
+    ov.jb = std::min(h->ct.RJ1, sh.r1 - 4);
+  }
+  if (exchange) {
+    if (!h->comm_stream &&
+        (cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+         cudaEventCreateWithFlags(&h->ev_halo0, cudaEventDisableTiming) != cudaSuccess ||
+         cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming) != cudaSuccess))
+      s = fail(BSF_E_CUDA, "stream creation failed");
+    std::string err;
+    if (s == BSF_OK && (cudaEventRecord(h->ev_halo0, st) != cudaSuccess ||
+                        cudaStreamWaitEvent(h->comm_stream, h->ev_halo0, 0) != cudaSuccess))
+      s = fail(BSF_E_CUDA, "event");
+    if (s == BSF_OK && bsf::nccl_halo_exchange(d_x, sh.n_u, sh.r0, sh.r1, sh.xlo, sh.xhi, rank, nranks, nccl_comm,
+                                               h->comm_stream, err))
+      s = fail(BSF_E_NCCL, err);
+    if (s == BSF_OK && cudaEventRecord(h->ev_halo, h->comm_stream) != cudaSuccess) s = fail(BSF_E_CUDA, "event");
+    ov.ready = h->ev_halo;
+    if (s == BSF_OK && !(ov.jb > ov.ja) && cudaStreamWaitEvent(st, h->ev_halo, 0) != cudaSuccess)   // no overlap
+      s = fail(BSF_E_CUDA, "event");
+  }
+  int nl = 0;
+  if (s == BSF_OK) {
+    int rc;
+    if (h->tile_ok && !(flags & BSF_GENERIC_PATH))
+      rc = bsf::tile_eval(h->tt, sh, d_x, 0, h->mat, flags, 1, d_energy, d_grad, 0, d_vals, 0, st, &nl, h->dalloc(),
+                          nullptr, (h->core_ok && !(flags & BSF_TILE_ONLY)) ? &h->ct : nullptr, &h->ft, nullptr,
+                          (ov.jb > ov.ja) ? &ov : nullptr);
+    else
+      rc = bsf::generic_eval(h->gt, d_x, h->mat, flags, (int64_t)sh.col_idx.size(), (int64_t)(sh.r1 - sh.r0) * sh.n_u,
+                             d_energy, d_grad, d_vals, st, &nl);
+    if (rc) s = check_cuda("kernel launch") == BSF_OK ? fail(BSF_E_CUDA, "launch failed") : BSF_E_CUDA;
+  }
+  h->last_launches = nl;
+  if (prev != h->device) cudaSetDevice(prev);
+  return s;
 }
 
 extern "C" bsf_status bsf_allreduce_sum(double* d_buf, int64_t n, void* nccl_comm, bsf_stream stream) {

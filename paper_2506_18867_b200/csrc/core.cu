@@ -53,6 +53,7 @@ struct CoreArgs {
   const double* params;
   int n_u, xlo, xhi, r0;
   int CI0, CI1, RJ0, RJ1, nstrips, nchunks;
+  int JA, JB;              // rows of this launch ([RJ0, RJ1) or a sub-range; addressing stays relative to RJ0)
   int project, flags, dbg;
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
   const double* tabs;      // device [104]: S[4][9][2] | LA[9] | LB[9] | LC[9] | what[5]
@@ -353,9 +354,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
   CT_MARK(TK0);
   const int strip = blockIdx.x, chunk = blockIdx.y, item = blockIdx.z;
   const int i0 = A.CI0 + strip * kW, i1 = min(i0 + kW, A.CI1);
-  const int nsteps = (A.RJ1 - A.RJ0 + kRows - 1) / kRows;
+  const int nsteps = (A.JB - A.JA + kRows - 1) / kRows;
   const int sa = chunk * nsteps / A.nchunks, sb = (chunk + 1) * nsteps / A.nchunks;
-  const int ja = A.RJ0 + kRows * sa, jb = min(A.RJ0 + kRows * sb, A.RJ1);
+  const int ja = A.JA + kRows * sa, jb = min(A.JA + kRows * sb, A.JB);
   const double* __restrict__ x = A.x + item * A.xs;
   double* vals = A.vals ? A.vals + item * A.vs : nullptr;
   double* gout = A.g ? A.g + item * A.gs : nullptr;
@@ -841,11 +842,11 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
 
 int core_ctas_per_item(const CoreTables& ct, int nchunks) { return ct.nstrips * nchunks; }
 
-int core_pick_chunks(const CoreTables& ct, int nbatch) {
+int core_pick_chunks(const CoreTables& ct, int nbatch, int rows_override) {
   // row chunks per (strip, item): minimise (waves of 1 CTA per SM) x (rows per chunk + the 6-row prologue
   // of a chunk); chunks of >= 16 rows.  The band / corner kernels run beside k_core and fill a partial
   // last wave, so large batches prefer few long chunks and small ones many.
-  const int rows = ct.RJ1 - ct.RJ0;
+  const int rows = rows_override >= 0 ? rows_override : ct.RJ1 - ct.RJ0;
   const int per = std::max(1, ct.nstrips * std::max(1, nbatch));
   const int maxch = std::max(1, rows / 16);
   int best = 1;
@@ -862,9 +863,12 @@ int core_pick_chunks(const CoreTables& ct, int nbatch) {
 int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride, double* e_part,
               int64_t e_stride, int64_t e_off, int nchunks, const double* d_params, double detJ_ref,
-              cudaStream_t st, const IpFused* ip) {
+              cudaStream_t st, const IpFused* ip, int row_begin, int row_end) {
   (void)detJ_ref;
   CoreArgs A;
+  A.JA = row_begin >= 0 ? row_begin : ct.RJ0;
+  A.JB = row_end >= 0 ? row_end : ct.RJ1;
+  if (A.JB <= A.JA) return 0;
   A.xhat = ip ? ip->xhat : nullptr; A.xhs = ip ? ip->xhs : 0; A.mass = ip ? ip->mass : nullptr;
   A.ipk = ip ? ip->k : 0.0;
   for (int c = 0; c < 3; ++c) A.grav[c] = ip ? ip->grav[c] : 0.0;

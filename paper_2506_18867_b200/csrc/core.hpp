@@ -165,9 +165,9 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
 int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride, double* e_part,
               int64_t e_stride, int64_t e_off, int nchunks, const double* d_params, double detJ_ref,
-              cudaStream_t st, const struct IpFused* ip = nullptr);
+              cudaStream_t st, const struct IpFused* ip = nullptr, int row_begin = -1, int row_end = -1);
 
 int core_ctas_per_item(const CoreTables& ct, int nchunks);
-int core_pick_chunks(const CoreTables& ct, int nbatch);
+int core_pick_chunks(const CoreTables& ct, int nbatch, int rows = -1);
 
 }  // namespace bsf

@@ -890,15 +890,20 @@ int tile_set_core(TileTables& tt, const Sheet& sh, const CoreTables& ct, const s
 int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stride, const Mat& mat, int flags,
               int nbatch, double* d_E, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride,
               cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc, const double* d_params,
-              const CoreTables* ct, const FrameTables* ft, const IpFused* ip) {
+              const CoreTables* ct, const FrameTables* ft, const IpFused* ip, const HaloOverlap* halo) {
   const bool core = ct && tt.core && ct->ok;
   if (ip && !(core && ft && ft->ok)) return -1;   // the fused incremental potential needs core + band + corners
   if (core && ft && ft->ok) {
     // frame kernel (full frame rows) + core kernel (full core rows): disjoint rows, one energy array
     // [item][frame tiles | core CTAs]; every slot is written on every call
-    const int core_nch = core_pick_chunks(*ct, nbatch);
+    // halo overlap: the interior core rows [ja, jb) first (own chunking), then the two boundary row
+    // ranges with one chunk each; energy slots [frame tiles | band CTAs | core CTAs of each launch]
+    const bool ov = halo && halo->jb > halo->ja && halo->ja >= ct->RJ0 && halo->jb <= ct->RJ1;
+    const int core_nch = ov ? core_pick_chunks(*ct, nbatch, halo->jb - halo->ja) : core_pick_chunks(*ct, nbatch);
     const int64_t nfb = ft->ntiles + ft->band.nctas;   // energy slots: [frame tiles | band CTAs | core CTAs]
-    const int64_t e_stride = nfb + core_ctas_per_item(*ct, core_nch);
+    const int64_t nb_lo = (ov && halo->ja > ct->RJ0) ? core_ctas_per_item(*ct, 1) : 0;   // boundary launches
+    const int64_t nb_hi = (ov && halo->jb < ct->RJ1) ? core_ctas_per_item(*ct, 1) : 0;
+    const int64_t e_stride = nfb + core_ctas_per_item(*ct, core_nch) + nb_lo + nb_hi;
     const int64_t need = (int64_t)nbatch * e_stride;
     if (need > tt.e_cap) {
       void* p = dalloc(need * sizeof(double));
@@ -914,16 +919,32 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
           cudaEventCreateWithFlags(&tt.ev_join, cudaEventDisableTiming) != cudaSuccess)
         return -6;
     }
+    int rc = 0;
+    if (ov) {   // interior rows while the halo is in flight, then wait for it
+      rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
+                     nfb, core_nch, d_params, tt.detJ_ref, st, ip, halo->ja, halo->jb);
+      if (rc) return rc;
+      if (cudaStreamWaitEvent(st, halo->ready, 0) != cudaSuccess) return -6;
+    }
     if (cudaEventRecord(tt.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(tt.side, tt.ev_fork, 0) != cudaSuccess)
       return -6;
-    int rc = frame_eval(*ft, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
+    rc = frame_eval(*ft, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
                         tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, tt.side, ip);
     if (rc) return rc;
     rc = band_eval(ft->band, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
                    tt.e_part, e_stride, ft->ntiles, d_params, ct->G, ct->detJ, tt.side, ip);
     if (rc) return rc;
-    rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
-                   nfb, core_nch, d_params, tt.detJ_ref, st, ip);
+    if (ov) {
+      const int64_t o1 = nfb + core_ctas_per_item(*ct, core_nch), o2 = o1 + nb_lo;
+      rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
+                     o1, 1, d_params, tt.detJ_ref, st, ip, ct->RJ0, halo->ja);
+      if (rc) return rc;
+      rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
+                     o2, 1, d_params, tt.detJ_ref, st, ip, halo->jb, ct->RJ1);
+    } else {
+      rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
+                     nfb, core_nch, d_params, tt.detJ_ref, st, ip);
+    }
     if (rc) return rc;
     if (cudaEventRecord(tt.ev_join, tt.side) != cudaSuccess || cudaStreamWaitEvent(st, tt.ev_join, 0) != cudaSuccess)
       return -6;

@@ -74,6 +74,15 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
               int nbatch, double* d_E, double* d_g, int64_t g_stride, double* d_vals, int64_t v_stride,
               cudaStream_t st, int* launches, const std::function<void*(size_t)>& dalloc,
               const double* d_params = nullptr, const CoreTables* ct = nullptr,
-              const struct FrameTables* ft = nullptr, const struct IpFused* ip = nullptr);
+              const struct FrameTables* ft = nullptr, const struct IpFused* ip = nullptr,
+              const struct HaloOverlap* halo = nullptr);
+
+// Overlap of the slab halo exchange with the assembly: the core rows [ja, jb), which read
+// owned positions only, are launched first; `ready` (recorded after the exchange on another stream) is
+// waited for before every launch that reads halo rows (the remaining core rows, bands, corners).
+struct HaloOverlap {
+  int ja, jb;
+  cudaEvent_t ready;
+};
 
 }  // namespace bsf

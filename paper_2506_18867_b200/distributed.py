@@ -118,8 +118,13 @@ class SlabSheet:
     def assemble(self, flags=1, stream=None, reduce_energy=True):
         """Halo exchange, local fused assembly, energy all-reduce.  Returns (E_total[1], g, vals)."""
         from . import _check, _stream, lib
-        self.exchange(stream)
-        self.h.eval_all(self.x, self.E, self.g, self.v, flags, stream)
+        if self.comm is not None or self.world == 1:
+            # library communicator: the exchange overlaps the assembly of the interior rows (SURVEY §8(e))
+            self.h.eval_all_slab(self.x, self.E, self.g, self.v, comm=self.comm.comm if self.comm else None,
+                                 rank=self.rank, nranks=self.world, flags=flags, stream=stream)
+        else:
+            self.exchange(stream)
+            self.h.eval_all(self.x, self.E, self.g, self.v, flags, stream)
         if reduce_energy and self.world > 1:
             if self.comm is not None:
                 _check(lib().bsf_allreduce_sum(C.c_void_p(self.E.data_ptr()), 1, self.comm.comm, _stream(stream)))
