@@ -239,6 +239,14 @@ bsf_status bsf_allreduce_sum(double* d_buf, int64_t n, void* nccl_comm, bsf_stre
  * rest shape, non-REDUCED rules, small sheet, host-only handle).  Host call, no device work. */
 bsf_status bsf_get_core_rect(bsf_handle h, int32_t* rect4);
 
+/* Live per-kernel timing for the roofline of the dominant kernel (bench.py): with ncalls > 0 every
+ * following call on the core + band path records CUDA events around the k_core launch (on the caller's
+ * stream) and the k_band launch (on the side stream), in a ring of the last ncalls calls; ncalls = 0 turns
+ * it off.  bsf_get_kernel_timing synchronises on those events and writes the durations in ms of the last
+ * min(n, recorded) calls, oldest first (either pointer may be NULL); returns the count. */
+bsf_status bsf_set_kernel_timing(bsf_handle h, int ncalls);
+int bsf_get_kernel_timing(bsf_handle h, float* core_ms, float* band_ms, int n);
+
 /* Number of kernel launches the most recent compute call enqueued (for the bench's claim). */
 int bsf_last_launch_count(bsf_handle h);
 

@@ -30,7 +30,7 @@ SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_mate
            "bsf_halo_exchange", "bsf_nccl_get_unique_id", "bsf_nccl_comm_init", "bsf_nccl_comm_destroy",
            "bsf_allreduce_sum", "bsf_get_core_rect", "bsf_eval_all_batch_host", "bsf_set_inertia",
            "bsf_get_lumped_mass", "bsf_eval_ip_batch", "bsf_bsr_spmv", "bsf_gershgorin", "bsf_pcg",
-           "bsf_eval_all_slab",
+           "bsf_eval_all_slab", "bsf_set_kernel_timing", "bsf_get_kernel_timing",
            "bsf_last_launch_count", "bsf_last_error"]
 
 
@@ -88,6 +88,8 @@ def lib():
         L.bsf_get_lumped_mass.argtypes = [vp, dp]
         L.bsf_eval_ip_batch.argtypes = [vp, C.c_int, vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, vp, C.c_int64,
                                         C.c_int, vp]
+        L.bsf_set_kernel_timing.argtypes = [vp, C.c_int]
+        L.bsf_get_kernel_timing.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_float), C.c_int]
         L.bsf_eval_all_slab.argtypes = [vp, vp, vp, C.c_int, C.c_int, vp, vp, vp, C.c_int, vp]
         L.bsf_bsr_spmv.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_gershgorin.argtypes = [vp, vp, dp, dp, vp]
@@ -269,6 +271,16 @@ class Sheet:
         interior rows; outputs as eval_all."""
         _check(lib().bsf_eval_all_slab(self._h, _ptr(x), comm, int(rank), int(nranks), _ptr(energy), _ptr(grad),
                                        _ptr(vals), int(flags), _stream(stream)))
+
+    def set_kernel_timing(self, ncalls):
+        """Record CUDA events around k_core / k_band in each of the next calls (ring of `ncalls`)."""
+        _check(lib().bsf_set_kernel_timing(self._h, int(ncalls)))
+
+    def kernel_timing(self, n):
+        """(core_ms, band_ms) lists of the last min(n, recorded) calls (synchronises)."""
+        c, b = (C.c_float * max(n, 1))(), (C.c_float * max(n, 1))()
+        k = lib().bsf_get_kernel_timing(self._h, c, b, int(n))
+        return list(c[:k]), list(b[:k])
 
     def spmv(self, vals, x, y=None, stream=None):
         """y = H x with the BSR values `vals` [nnzb, 3, 3]; x in the position layout (x_shape()), y [rows, n_u, 3]."""

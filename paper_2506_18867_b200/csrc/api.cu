@@ -84,6 +84,7 @@ struct bsf_sheet {
     if (cg_graph.e0) cudaEventDestroy(cg_graph.e0);
     if (cg_graph.e1) cudaEventDestroy(cg_graph.e1);
     for (StageUse& u : stage_uses) cudaEventDestroy(u.done);
+    for (cudaEvent_t e : tt.tev) cudaEventDestroy(e);
     for (void* p : allocs) cudaFree(p);
     cudaSetDevice(prev);
   }
@@ -822,6 +823,43 @@ extern "C" bsf_status bsf_eval_all_slab(bsf_handle h, double* d_x, void* nccl_co
   h->last_launches = nl;
   if (prev != h->device) cudaSetDevice(prev);
   return s;
+}
+
+extern "C" bsf_status bsf_set_kernel_timing(bsf_handle h, int ncalls) {
+  if (!h || ncalls < 0) return fail(BSF_E_INVALID_ARG, "bad arguments");
+  if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  cudaDeviceSynchronize();
+  for (cudaEvent_t e : h->tt.tev) cudaEventDestroy(e);
+  h->tt.tev.assign(4 * (size_t)ncalls, nullptr);
+  bsf_status s = BSF_OK;
+  for (cudaEvent_t& e : h->tt.tev)
+    if (cudaEventCreate(&e) != cudaSuccess) { s = fail(BSF_E_CUDA, "event creation failed"); break; }
+  h->tt.tev_n = s == BSF_OK ? ncalls : 0;
+  h->tt.tev_next = h->tt.tev_count = 0;
+  if (prev != h->device) cudaSetDevice(prev);
+  return s;
+}
+
+extern "C" int bsf_get_kernel_timing(bsf_handle h, float* core_ms, float* band_ms, int n) {
+  if (!h || h->tt.tev_n == 0) return 0;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  const int cnt = std::min(n, h->tt.tev_count);
+  // oldest first: the ring's last `cnt` calls
+  for (int k = 0; k < cnt; ++k) {
+    const int slot = ((h->tt.tev_next - cnt + k) % h->tt.tev_n + h->tt.tev_n) % h->tt.tev_n;
+    cudaEvent_t* tv = h->tt.tev.data() + 4 * slot;
+    cudaEventSynchronize(tv[1]);
+    cudaEventSynchronize(tv[3]);
+    if (core_ms && cudaEventElapsedTime(&core_ms[k], tv[0], tv[1]) != cudaSuccess) core_ms[k] = -1.0f;
+    if (band_ms && cudaEventElapsedTime(&band_ms[k], tv[2], tv[3]) != cudaSuccess) band_ms[k] = -1.0f;
+  }
+  if (prev != h->device) cudaSetDevice(prev);
+  return cnt;
 }
 
 extern "C" bsf_status bsf_allreduce_sum(double* d_buf, int64_t n, void* nccl_comm, bsf_stream stream) {

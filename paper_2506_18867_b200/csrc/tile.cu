@@ -931,9 +931,17 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     rc = frame_eval(*ft, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
                         tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, tt.side, ip);
     if (rc) return rc;
+    cudaEvent_t* tv = nullptr;   // [core start, core end, band start, band end] of this call
+    if (tt.tev_n > 0) {
+      tv = tt.tev.data() + 4 * tt.tev_next;
+      tt.tev_next = (tt.tev_next + 1) % tt.tev_n;
+      tt.tev_count = std::min(tt.tev_count + 1, tt.tev_n);
+      if (cudaEventRecord(tv[2], tt.side) != cudaSuccess) return -6;
+    }
     rc = band_eval(ft->band, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
                    tt.e_part, e_stride, ft->ntiles, d_params, ct->G, ct->detJ, tt.side, ip);
     if (rc) return rc;
+    if (tv && (cudaEventRecord(tv[3], tt.side) != cudaSuccess || cudaEventRecord(tv[0], st) != cudaSuccess)) return -6;
     if (ov) {
       const int64_t o1 = nfb + core_ctas_per_item(*ct, core_nch), o2 = o1 + nb_lo;
       rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
@@ -946,6 +954,7 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
                      nfb, core_nch, d_params, tt.detJ_ref, st, ip);
     }
     if (rc) return rc;
+    if (tv && cudaEventRecord(tv[1], st) != cudaSuccess) return -6;
     if (cudaEventRecord(tt.ev_join, tt.side) != cudaSuccess || cudaStreamWaitEvent(st, tt.ev_join, 0) != cudaSuccess)
       return -6;
     int nl = 1 + (ft->ntiles > 0) + (ft->band.ok && ft->band.nctas > 0);

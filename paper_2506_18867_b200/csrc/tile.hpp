@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <functional>
 #include <string>
+#include <vector>
 
 #include "dev.hpp"
 #include "host.hpp"
@@ -60,6 +61,10 @@ struct TileTables {
   int64_t e_core_cap = 0;
   cudaStream_t side = nullptr;     // frame kernel stream (fork / join with the caller's stream)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // live per-kernel timing (bsf_set_kernel_timing): per call, event pairs around the core launch (caller's
+  // stream) and the band launch (side stream), in a ring of tev_n calls
+  std::vector<cudaEvent_t> tev;
+  int tev_n = 0, tev_next = 0, tev_count = 0;
 };
 
 struct CoreTables;

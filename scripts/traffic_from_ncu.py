@@ -1,7 +1,8 @@
 """Build profiles/<round>_traffic.json from an ncu --set full capture of one bsf_eval_all_batch call
 (k_frame, k_band, k_core): DRAM bytes per algorithmic byte (read here with `ncu -i`, no GPU needed).
 
-usage: python scripts/traffic_from_ncu.py gpurun_out/core_full.ncu-rep 20 profiles/r01_traffic.json
+usage: python scripts/traffic_from_ncu.py gpurun_out/core_full.ncu-rep 20 profiles/r01_traffic.json [core_cps]
+core_cps: control points of the core rectangle (C2: 120 x 120 = 14400) for k_core's own ratio.
 """
 import csv, io, json, subprocess, sys, os
 
@@ -29,6 +30,11 @@ h = B.Sheet.from_sheet(sh, device=-1)
 n_cp = sh.n_u * sh.n_v
 alg_MB = nst * (48.0 * n_cp + 72.0 * h.nnzb) / 1e6
 tot = sum(v["dram_read_MB"] + v["dram_write_MB"] for v in kern.values())
+core_cps = int(sys.argv[4]) if len(sys.argv) > 4 else 14400
+for name, v in kern.items():
+    if name.startswith("k_core"):   # k_core's algorithmic bytes: 48 B per core control point + 23 blocks x 72 B
+        v["algorithmic_MB"] = nst * core_cps * (48 + 23 * 72) / 1e6
+        v["dram_bytes_per_algorithmic_byte"] = (v["dram_read_MB"] + v["dram_write_MB"]) / v["algorithmic_MB"]
 json.dump({"dram_bytes_per_algorithmic_byte": tot / alg_MB,
            "source": f"{rep} (ncu --set full, {', '.join(sorted(kern))} of one call, {nst} C2 states)",
            "kernels": kern, "algorithmic_MB": alg_MB,
