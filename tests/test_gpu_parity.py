@@ -381,3 +381,20 @@ def test_set_inertia_repeated_reuses_tables():
                       hdiag=diag_block_norms(vr, rp, ci, 0, sh.n_u), cmax=np.abs(sh.x).max(),
                       vabs=o.eval_ip(sh.x, XH[0].cpu().numpy(), m, dt, (0, -1.0, 0), pinned if pin_rows else None,
                                      flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2])
+
+
+def test_live_kernel_timing_ring():
+    """bsf_set_kernel_timing records k_core / k_band durations of the last calls (oldest first), and
+    recording does not change the outputs."""
+    sh = W.make_c2(state=7)
+    s = B.Sheet.from_sheet(sh)
+    x = torch.from_numpy(sh.x).cuda()
+    E0, g0, v0 = s(x, B.PROJECT_PSD)
+    s.set_kernel_timing(2)
+    for _ in range(3):
+        E1, g1, v1 = s(x, B.PROJECT_PSD)
+    core, band = s.kernel_timing(5)
+    assert len(core) == 2 and len(band) == 2 and all(t > 0 for t in core + band), (core, band)
+    assert torch.equal(g0, g1) and torch.equal(v0, v1) and torch.equal(E0, E1)
+    s.set_kernel_timing(0)
+    assert s.kernel_timing(5) == ([], [])
