@@ -166,13 +166,16 @@ bsf_status bsf_eval_all_batch_host(bsf_handle h, int nbatch, const double* h_x, 
  * bsf_get_lumped_mass: host m[owned rows][n_u] of the last bsf_set_inertia.
  * bsf_eval_ip_batch: as bsf_eval_all_batch plus the terms above; d_xhat: device, the predicted positions
  * x^ = x^n + dt v^n of the owned control points, [owned rows][n_u][3] per item, item stride xhat_stride
- * (doubles).  BSF_E_INVALID_ARG before bsf_set_inertia. */
+ * (doubles).  d_params: optional (device, as bsf_eval_all_batch_params, affine sheets): a batch of
+ * different sheets of this grid; each item's masses are the handle's scaled by its det(dX/d(u,v)) over the
+ * handle's (the same areal density).  BSF_E_INVALID_ARG before bsf_set_inertia. */
 bsf_status bsf_set_inertia(bsf_handle h, double areal_density, double dt, const double* gravity,
                            const uint8_t* pinned);
 bsf_status bsf_get_lumped_mass(bsf_handle h, double* m);
 bsf_status bsf_eval_ip_batch(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride, const double* d_xhat,
-                             int64_t xhat_stride, double* d_energy, double* d_grad, int64_t grad_stride,
-                             double* d_vals, int64_t vals_stride, int flags, bsf_stream stream);
+                             int64_t xhat_stride, const double* d_params, double* d_energy, double* d_grad,
+                             int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags,
+                             bsf_stream stream);
 
 /* ---- Linear algebra on the assembled Hessian (solve.cu) --------------------------------
  * The projected Newton step solves (H_inertia + H_elasticity) dC = -g; the paper

@@ -86,8 +86,8 @@ def lib():
                                               C.c_int64, C.c_int, C.c_int, vp]
         L.bsf_set_inertia.argtypes = [vp, C.c_double, C.c_double, dp, C.POINTER(C.c_uint8)]
         L.bsf_get_lumped_mass.argtypes = [vp, dp]
-        L.bsf_eval_ip_batch.argtypes = [vp, C.c_int, vp, C.c_int64, vp, C.c_int64, vp, vp, C.c_int64, vp, C.c_int64,
-                                        C.c_int, vp]
+        L.bsf_eval_ip_batch.argtypes = [vp, C.c_int, vp, C.c_int64, vp, C.c_int64, vp, vp, vp, C.c_int64, vp,
+                                        C.c_int64, C.c_int, vp]
         L.bsf_set_kernel_timing.argtypes = [vp, C.c_int]
         L.bsf_get_kernel_timing.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(C.c_float), C.c_int]
         L.bsf_eval_all_slab.argtypes = [vp, vp, vp, C.c_int, C.c_int, vp, vp, vp, C.c_int, vp]
@@ -255,7 +255,7 @@ class Sheet:
         _check(lib().bsf_get_lumped_mass(self._h, m.ctypes.data_as(C.POINTER(C.c_double))))
         return m
 
-    def eval_ip_batch(self, x, xhat, energy=None, grad=None, vals=None, flags=0, stream=None):
+    def eval_ip_batch(self, x, xhat, energy=None, grad=None, vals=None, flags=0, stream=None, params=None):
         """Incremental potential for a batch: x [B, *x_shape()], xhat [B, rows, n_u, 3] (CUDA float64);
         outputs as eval_all_batch."""
         B = x.shape[0]
@@ -264,7 +264,8 @@ class Sheet:
         gs = grad[0].numel() if grad is not None else 0
         vs = vals[0].numel() if vals is not None else 0
         _check(lib().bsf_eval_ip_batch(self._h, int(B), _ptr(x), x[0].numel(), _ptr(xhat), xhat[0].numel(),
-                                       _ptr(energy), _ptr(grad), gs, _ptr(vals), vs, int(flags), _stream(stream)))
+                                       _ptr(params), _ptr(energy), _ptr(grad), gs, _ptr(vals), vs, int(flags),
+                                       _stream(stream)))
 
     def eval_all_slab(self, x, energy=None, grad=None, vals=None, comm=None, rank=0, nranks=1, flags=0, stream=None):
         """Halo exchange (NCCL communicator handle `comm`, nranks > 1) overlapped with the assembly of the

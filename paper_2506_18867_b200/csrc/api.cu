@@ -476,8 +476,8 @@ bsf_status bsf_get_lumped_mass(bsf_handle h, double* m) {
 }
 
 bsf_status bsf_eval_ip_batch(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride, const double* d_xhat,
-                             int64_t xhat_stride, double* d_energy, double* d_grad, int64_t grad_stride, double* d_vals,
-                             int64_t vals_stride, int flags, bsf_stream stream) {
+                             int64_t xhat_stride, const double* d_params, double* d_energy, double* d_grad,
+                             int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags, bsf_stream stream) {
   if (!h || !d_x || !d_xhat || nbatch < 0) return fail(BSF_E_INVALID_ARG, "null argument / negative batch");
   if (!h->ip_set) return fail(BSF_E_INVALID_ARG, "bsf_set_inertia has not been called");
   if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
@@ -487,11 +487,14 @@ bsf_status bsf_eval_ip_batch(bsf_handle h, int nbatch, const double* d_x, int64_
   // epilogue pass after the assembly; the pinned elimination always runs after
   const bool fused = h->tile_ok && h->core_ok && h->ft.ok && !(flags & (BSF_TILE_ONLY | BSF_GENERIC_PATH)) &&
                      !ip_epilogue_forced();
+  if (d_params && !(h->sh.affine && h->tt.detJ_ref > 0.0))
+    return fail(BSF_E_INVALID_ARG, "per-item parameters need an affine sheet");
   bsf::IpFused ipf;
   ipf.xhat = d_xhat; ipf.xhs = xhat_stride; ipf.mass = h->d_mass; ipf.k = h->ip_k;
   for (int c = 0; c < 3; ++c) ipf.grav[c] = h->ip_g[c];
+  ipf.params = d_params; ipf.detJ_ref = h->tt.detJ_ref > 0.0 ? h->tt.detJ_ref : 1.0;   // the sheet's det J
   bsf_status s = eval_batch_impl(h, nbatch, d_x, x_stride, d_energy, d_grad, grad_stride, d_vals, vals_stride, flags,
-                                 stream, nullptr, fused ? &ipf : nullptr);
+                                 stream, d_params, fused ? &ipf : nullptr);
   if (s != BSF_OK || nbatch == 0) return s;
   int prev = 0;
   cudaGetDevice(&prev);
@@ -510,6 +513,7 @@ bsf_status bsf_eval_ip_batch(bsf_handle h, int nbatch, const double* d_x, int64_
     A.ncp = (int)ncp; A.n_u = h->sh.n_u; A.r0 = h->sh.r0; A.xlo = h->sh.xlo;
     A.k = h->ip_k;
     for (int c = 0; c < 3; ++c) A.grav[c] = h->ip_g[c];
+    A.params = d_params; A.detJ_ref = ipf.detJ_ref;
     int nl = 0;
     if (fused ? bsf::ip_pin(A, nbatch, static_cast<cudaStream_t>(stream), &nl)
               : bsf::ip_eval(A, nbatch, d_energy, static_cast<cudaStream_t>(stream), &nl))

@@ -74,6 +74,8 @@ struct BandArgs {
   int64_t xhs;
   const double* mass;
   double ipk, grav[3];
+  const double* ipar;      // optional per-item parameters: masses scale by ipar[9 item + 4] / ip_detJ
+  double ip_detJ;
 };
 
 template <int B, int E, class F>
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
     if (valid && A.xhat) {   // incremental potential: diagonal m/dt^2, gradient and energy (gradient lanes)
       const int ai = axis ? t : s, aj = axis ? s : t;
       const int64_t aloc = (int64_t)(aj - A.r0) * A.n_u + ai;
-      const double mm = A.mass[aloc];
+      const double mm = A.mass[aloc] * (A.ipar ? A.ipar[9 * (int64_t)item + 4] / A.ip_detJ : 1.0);
       if (hess) {
         if (r3 == c3) acc[12] += A.ipk * mm;
       } else {
@@ -694,6 +696,8 @@ int band_eval(const BandTables& bt, const Sheet& sh, const double* d_x, int64_t 
   A.xhat = ip ? ip->xhat : nullptr; A.xhs = ip ? ip->xhs : 0; A.mass = ip ? ip->mass : nullptr;
   A.ipk = ip ? ip->k : 0.0;
   for (int c = 0; c < 3; ++c) A.grav[c] = ip ? ip->grav[c] : 0.0;
+  A.ipar = ip ? ip->params : nullptr;
+  A.ip_detJ = ip ? ip->detJ_ref : 1.0;
   dim3 grid(bt.nctas, nbatch);
   k_band<<<grid, kThreads, bt.smem, st>>>(A);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;

@@ -63,6 +63,8 @@ struct CoreArgs {
   int64_t xhs;
   const double* mass;
   double ipk, grav[3];
+  const double* ipar;      // optional per-item parameters: masses scale by ipar[9 item + 4] / ip_detJ
+  double ip_detJ;
 };
 
 // shared constants block (doubles)
@@ -359,6 +361,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
   const int ja = A.JA + kRows * sa, jb = min(A.JA + kRows * sb, A.JB);
   const double* __restrict__ x = A.x + item * A.xs;
   double* vals = A.vals ? A.vals + item * A.vs : nullptr;
+  // incremental potential: per-item mass scale (det J of the item's affine rest map over the handle's)
+  const double msc = (IP && A.ipar) ? A.ipar[9 * (int64_t)item + 4] / A.ip_detJ : 1.0, ipk_m = A.ipk * msc;
   double* gout = A.g ? A.g + item * A.gs : nullptr;
 
   // ---- per-item affine map and stiffness
@@ -501,7 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
             }
             double* gdst = nullptr;
             const uint32_t par = k & 1;
-            const double dshift = (IP && diag && active) ? A.ipk * A.mass[(int64_t)(jr - A.r0) * A.n_u + i] : 0.0;
+            const double dshift = (IP && diag && active) ? ipk_m * A.mass[(int64_t)(jr - A.r0) * A.n_u + i] : 0.0;
             if (PI == 0)
               gather_role<0>(base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
                              8 * (o_pv - o_uu), diag, cst, st_lane,
@@ -546,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
             // incremental potential: m/dt^2 (x - xhat) - m g on the gradient, its energy on this lane
             double g0 = 0.0;
             if constexpr (IP) {
-              const double mm = A.mass[al], xa = x[((int64_t)(jr - A.xlo) * A.n_u + i) * 3 + r];
+              const double mm = A.mass[al] * msc, xa = x[((int64_t)(jr - A.xlo) * A.n_u + i) * 3 + r];
               const double d = xa - A.xhat[item * A.xhs + al * 3 + r], gr = A.grav[r];
               g0 = A.ipk * mm * d - mm * gr;
               e_acc += 0.5 * A.ipk * mm * d * d - mm * gr * xa;
@@ -872,6 +876,8 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
   A.xhat = ip ? ip->xhat : nullptr; A.xhs = ip ? ip->xhs : 0; A.mass = ip ? ip->mass : nullptr;
   A.ipk = ip ? ip->k : 0.0;
   for (int c = 0; c < 3; ++c) A.grav[c] = ip ? ip->grav[c] : 0.0;
+  A.ipar = ip ? ip->params : nullptr;
+  A.ip_detJ = ip ? ip->detJ_ref : 1.0;
   A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride;
   A.epart = e_part; A.e_stride = e_stride; A.e_off = e_off;
   A.row_ptr = ct.row_ptr; A.rp_base = ct.rp_base; A.rp_stride = ct.rp_stride; A.params = d_params;

@@ -70,6 +70,8 @@ struct FrameArgs {
   int64_t xhs;
   const double* mass;
   double ipk, grav[3];
+  const double* ipar;      // optional per-item parameters: masses scale by ipar[9 item + 4] / ip_detJ
+  double ip_detJ;
 };
 
 constexpr int kPosD = 8 * 8 * 3;    // (tw + 4) * (th + 4) * 3 for 4x4 tiles
@@ -235,7 +237,8 @@ __global__ void __launch_bounds__(kThreads, 3) k_frame(const FrameArgs A) {
         hb = fma(rec[ea], rec[eb], hb);
       }
     }
-    if (A.xhat && task.w) hb += A.ipk * A.mass[task.w - 1];   // diagonal block: inertia m_a/dt^2
+    if (A.xhat && task.w)   // diagonal block: inertia m_a/dt^2
+      hb += A.ipk * A.mass[task.w - 1] * (A.ipar ? A.ipar[9 * (int64_t)item + 4] / A.ip_detJ : 1.0);
     h[0] += hb; h[4] += hb; h[8] += hb;
     if (A.vals) {
       double* dst = A.vals + item * A.vs + (int64_t)out * 9;
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_frame(const FrameArgs A) {
       const int aj = (int)(al / A.n_u) + A.r0, ai = (int)(al % A.n_u);
       const double* xa = pos + ((aj - (j0 - 2)) * PW + (ai - (i0 - 2))) * 3;
       const double* xh = A.xhat + item * A.xhs + 3 * al;
-      const double mm = A.mass[al];
+      const double mm = A.mass[al] * (A.ipar ? A.ipar[9 * (int64_t)item + 4] / A.ip_detJ : 1.0);
       double gi[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
@@ -517,6 +520,8 @@ int frame_eval(const FrameTables& ft, const Sheet& sh, const double* d_x, int64_
   A.xhat = ip ? ip->xhat : nullptr; A.xhs = ip ? ip->xhs : 0; A.mass = ip ? ip->mass : nullptr;
   A.ipk = ip ? ip->k : 0.0;
   for (int c = 0; c < 3; ++c) A.grav[c] = ip ? ip->grav[c] : 0.0;
+  A.ipar = ip ? ip->params : nullptr;
+  A.ip_detJ = ip ? ip->detJ_ref : 1.0;
   A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride;
   A.epart = e_part; A.e_stride = e_stride; A.e_off = e_off;
   A.row_ptr = d_row_ptr; A.params = d_params;

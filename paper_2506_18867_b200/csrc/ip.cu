@@ -25,7 +25,8 @@ __global__ void __launch_bounds__(kIpThreads) k_ip(IpArgs A) {
     const int j = a / A.n_u, i = a - j * A.n_u;   // owned-row index j (row r0 + j)
     const double* x = A.x + item * A.xs + ((int64_t)(j + A.r0 - A.xlo) * A.n_u + i) * 3;
     const double* xh = A.xhat + item * A.xhs + (int64_t)a * 3;
-    const double m = A.mass[a], km = A.k * m;
+    const double msc = A.params ? A.params[9 * (int64_t)item + 4] / A.detJ_ref : 1.0;   // per-item det J
+    const double m = A.mass[a] * msc, km = A.k * m;
     double d[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {

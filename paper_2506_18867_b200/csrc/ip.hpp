@@ -24,6 +24,8 @@ struct IpArgs {
   int ncp, n_u, r0, xlo;
   double k;              // 1 / dt^2
   double grav[3];
+  const double* params;  // optional per-item affine parameters [item][9]: masses scale by params[4] / detJ_ref
+  double detJ_ref;
 };
 
 // Fused form (the assembly kernels add the terms themselves: core, band and corner kernels): the
@@ -34,6 +36,8 @@ struct IpFused {
   const double* mass;    // [owned cps]
   double k;
   double grav[3];
+  const double* params;  // optional per-item affine parameters: masses scale by params[9 item + 4] / detJ_ref
+  double detJ_ref;
 };
 
 int ip_eval(IpArgs A, int nbatch, double* d_energy, cudaStream_t st, int* launches);

@@ -398,3 +398,34 @@ def test_live_kernel_timing_ring():
     assert torch.equal(g0, g1) and torch.equal(v0, v1) and torch.equal(E0, E1)
     s.set_kernel_timing(0)
     assert s.kernel_timing(5) == ([], [])
+
+
+def test_incremental_potential_batch_of_different_sheets():
+    """bsf_eval_ip_batch with per-item affine parameters (C5 layout): each item's masses follow its own rest
+    map (det J), against each sheet's own oracle incremental potential."""
+    sheets = W.make_c5(count=3, n=40)
+    s = B.Sheet.from_sheet(sheets[0])
+    R0, dt, grav = 0.12, 5e-3, np.array([0.0, 0.0, -9.81])
+    s.set_inertia(R0, dt, gravity=grav)
+    X = torch.stack([torch.from_numpy(q.x) for q in sheets]).cuda()
+    rng = np.random.default_rng(21)
+    XH = X + torch.from_numpy(rng.normal(0, 1e-3, tuple(X.shape))).cuda()
+    P = torch.from_numpy(np.stack([B.affine_params(q.rest_xy, B.material_from_young(q.E, q.nu, q.h))
+                                   for q in sheets])).cuda()
+    nb = len(sheets)
+    E = torch.zeros(nb, dtype=torch.float64, device="cuda")
+    G = torch.zeros_like(X)
+    V = torch.zeros((nb, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    for path in (0, B.TILE_ONLY):   # fused kernels; epilogue kernel
+        s.eval_ip_batch(X, XH, E, G, V, flags=B.PROJECT_PSD | path, params=P)
+        torch.cuda.synchronize()
+        for k, q in enumerate(sheets):
+            o = O.Oracle.from_sheet(q)
+            m = o.lumped_mass(R0)
+            xh = XH[k].cpu().numpy()
+            Er, gr, vr = o.eval_ip(q.x, xh, m, dt, grav, flags=O.FLAG_PROJECT)
+            rp, ci = o.pattern()
+            va = o.eval_ip(q.x, xh, m, dt, grav, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False,
+                           gradient=False)[2]
+            assert_parity(float(E[k]), G[k].cpu().numpy(), V[k].cpu().numpy(), Er, gr, vr, what=f"C5 IP item {k}",
+                          hdiag=diag_block_norms(vr, rp, ci, 0, q.n_u), cmax=np.abs(q.x).max(), vabs=va)
