@@ -20,7 +20,8 @@
 //   * optional PSD projection of each FBW term by cyclic Jacobi eigen-decomposition (D7);
 //   * scatter into the oracle's own set-union BSR pattern by binary search.
 //
-//  Parity status of each function: see the header of tests/test_oracle_pins.py; every function
+//  Parity status of each function: see the headers of tests/test_oracle_pins.py and (incremental
+//  potential: lumped mass, inertia, gravity, pinned elimination) tests/test_oracle_ip.py; every function
 //  below is pinned (no "parity unpinned" entries) except the membrane stiffness convention
 //  mu_st/mu_sh of oracle_material_from_young (D6, a naming convention: "parity unpinned").
 // =====================================================================================
