@@ -132,6 +132,16 @@ def _hptr(t):
     return C.c_void_p(t.data_ptr())
 
 
+def _item(t):
+    """Elements per batch item of a [B, ...] tensor (0 if None; valid for B == 0)."""
+    if t is None:
+        return 0
+    n = 1
+    for d in t.shape[1:]:
+        n *= int(d)
+    return n
+
+
 def _stream(stream):
     import torch
     s = torch.cuda.current_stream() if stream is None else stream
@@ -234,9 +244,9 @@ class Sheet:
         B = x.shape[0]
         if tuple(x.shape[1:]) != self.x_shape():
             raise ValueError(f"x must be [B, {self.x_shape()}]")
-        gs = grad[0].numel() if grad is not None else 0
-        vs = vals[0].numel() if vals is not None else 0
-        _check(lib().bsf_eval_all_batch(self._h, int(B), _ptr(x), x[0].numel(), _ptr(energy), _ptr(grad), gs,
+        gs = _item(grad)
+        vs = _item(vals)
+        _check(lib().bsf_eval_all_batch(self._h, int(B), _ptr(x), _item(x), _ptr(energy), _ptr(grad), gs,
                                         _ptr(vals), vs, int(flags), _stream(stream)))
 
     def set_inertia(self, areal_density, dt, gravity=None, pinned=None):
@@ -261,9 +271,9 @@ class Sheet:
         B = x.shape[0]
         if tuple(x.shape[1:]) != self.x_shape() or tuple(xhat.shape) != (B, self.row_end - self.row_begin, self.n_u, 3):
             raise ValueError("x must be [B, *x_shape()] and xhat [B, rows, n_u, 3]")
-        gs = grad[0].numel() if grad is not None else 0
-        vs = vals[0].numel() if vals is not None else 0
-        _check(lib().bsf_eval_ip_batch(self._h, int(B), _ptr(x), x[0].numel(), _ptr(xhat), xhat[0].numel(),
+        gs = _item(grad)
+        vs = _item(vals)
+        _check(lib().bsf_eval_ip_batch(self._h, int(B), _ptr(x), _item(x), _ptr(xhat), _item(xhat),
                                        _ptr(params), _ptr(energy), _ptr(grad), gs, _ptr(vals), vs, int(flags),
                                        _stream(stream)))
 
@@ -317,9 +327,9 @@ class Sheet:
             raise ValueError(f"x_host / x_stage must be [B, {self.x_shape()}]")
         if x_host.is_cuda or not x_stage.is_cuda:
             raise ValueError("x_host must be a CPU tensor and x_stage a CUDA tensor")
-        gs = grad[0].numel() if grad is not None else 0
-        vs = vals[0].numel() if vals is not None else 0
-        _check(lib().bsf_eval_all_batch_host(self._h, int(B), _hptr(x_host), x_host[0].numel(), _ptr(x_stage),
+        gs = _item(grad)
+        vs = _item(vals)
+        _check(lib().bsf_eval_all_batch_host(self._h, int(B), _hptr(x_host), _item(x_host), _ptr(x_stage),
                                              _ptr(params), _hptr(energy_host), _ptr(energy), _ptr(grad), gs,
                                              _ptr(vals), vs, int(flags), int(chunk), _stream(stream)))
 
@@ -329,9 +339,9 @@ class Sheet:
         B = x.shape[0]
         if tuple(x.shape[1:]) != self.x_shape() or tuple(params.shape) != (B, 9):
             raise ValueError("x must be [B, *x_shape()] and params [B, 9]")
-        gs = grad[0].numel() if grad is not None else 0
-        vs = vals[0].numel() if vals is not None else 0
-        _check(lib().bsf_eval_all_batch_params(self._h, int(B), _ptr(x), x[0].numel(), _ptr(params), _ptr(energy),
+        gs = _item(grad)
+        vs = _item(vals)
+        _check(lib().bsf_eval_all_batch_params(self._h, int(B), _ptr(x), _item(x), _ptr(params), _ptr(energy),
                                                _ptr(grad), gs, _ptr(vals), vs, int(flags), _stream(stream)))
 
     def eval_energy(self, x, energy, flags=0, stream=None):

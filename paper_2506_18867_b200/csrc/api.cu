@@ -365,8 +365,8 @@ static bool ip_epilogue_forced() {   // debug / comparison switch, read once
 static bsf_status eval_batch_impl(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride, double* d_energy,
                                   double* d_grad, int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags,
                                   bsf_stream stream, const double* d_params, const bsf::IpFused* ip = nullptr) {
+  if (h && nbatch == 0) return BSF_OK;   // empty batch: no-op (its pointers may be NULL)
   if (!h || !d_x || nbatch < 0) return fail(BSF_E_INVALID_ARG, "null argument / negative batch");
-  if (nbatch == 0) return BSF_OK;
   if (flags & ~31) return fail(BSF_E_INVALID_ARG, "unknown flag bits");
   if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
   const int64_t xn = (int64_t)(h->sh.xhi - h->sh.xlo) * h->sh.n_u * 3;
@@ -478,6 +478,7 @@ bsf_status bsf_get_lumped_mass(bsf_handle h, double* m) {
 bsf_status bsf_eval_ip_batch(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride, const double* d_xhat,
                              int64_t xhat_stride, const double* d_params, double* d_energy, double* d_grad,
                              int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags, bsf_stream stream) {
+  if (h && nbatch == 0) return BSF_OK;   // empty batch: no-op
   if (!h || !d_x || !d_xhat || nbatch < 0) return fail(BSF_E_INVALID_ARG, "null argument / negative batch");
   if (!h->ip_set) return fail(BSF_E_INVALID_ARG, "bsf_set_inertia has not been called");
   if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
@@ -616,6 +617,7 @@ bsf_status bsf_eval_all_batch_host(bsf_handle h, int nbatch, const double* h_x, 
                                    const double* d_params, double* h_energy, double* d_energy, double* d_grad,
                                    int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags, int chunk,
                                    bsf_stream stream) {
+  if (h && nbatch == 0) return BSF_OK;   // empty batch: no-op
   if (!h || !h_x || !d_x_stage || nbatch < 0) return fail(BSF_E_INVALID_ARG, "null argument / negative batch");
   if (h_energy && !d_energy) return fail(BSF_E_INVALID_ARG, "h_energy needs the device energy buffer");
   const bool async_stage = (flags & BSF_ASYNC_STAGE) != 0;

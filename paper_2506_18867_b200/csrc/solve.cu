@@ -348,6 +348,12 @@ int pcg(const SolveArgs& A, const double* d_vals, const double* d_b, double* d_x
   double hs[kSN];
   *status = 0;
   for (int it = 0;; it += check_every) {
+    if (max_iter <= 0) {   // no iterations: report the initial residual
+      if (cudaMemcpyAsync(hs, W.S, sizeof(hs), cudaMemcpyDeviceToHost, run) != cudaSuccess ||
+          cudaStreamSynchronize(run) != cudaSuccess)
+        return -6;
+      break;
+    }
     if (Gr) { if (cudaGraphLaunch(Gr->exec, run) != cudaSuccess) return -6; }
     else chunk(run);
     if (cudaPeekAtLastError() != cudaSuccess) return -6;
@@ -363,7 +369,7 @@ int pcg(const SolveArgs& A, const double* d_vals, const double* d_b, double* d_x
   *iters = (int)hs[kSIter];
   *relres = hs[kSBnorm2] > 0.0 ? std::sqrt(hs[kSRr] / hs[kSBnorm2]) : 0.0;
   // 0 converged, 1 iteration budget spent, 2 not SPD
-  *status = hs[kSDone] == 1.0 ? 0 : ((hs[kSDone] == 2.0 || bad) ? 2 : 1);
+  *status = (hs[kSDone] == 1.0 || hs[kSRr] == 0.0) ? 0 : ((hs[kSDone] == 2.0 || bad) ? 2 : 1);
   return 0;
 }
 

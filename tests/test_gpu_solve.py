@@ -90,3 +90,29 @@ def test_pcg_rejects_indefinite():
     s = B.Sheet.from_sheet(sh)
     with pytest.raises(B.BsfError):
         s.pcg(torch.from_numpy(v).cuda(), torch.from_numpy(np.ones_like(g)).cuda(), max_iter=50, rtol=1e-10)
+
+
+def test_solve_and_ip_edge_cases():
+    """b = 0 converges at once to x = 0; max_iter = 0 leaves the initial guess; invalid inertia settings and
+    PCG on a slab handle are refused; an empty batch is a no-op."""
+    sh = W.make_c1()
+    o, m, xhat, g, v = _ip_system(sh)
+    s = B.Sheet.from_sheet(sh)
+    V = torch.from_numpy(v).cuda()
+    zero = torch.zeros((sh.n_v, sh.n_u, 3), dtype=torch.float64, device="cuda")
+    x, it, rr = s.pcg(V, zero.clone(), max_iter=100, rtol=1e-10)
+    assert it == 0 and rr == 0.0 and torch.count_nonzero(x) == 0
+    x0 = torch.ones_like(zero)
+    x, it, rr = s.pcg(V, torch.from_numpy(-g).cuda(), x=x0.clone(), max_iter=0, rtol=1e-10)
+    assert torch.equal(x, x0)
+    with pytest.raises(B.BsfError):
+        s.set_inertia(0.1, 0.0)
+    with pytest.raises(B.BsfError):
+        s.set_inertia(-1.0, 1e-3)
+    slab = B.Sheet.from_sheet(sh, row_begin=4, row_end=10)
+    _, _, vs = O.Oracle.from_sheet(sh, r0=4, r1=10).eval(sh.x, flags=O.FLAG_PROJECT)
+    with pytest.raises(B.BsfError):
+        slab.pcg(torch.from_numpy(vs).cuda(), torch.zeros((6, sh.n_u, 3), dtype=torch.float64, device="cuda"))
+    s.set_inertia(0.1, 1e-3)
+    X = torch.zeros((0,) + s.x_shape(), dtype=torch.float64, device="cuda")
+    s.eval_ip_batch(X, torch.zeros((0, sh.n_v, sh.n_u, 3), dtype=torch.float64, device="cuda"))
