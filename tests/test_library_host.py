@@ -96,3 +96,27 @@ def test_host_only_handle_refuses_compute():
     s = B.Sheet.from_sheet(sh, device=-1)
     with pytest.raises((B.BsfError, ValueError)):
         s.eval_all(torch.zeros(s.x_shape(), dtype=torch.float64))
+
+
+def test_host_only_handle_refuses_every_compute_entry_point():
+    """Every device entry point returns BSF_E_NO_DEVICE on a host-only handle (device = -1) without touching
+    its (dummy, non-null) pointers; the host-side inertia set-up and mass query still work."""
+    import ctypes as C
+    sh = W.make_c1()
+    s = B.Sheet.from_sheet(sh, device=-1)
+    L = B.lib()
+    p = C.c_void_p(16)   # never dereferenced
+    no_dev = -9
+    assert L.bsf_eval_all(s._h, p, p, p, p, 0, None) == no_dev
+    assert L.bsf_eval_all_batch(s._h, 1, p, 0, p, p, 0, p, 0, 0, None) == no_dev
+    assert L.bsf_eval_all_slab(s._h, p, None, 0, 1, p, p, p, 0, None) == no_dev
+    assert L.bsf_bsr_spmv(s._h, p, p, p, None) == no_dev
+    lo, hi = C.c_double(), C.c_double()
+    assert L.bsf_gershgorin(s._h, p, C.byref(lo), C.byref(hi), None) == no_dev
+    it, rr = C.c_int(), C.c_double()
+    assert L.bsf_pcg(s._h, p, p, p, 10, 1e-8, C.byref(it), C.byref(rr), None) == no_dev
+    assert L.bsf_set_kernel_timing(s._h, 4) == no_dev
+    s.set_inertia(0.2, 1e-3, gravity=(0, 0, -9.81))
+    assert s.lumped_mass().shape == (sh.n_v, sh.n_u)
+    assert L.bsf_eval_ip_batch(s._h, 1, p, 0, p, 0, None, p, p, 0, p, 0, 0, None) == no_dev
+    assert L.bsf_eval_ip_batch(s._h, 0, None, 0, None, 0, None, None, None, 0, None, 0, 0, None) == 0   # empty batch
