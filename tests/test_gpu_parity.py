@@ -305,6 +305,10 @@ def test_incremental_potential_matches_oracle(case):
         pinned = np.zeros((sh.n_v, sh.n_u), bool)
         pinned[-1, :] = True
         pinned[0, :3] = True
+    if case == "slab":   # a pinned row inside the slab and one outside it within the columns' reach
+        pinned = np.zeros((sh.n_v, sh.n_u), bool)
+        pinned[50, 10:20] = True
+        pinned[91, :] = True
     o = O.Oracle.from_sheet(sh, r0=r0, r1=r1)
     m = o.lumped_mass(R0)
     rng = np.random.default_rng(17)
