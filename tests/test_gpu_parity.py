@@ -433,3 +433,30 @@ def test_incremental_potential_batch_of_different_sheets():
                            gradient=False)[2]
             assert_parity(float(E[k]), G[k].cpu().numpy(), V[k].cpu().numpy(), Er, gr, vr, what=f"C5 IP item {k}",
                           hdiag=diag_block_norms(vr, rp, ci, 0, q.n_u), cmax=np.abs(q.x).max(), vabs=va)
+
+
+def test_incremental_potential_curved_rest():
+    """Non-affine (curved) rest shape: per-point rest data on the tile path, masses with varying det J, the
+    epilogue kernel; against the oracle."""
+    base = W.make_sheet(20, 1.0, 12, n_modes=3, amp=3e-3, lam=0.2)
+    rest = W.make_curved_rest(20, 20, 5)
+    sh = W.Sheet(20, 20, base.knots_u, base.knots_v, rest, base.x, base.E, base.nu, base.h)
+    o = O.Oracle.from_sheet(sh)
+    R0, dt, grav = 0.3, 2e-3, np.array([0.1, -9.81, 0.0])
+    m = o.lumped_mass(R0)
+    s = B.Sheet.from_sheet(sh)
+    s.set_inertia(R0, dt, gravity=grav)
+    assert np.max(np.abs(s.lumped_mass() - m)) < 1e-14 * m.max()
+    rng = np.random.default_rng(8)
+    xh = sh.x + rng.normal(0, 1e-3, sh.x.shape)
+    E = torch.zeros(1, dtype=torch.float64, device="cuda")
+    G = torch.zeros((1, 20, 20, 3), dtype=torch.float64, device="cuda")
+    V = torch.zeros((1, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    s.eval_ip_batch(torch.from_numpy(sh.x).cuda().unsqueeze(0), torch.from_numpy(xh).cuda().unsqueeze(0), E, G, V,
+                    flags=B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    Er, gr, vr = o.eval_ip(sh.x, xh, m, dt, grav, flags=O.FLAG_PROJECT)
+    rp, ci = o.pattern()
+    va = o.eval_ip(sh.x, xh, m, dt, grav, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
+    assert_parity(E.item(), G[0].cpu().numpy(), V[0].cpu().numpy(), Er, gr, vr, what="IP curved rest",
+                  hdiag=diag_block_norms(vr, rp, ci, 0, 20), cmax=np.abs(sh.x).max(), vabs=va)
