@@ -300,7 +300,7 @@ int pcg(const SolveArgs& A, const double* d_vals, const double* d_b, double* d_x
   const int nbv = (A.nrows + kVecThreads - 1) / kVecThreads;
   const int nbs = (A.nrows + kWarpsPerBlk - 1) / kWarpsPerBlk;
   const int nbn = (n3 + kVecThreads - 1) / kVecThreads;
-  cudaMemsetAsync(W.bad, 0, sizeof(int), st);
+  if (cudaMemsetAsync(W.bad, 0, sizeof(int), st) != cudaSuccess) return -6;
   k_diag_inv<<<(A.nrows + 127) / 128, 128, 0, st>>>(A.diag, d_vals, W.dinv, A.nrows, W.bad);
   // |b|^2
   k_dot<<<nbv, kVecThreads, 0, st>>>(d_b, d_b, n3, W.part);
@@ -364,8 +364,11 @@ int pcg(const SolveArgs& A, const double* d_vals, const double* d_b, double* d_x
   }
   if (Gr && (cudaEventRecord(Gr->e1, run) != cudaSuccess || cudaStreamWaitEvent(st, Gr->e1, 0) != cudaSuccess))
     return -6;
+  // the diagonal-block check ran on st before the iterations, which `run` has been synchronised behind
   int bad = 0;
-  cudaMemcpy(&bad, W.bad, sizeof(int), cudaMemcpyDeviceToHost);
+  if (cudaMemcpyAsync(&bad, W.bad, sizeof(int), cudaMemcpyDeviceToHost, run) != cudaSuccess ||
+      cudaStreamSynchronize(run) != cudaSuccess)
+    return -6;
   *iters = (int)hs[kSIter];
   *relres = hs[kSBnorm2] > 0.0 ? std::sqrt(hs[kSRr] / hs[kSBnorm2]) : 0.0;
   // 0 converged, 1 iteration budget spent, 2 not SPD
