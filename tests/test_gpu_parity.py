@@ -177,6 +177,34 @@ def test_batch_matches_single_calls():
                   hdiag=diag_block_norms(vr, rp, ci, 0, sheets[1].n_u), cmax=np.abs(sheets[1].x).max(), vabs=va)
 
 
+def test_c2_bench_launch_100_states():
+    """C2 in exactly the bench's launch: the 100 seeded states of bench.workload("C2") in one
+    bsf_eval_all_batch call (one long row chunk per core strip at this batch size).  Three items
+    against the oracle; sampled items bit for bit against single-state calls (many short chunks)."""
+    import bench
+    sheets = bench.workload("C2", 100)
+    s = B.Sheet.from_sheet(sheets[0])
+    X = torch.stack([torch.from_numpy(q.x) for q in sheets]).cuda()
+    nb = len(sheets)
+    E = torch.zeros(nb, dtype=torch.float64, device="cuda")
+    G = torch.zeros((nb,) + tuple(X.shape[1:]), dtype=torch.float64, device="cuda")
+    V = torch.zeros((nb, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    s.eval_all_batch(X, E, G, V, B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    for k in (0, 37, 99):
+        E1, g1, v1 = s(X[k].contiguous(), B.PROJECT_PSD)
+        assert torch.equal(g1, G[k]) and torch.equal(v1, V[k])
+        assert rel_energy(float(E1.item()), float(E[k])) <= 1e-13
+    for k in (0, 51, 99):
+        q = sheets[k]
+        o = O.Oracle.from_sheet(q)
+        Er, gr, vr = o.eval(q.x, flags=O.FLAG_PROJECT)
+        rp, ci = o.pattern()
+        va = o.eval(q.x, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
+        assert_parity(float(E[k]), G[k].cpu().numpy(), V[k].cpu().numpy(), Er, gr, vr, what=f"C2 bench item {k}",
+                      hdiag=diag_block_norms(vr, rp, ci, 0, q.n_u), cmax=np.abs(q.x).max(), vabs=va)
+
+
 def test_slab_sheet_nccl_single_rank():
     """The library's NCCL entry points on one rank (unique id, comm init, all-reduce) and the
     SlabSheet driver against the oracle."""
