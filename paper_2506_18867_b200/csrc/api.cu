@@ -17,6 +17,7 @@
 #include "tile.hpp"
 #include "ip.hpp"
 #include "solve.hpp"
+#include "g3.hpp"
 
 namespace bsf {
 int generic_eval(const GenericTables& t, const double* d_x, const Mat& mat, int flags, int64_t nnzb, int64_t nrows,
@@ -41,6 +42,9 @@ struct bsf_sheet {
   bsf::CoreTables ct;
   bool core_ok = false;
   bsf::FrameTables ft;
+  bsf::G3Tables g3;                     // G3-FULL rule on affine sheets (g3.cu)
+  bool g3_ok = false;
+  bool generic_ok = false;              // generic gather path built (point count fits its index packing)
   cudaStream_t copy_stream = nullptr;   // host-buffer calls: position uploads
   cudaEvent_t ev_copy = nullptr, ev_start = nullptr;
   struct StageUse { const void* ptr; cudaEvent_t done; };   // BSF_ASYNC_STAGE: last reader of each stage
@@ -139,7 +143,9 @@ bsf_status build_generic(bsf_sheet* h) {
   const bsf::Sheet& sh = h->sh;
   bsf::GenericTables& t = h->gt;
   const int64_t M = (int64_t)sh.mem.size(), B = (int64_t)sh.bend.size();
-  if (M >= (1 << 23) || B >= (1 << 23)) return fail(BSF_E_INVALID_ARG, "too many quadrature points per handle (use slabs)");
+  // the incidence lists pack point indices in 23 bits: larger handles run on the tile / G3 kernels only
+  h->generic_ok = !(M >= (1 << 23) || B >= (1 << 23));
+  if (!h->generic_ok) return BSF_OK;
   t.Mm = M;
   t.Bm = B;
   const int nu = sh.n_u;
@@ -294,6 +300,13 @@ bsf_status bsf_create(int n_u, int n_v, const double* knots_u, const double* kno
         }
       }
     }
+    if (s == BSF_OK) {   // G3-FULL on affine sheets: its own kernel (else tile / generic)
+      const int grc = bsf::build_g3(h->sh, h->g3, terr, h->dalloc());
+      if (grc < 0) s = fail(BSF_E_OOM, terr);
+      h->g3_ok = (grc == 0);
+    }
+    if (s == BSF_OK && !h->generic_ok && !h->tile_ok && !h->g3_ok)
+      s = fail(BSF_E_INVALID_ARG, "too many quadrature points per handle (use slabs)");
   }
   cudaSetDevice(prev);
   if (s != BSF_OK) {
@@ -331,6 +344,8 @@ bsf_status bsf_get_pattern(bsf_handle h, int32_t* row_ptr, int32_t* col_idx) {
   return BSF_OK;
 }
 
+static bool use_g3(bsf_handle h, int flags) { return h->g3_ok && !(flags & (BSF_GENERIC_PATH | BSF_TILE_ONLY)); }
+
 bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, double* d_grad, double* d_vals, int flags,
                         bsf_stream stream) {
   if (!h || !d_x) return fail(BSF_E_INVALID_ARG, "null argument");
@@ -346,10 +361,15 @@ bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, doubl
   auto st = static_cast<cudaStream_t>(stream);
   int nl = 0;
   int rc;
-  if (h->tile_ok && !(flags & BSF_GENERIC_PATH))
+  if (use_g3(h, flags))
+    rc = bsf::g3_eval(h->g3, d_x, 0, m, flags, 1, d_energy, d_grad, 0, d_vals, 0, nullptr, st, &nl, h->dalloc());
+  else if (h->tile_ok && !(flags & BSF_GENERIC_PATH))
     rc = bsf::tile_eval(h->tt, h->sh, d_x, 0, m, flags, 1, d_energy, d_grad, 0, d_vals, 0, st, &nl, h->dalloc(), nullptr,
                         (h->core_ok && !(flags & BSF_TILE_ONLY)) ? &h->ct : nullptr, &h->ft);
-  else
+  else if (!h->generic_ok) {
+    if (prev != h->device) cudaSetDevice(prev);
+    return fail(BSF_E_INVALID_ARG, "generic path not built for this handle (too many points; use slabs)");
+  } else
     rc = bsf::generic_eval(h->gt, d_x, m, flags, nnzb, nrows, d_energy, d_grad, d_vals, st, &nl);
   h->last_launches = nl;
   if (prev != h->device) cudaSetDevice(prev);
@@ -380,14 +400,22 @@ static bsf_status eval_batch_impl(bsf_handle h, int nbatch, const double* d_x, i
   if (prev != h->device) cudaSetDevice(h->device);
   auto st = static_cast<cudaStream_t>(stream);
   int nl = 0, rc = 0;
-  if (d_params && !(h->tile_ok && h->sh.affine && !(flags & BSF_GENERIC_PATH))) {
+  if (d_params && !use_g3(h, flags) && !(h->tile_ok && h->sh.affine && !(flags & BSF_GENERIC_PATH))) {
     if (prev != h->device) cudaSetDevice(prev);
     return fail(BSF_E_INVALID_ARG, "per-item parameters need an affine sheet on the tile path");
   }
-  if (h->tile_ok && !(flags & BSF_GENERIC_PATH)) {
+  if (use_g3(h, flags)) {
+    if (ip) rc = -1;   // the incremental potential takes the epilogue path on this kernel
+    else
+      rc = bsf::g3_eval(h->g3, d_x, x_stride, h->mat, flags, nbatch, d_energy, d_grad, grad_stride, d_vals, vals_stride,
+                        d_params, st, &nl, h->dalloc());
+  } else if (h->tile_ok && !(flags & BSF_GENERIC_PATH)) {
     rc = bsf::tile_eval(h->tt, h->sh, d_x, x_stride, h->mat, flags, nbatch, d_energy, d_grad, grad_stride, d_vals,
                         vals_stride, st, &nl, h->dalloc(), d_params,
                         (h->core_ok && !(flags & BSF_TILE_ONLY)) ? &h->ct : nullptr, &h->ft, ip);
+  } else if (!h->generic_ok) {
+    if (prev != h->device) cudaSetDevice(prev);
+    return fail(BSF_E_INVALID_ARG, "generic path not built for this handle (too many points; use slabs)");
   } else {
     const int64_t nrows = (int64_t)(h->sh.r1 - h->sh.r0) * h->sh.n_u, nnzb = (int64_t)h->sh.col_idx.size();
     for (int b = 0; b < nbatch && rc == 0; ++b) {
@@ -817,14 +845,20 @@ extern "C" bsf_status bsf_eval_all_slab(bsf_handle h, double* d_x, void* nccl_co
   int nl = 0;
   if (s == BSF_OK) {
     int rc;
-    if (h->tile_ok && !(flags & BSF_GENERIC_PATH))
+    if (use_g3(h, flags)) {
+      if (ov.jb > ov.ja && cudaStreamWaitEvent(st, ov.ready, 0) != cudaSuccess) rc = -6;   // no split on this path
+      else rc = bsf::g3_eval(h->g3, d_x, 0, h->mat, flags, 1, d_energy, d_grad, 0, d_vals, 0, nullptr, st, &nl, h->dalloc());
+    } else if (h->tile_ok && !(flags & BSF_GENERIC_PATH))
       rc = bsf::tile_eval(h->tt, sh, d_x, 0, h->mat, flags, 1, d_energy, d_grad, 0, d_vals, 0, st, &nl, h->dalloc(),
                           nullptr, (h->core_ok && !(flags & BSF_TILE_ONLY)) ? &h->ct : nullptr, &h->ft, nullptr,
                           (ov.jb > ov.ja) ? &ov : nullptr);
+    else if (!h->generic_ok)
+      rc = -100;
     else
       rc = bsf::generic_eval(h->gt, d_x, h->mat, flags, (int64_t)sh.col_idx.size(), (int64_t)(sh.r1 - sh.r0) * sh.n_u,
                              d_energy, d_grad, d_vals, st, &nl);
-    if (rc) s = check_cuda("kernel launch") == BSF_OK ? fail(BSF_E_CUDA, "launch failed") : BSF_E_CUDA;
+    if (rc == -100) s = fail(BSF_E_INVALID_ARG, "generic path not built for this handle (too many points; use slabs)");
+    else if (rc) s = check_cuda("kernel launch") == BSF_OK ? fail(BSF_E_CUDA, "launch failed") : BSF_E_CUDA;
   }
   h->last_launches = nl;
   if (prev != h->device) cudaSetDevice(prev);
