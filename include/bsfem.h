@@ -65,8 +65,12 @@ enum {
   BSF_PROJECT_PSD = 1,   /* per-term PSD projection of the FBW F-space Hessian (D7)  */
   BSF_NO_MEMBRANE = 2,   /* debug: drop the membrane terms                                       */
   BSF_NO_BENDING = 4,    /* debug: drop the bending terms                                        */
-  BSF_GENERIC_PATH = 8,  /* force the generic point/gather kernels instead of the fused tile path */
-  BSF_TILE_ONLY = 16,    /* debug: the tile kernel on the whole sheet, without the interior core kernel */
+  BSF_GENERIC_PATH = 8,  /* force the generic point/gather kernels instead of the fused tile path; handles
+                            with >= 2^23 points per rule (e.g. G3-FULL at 1024^2) do not build that path and
+                            return BSF_E_INVALID_ARG for this flag */
+  BSF_TILE_ONLY = 16,    /* debug: the tile kernel on the whole sheet, without the interior core kernel (and
+                            not the G3-FULL kernel k_g3); falls back to the generic path where the tile
+                            kernel does not fit */
   BSF_ASYNC_STAGE = 32   /* bsf_eval_all_batch_host only: the upload into d_x_stage waits only for the previous
                             host-buffer call on this handle that read the same d_x_stage (not for all work
                             queued on `stream`), so alternating two staging buffers overlaps one call's
