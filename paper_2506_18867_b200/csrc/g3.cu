@@ -57,7 +57,7 @@ struct G3Args {
   const int8_t* vcls;
   const double* beta;
   int n_u, n_v, Su, Sv, r0, xlo, xhi, tlo, thi, cint_u, cint_v;
-  int project, flags;
+  int project, flags, dbg;
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
   double what[kNG];
 };
@@ -220,9 +220,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_g3(const G3Args A) {
   // same instructions whatever the chunking (bit-identical results across launch configurations).
   for (int j = ja - 2; j < jb; j += 2) {
     __syncthreads();
-    e_acc += span_rows(A, x, rec, pos, tab, kc, i0, i1, ja, jb, j, tid);
+    if (!(A.dbg & 1) || j < ja) e_acc += span_rows(A, x, rec, pos, tab, kc, i0, i1, ja, jb, j, tid);
     __syncthreads();
-    if (j < ja || (!hess_warp && !grad_warp)) continue;
+    if (j < ja || (!hess_warp && !grad_warp) || (A.dbg & 2)) continue;
     const int i = i0 + m, jr = j + h;
     const bool active = i < i1 && jr < jb;
     int sl[3];
@@ -613,6 +613,10 @@ int g3_eval(G3Tables& gt, const double* d_x, int64_t x_stride, const Mat& mat, i
   A.n_u = gt.n_u; A.n_v = gt.n_v; A.Su = gt.Su; A.Sv = gt.Sv; A.r0 = gt.r0; A.xlo = gt.xlo; A.xhi = gt.xhi;
   A.tlo = gt.tlo; A.thi = gt.thi; A.cint_u = std::max(gt.cint_u, 0); A.cint_v = std::max(gt.cint_v, 0);
   A.project = (flags & 1) ? 1 : 0; A.flags = flags;
+  {   // profiling switches (read once per process): 1 no point phase after the first step, 2 no gather
+    static const int dbg = getenv("BSF_G3_DEBUG") ? atoi(getenv("BSF_G3_DEBUG")) : 0;
+    A.dbg = dbg;
+  }
   A.G00 = gt.G[0]; A.G01 = gt.G[1]; A.G10 = gt.G[2]; A.G11 = gt.G[3]; A.detJ = gt.detJ;
   A.mu1 = (flags & 2) ? 0.0 : mat.mu_st1;
   A.mu2 = (flags & 2) ? 0.0 : mat.mu_st2;
