@@ -25,7 +25,8 @@
  *    its precomputed tables and scratch, released by bsf_destroy.
  *  - Asynchrony: compute calls validate arguments synchronously, enqueue kernels on `stream` and
  *    return without synchronising; asynchronous CUDA faults surface as BSF_E_CUDA on a later call.
- *    All compute calls are CUDA-graph capturable.
+ *    All compute calls are CUDA-graph capturable once the handle has run one call of the same batch
+ *    size outside the capture (that call sizes the handle's scratch: energy partials, CTA lists).
  *  - Errors: every call returns bsf_status; bsf_last_error() gives a thread-local message.
  *  - Thread safety: one handle may be used by one host thread / stream at a time.
  */

@@ -594,7 +594,8 @@ int g3_eval(G3Tables& gt, const double* d_x, int64_t x_stride, const Mat& mat, i
       gt.cta_uni = static_cast<int4*>(p);
       gt.uni_cap = (int)gt.h_uni.size();
     }
-    if (cudaMemcpy(gt.cta_uni, gt.h_uni.data(), sizeof(int4) * gt.h_uni.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    if (cudaMemcpyAsync(gt.cta_uni, gt.h_uni.data(), sizeof(int4) * gt.h_uni.size(), cudaMemcpyHostToDevice, st) !=
+        cudaSuccess)
       return -6;
     gt.n_uni = (int)gt.h_uni.size();
     gt.chunk_key = nbatch;

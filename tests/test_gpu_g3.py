@@ -130,3 +130,28 @@ def test_g3_c4_full_size_sampled_rows():
     assert rel_energy(float(E.item()), parts) <= 1e-12
     with pytest.raises(B.BsfError):   # no generic fallback at this size
         s(xd, B.PROJECT_PSD | B.GENERIC_PATH)
+
+
+def test_g3_cuda_graph_capture_and_replay():
+    """The G3 launches (frame + interior instances + energy) capture into a CUDA graph after one warm call of
+    the same batch size; replaying on new positions gives the direct call's outputs bit for bit."""
+    sheets = [W.make_sheet(40, 1.0, 20 + k, n_modes=3, amp=5e-3) for k in range(2)]
+    s = B.Sheet.from_sheet(sheets[0], G3, G3)
+    X = torch.stack([torch.from_numpy(q.x) for q in sheets]).cuda()
+    E = torch.zeros(2, dtype=torch.float64, device="cuda")
+    G = torch.zeros_like(X)
+    V = torch.zeros((2, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        s.eval_all_batch(X, E, G, V, B.PROJECT_PSD, st)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        s.eval_all_batch(X, E, G, V, B.PROJECT_PSD, st)
+    X.copy_(torch.stack([torch.from_numpy(W.make_sheet(40, 1.0, 30 + k, n_modes=3, amp=5e-3).x) for k in range(2)]))
+    g.replay()
+    torch.cuda.synchronize()
+    E2, G2, V2 = torch.zeros_like(E), torch.zeros_like(G), torch.zeros_like(V)
+    s.eval_all_batch(X, E2, G2, V2, B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    assert torch.equal(G, G2) and torch.equal(V, V2) and torch.equal(E, E2)
