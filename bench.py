@@ -193,7 +193,9 @@ def bench_c4_slabs(args, rank, world, local_rank):
     flags = args.flags | (B.GENERIC_PATH if args.generic else 0)
     sh = W.make_c4()
     comm = D.NcclComm(rank, world, local_rank) if world > 1 else None
-    slab = D.SlabSheet(sh, rank, world, device=local_rank, comm=comm)
+    # edge slabs also run the frame kernels: they own fewer rows (distributed.edge_rows_discount)
+    slab = D.SlabSheet(sh, rank, world, device=local_rank, comm=comm,
+                       edge_discount=D.edge_rows_discount(sh.n_v, world))
     owned = torch.from_numpy(np.ascontiguousarray(sh.x[slab.r0:slab.r1])).to(dev)
     owned_host = owned.cpu().pin_memory()
     slab.load_owned(owned)

@@ -16,17 +16,45 @@ import ctypes as C
 import numpy as np
 
 
-def slab_bounds(n_v: int, world: int):
-    """Balanced contiguous row slabs; every slab owns >= 2 rows (the halo exchange sends 2 rows)."""
+def slab_bounds(n_v: int, world: int, edge_discount: int = 0):
+    """Contiguous row slabs; every slab owns >= 2 rows (the halo exchange sends 2 rows).
+
+    edge_discount = 0: balanced.  > 0 (world >= 3): the first and last slab own that many rows fewer than
+    the balanced share, the middle slabs share the difference.  The edge slabs also carry the sheet's frame
+    (the edge bands and corners, whose kernels take SMs beside the interior kernel), so equal rows are not
+    equal time; `edge_rows_discount` gives the value measured for the fused path."""
     if world < 1 or n_v < 2 * world:
         raise ValueError(f"cannot split {n_v} rows into {world} slabs of >= 2 rows")
-    base, extra = divmod(n_v, world)
+    if edge_discount < 0:
+        raise ValueError("edge_discount must be >= 0")
+    base = n_v // world
+    d = min(edge_discount, max(0, base - 2)) if world >= 3 else 0
+    sizes = [0] * world
+    sizes[0] = sizes[-1] = base - d
+    rest = n_v - 2 * (base - d)
+    mb, mx = divmod(rest, world - 2) if world >= 3 else (0, 0)
+    if world >= 3:
+        for k in range(1, world - 1):
+            sizes[k] = mb + (1 if k - 1 < mx else 0)
+    else:
+        b2, e2 = divmod(n_v, world)
+        sizes = [b2 + (1 if k < e2 else 0) for k in range(world)]
     out, r = [], 0
-    for k in range(world):
-        n = base + (1 if k < extra else 0)
+    for n in sizes:
         out.append((r, r + n))
         r += n
+    assert r == n_v and all(b - a >= 2 for a, b in out)
     return out
+
+
+def edge_rows_discount(n_v: int, world: int) -> int:
+    """Rows taken off each edge slab of the fused path.  Model (B200, C4, scripts/slab_compute_bound.py): an
+    edge slab's band and corner kernels delay its interior kernel by ~29 us, ~12 row-steps of each of its 4
+    row chunks, i.e. ~48 rows to shed, spread so that each of the world - 2 middle slabs takes its share:
+    d = 48 (world - 2) / world (N=4: 24, N=8: 36), at most a quarter of the balanced share."""
+    if world < 3:
+        return 0
+    return min(round(48 * (world - 2) / world), (n_v // world) // 4)
 
 
 def halo_rows(r0: int, r1: int, n_v: int):
@@ -87,11 +115,11 @@ class SlabSheet:
     """One rank's slab of a sheet: handle, position buffer with halos, outputs."""
 
     def __init__(self, sh, rank: int, world: int, device: int = 0, comm: NcclComm | None = None, material=None,
-                 membrane_rule=0, bending_rule=0):
+                 membrane_rule=0, bending_rule=0, edge_discount: int = 0):
         import torch
 
         from . import Sheet
-        self.r0, self.r1 = slab_bounds(sh.n_v, world)[rank]
+        self.r0, self.r1 = slab_bounds(sh.n_v, world, edge_discount)[rank]
         self.lo, self.hi = halo_rows(self.r0, self.r1, sh.n_v)
         self.rank, self.world, self.comm = rank, world, comm
         self.n_u, self.n_v = sh.n_u, sh.n_v

@@ -1,5 +1,6 @@
 """One-GPU evidence for the C4 strong-scaling row: the compute time of ONE rank's slab of a
-1024^2 sheet at N = 1, 2, 4, 8 (slab_bounds(1024, N), the middle rank: halo rows on both sides), each rank
+1024^2 sheet at N = 1, 2, 4, 8 (slab_bounds(1024, N, d) for the balanced partition and the edge discount d the
+bench uses; the slowest of the first, middle and last rank), each rank
 timed alone on this GPU with CUDA events (bsf_eval_all on a slab handle, no exchange).  The N-GPU step is
 at least max over ranks of this time plus the halo exchange that the library overlaps with the interior
 rows; this prints the compute-only efficiency bound T1 / (N * T_N) = T1 / (N * slab time).  No rank waits
@@ -37,8 +38,11 @@ def time_call(s, x, flags, reps=20):
 sh = W.make_c4()
 rows = []
 t1 = None
+from paper_2506_18867_b200.distributed import edge_rows_discount
+
 for N in (1, 2, 4, 8):
-    bounds = slab_bounds(sh.n_v, N)
+  for disc in sorted({0, edge_rows_discount(sh.n_v, N)}):
+    bounds = slab_bounds(sh.n_v, N, disc)
     worst = 0.0
     for rank in sorted({0, N // 2, N - 1}):
         r0, r1 = bounds[rank]
@@ -48,8 +52,8 @@ for N in (1, 2, 4, 8):
         worst = max(worst, ms)
         s.close()
     t1 = worst if N == 1 else t1
-    row = {"N": N, "slab_rows": bounds[N // 2][1] - bounds[N // 2][0], "max_rank_ms": round(worst, 4),
-           "compute_efficiency_bound": round(t1 / (N * worst), 3)}
+    row = {"N": N, "edge_discount": disc, "rows_edge_mid": [bounds[0][1] - bounds[0][0], bounds[N // 2][1] - bounds[N // 2][0]],
+           "max_rank_ms": round(worst, 4), "compute_efficiency_bound": round(t1 / (N * worst), 3)}
     rows.append(row)
     print(json.dumps(row), flush=True)
 if len(sys.argv) > 1:

@@ -25,6 +25,22 @@ def test_slab_bounds():
         D.slab_bounds(5, 3)
 
 
+def test_slab_bounds_edge_discount():
+    """Edge slabs (which also carry the frame kernels) own fewer rows; the partition stays contiguous, complete
+    and >= 2 rows per slab, and reduces to the balanced one for 1-2 ranks or discount 0."""
+    for n_v, world in [(1024, 8), (1024, 4), (128, 3), (9, 4), (16, 3)]:
+        d = D.edge_rows_discount(n_v, world)
+        b = D.slab_bounds(n_v, world, d)
+        assert b[0][0] == 0 and b[-1][1] == n_v and all(b[k][1] == b[k + 1][0] for k in range(world - 1))
+        sizes = [r1 - r0 for r0, r1 in b]
+        assert min(sizes) >= 2 and sizes[0] == sizes[-1] <= min(sizes[1:-1])
+        mid = sizes[1:-1]
+        assert max(mid) - min(mid) <= 1
+    assert D.slab_bounds(1024, 8, 24)[0] == (0, 104) and D.slab_bounds(1024, 8, 24)[-1] == (920, 1024)
+    assert D.slab_bounds(1024, 2, 24) == D.slab_bounds(1024, 2)
+    assert D.slab_bounds(1024, 8, 0) == D.slab_bounds(1024, 8)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
