@@ -155,3 +155,45 @@ def test_g3_cuda_graph_capture_and_replay():
     s.eval_all_batch(X, E2, G2, V2, B.PROJECT_PSD)
     torch.cuda.synchronize()
     assert torch.equal(G, G2) and torch.equal(V, V2) and torch.equal(E, E2)
+
+
+@pytest.mark.parametrize("n,slab", [(5, None), (6, None), (40, (20, 22)), (40, (0, 2)), (40, (38, 40))])
+def test_g3_smallest_sheets_and_two_row_slabs(n, slab):
+    """Edge cases: the smallest G3 sheets (S = 3, 4: every span is a boundary span, no interior class) and
+    2-row slabs at the top, middle and bottom of a sheet."""
+    sh = W.make_sheet(n, 1.0, 40 + n, n_modes=2, amp=5e-3)
+    r0, r1 = slab if slab else (0, n)
+    _, Er, gr, vr, rp, ci, va = _oracle(sh, B.PROJECT_PSD, r0, r1)
+    s = B.Sheet.from_sheet(sh, G3, G3, row_begin=r0, row_end=r1)
+    E, g, v = _gpu(s, sh.x, B.PROJECT_PSD)
+    assert s.last_launch_count() <= 3
+    assert_parity(E, g, v, Er, gr, vr, what=f"g3 n={n} slab={slab}", hdiag=diag_block_norms(vr, rp, ci, r0, sh.n_u),
+                  cmax=np.abs(sh.x).max(), vabs=va)
+
+
+def test_g3_incremental_potential():
+    """bsf_eval_ip_batch on a G3-FULL handle (k_g3 + the incremental-potential epilogue) against the oracle's
+    eval_ip under the same rule, with pinned control points."""
+    sh = W.make_sheet(40, 1.0, 77, n_modes=3, amp=5e-3)
+    R0, dt, grav = 0.15, 4e-3, np.array([0.0, -9.81, 0.5])
+    pinned = np.zeros((sh.n_v, sh.n_u), bool)
+    pinned[-1, :] = True
+    mu = O.material_from_young(sh.E, sh.nu, sh.h)
+    o = O.Oracle.from_sheet(sh, G3, G3, mu=mu)
+    m = o.lumped_mass(R0)
+    rng = np.random.default_rng(5)
+    s = B.Sheet.from_sheet(sh, G3, G3)
+    s.set_inertia(R0, dt, gravity=grav, pinned=pinned)
+    xh = sh.x + rng.normal(0, 2e-3, sh.x.shape)
+    X = torch.from_numpy(sh.x).cuda().unsqueeze(0).contiguous()
+    XH = torch.from_numpy(xh).cuda().unsqueeze(0).contiguous()
+    E = torch.zeros(1, dtype=torch.float64, device="cuda")
+    G = torch.zeros_like(X)
+    V = torch.zeros((1, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    s.eval_ip_batch(X, XH, E, G, V, flags=B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    Er, gr, vr = o.eval_ip(sh.x, xh, m, dt, grav, pinned, flags=O.FLAG_PROJECT)
+    rp, ci = o.pattern()
+    va = o.eval_ip(sh.x, xh, m, dt, grav, pinned, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
+    assert_parity(E[0].item(), G[0].cpu().numpy(), V[0].cpu().numpy(), Er, gr, vr, what="g3 ip",
+                  hdiag=diag_block_norms(vr, rp, ci, 0, sh.n_u), cmax=np.abs(sh.x).max(), vabs=va)
