@@ -928,13 +928,6 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     }
     if (cudaEventRecord(tt.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(tt.side, tt.ev_fork, 0) != cudaSuccess)
       return -6;
-    static const int core_first_env = getenv("BSF_CORE_FIRST") ? atoi(getenv("BSF_CORE_FIRST")) : -1;
-    const bool core_first = !ov && core_first_env == 1;
-    if (core_first) {
-      rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
-                     nfb, core_nch, d_params, tt.detJ_ref, st, ip);
-      if (rc) return rc;
-    }
     rc = frame_eval(*ft, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
                         tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, tt.side, ip);
     if (rc) return rc;
@@ -956,7 +949,7 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
       if (rc) return rc;
       rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
                      o2, 1, d_params, tt.detJ_ref, st, ip, halo->jb, ct->RJ1);
-    } else if (!core_first) {
+    } else {
       rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
                      nfb, core_nch, d_params, tt.detJ_ref, st, ip);
     }
