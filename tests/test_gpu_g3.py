@@ -197,3 +197,21 @@ def test_g3_incremental_potential():
     va = o.eval_ip(sh.x, xh, m, dt, grav, pinned, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
     assert_parity(E[0].item(), G[0].cpu().numpy(), V[0].cpu().numpy(), Er, gr, vr, what="g3 ip",
                   hdiag=diag_block_norms(vr, rp, ci, 0, sh.n_u), cmax=np.abs(sh.x).max(), vabs=va)
+
+
+@pytest.mark.parametrize("rules", [(0, 2), (2, 0), (1, 2)])
+def test_mixed_rules_fall_back(rules):
+    """G3-FULL for one energy only: k_g3 does not apply (both energies must be G3-FULL); the tile / generic
+    path computes it, against the oracle under the same rule pair."""
+    sh = W.make_sheet(24, 1.0, 61, n_modes=3, amp=5e-3)
+    mr, br = rules
+    mu = O.material_from_young(sh.E, sh.nu, sh.h)
+    o = O.Oracle.from_sheet(sh, mr, br, mu=mu)
+    Er, gr, vr = o.eval(sh.x, flags=O.FLAG_PROJECT)
+    rp, ci = o.pattern()
+    va = o.eval(sh.x, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
+    s = B.Sheet.from_sheet(sh, mr, br)
+    assert np.array_equal(s.pattern()[1], ci)
+    E, g, v = _gpu(s, sh.x, B.PROJECT_PSD)
+    assert_parity(E, g, v, Er, gr, vr, what=f"rules {rules}", hdiag=diag_block_norms(vr, rp, ci, 0, sh.n_u),
+                  cmax=np.abs(sh.x).max(), vabs=va)
