@@ -48,7 +48,9 @@ typedef enum {
   BSF_E_KNOTS = -2,             /* knots not open, uniform, integer        */
   BSF_E_TOO_SMALL = -3,         /* < 3 spans per direction with a REDUCED rule                   */
   BSF_E_DEGENERATE_GEOMETRY = -4, /* det J <= 0 at a quadrature point (rest map not regular)     */
-  BSF_E_SINGULAR_STRETCH = -5,  /* reserved: |F e_beta| = 0 (FBW undefined)                      */
+  BSF_E_SINGULAR_STRETCH = -5,  /* |F e_beta| < 1e-12 at a membrane point (FBW undefined; SPEC.md:290
+                                   clamps, this library reports): detected by the kernels, returned by
+                                   the handle's next compute call or bsf_poll_status                 */
   BSF_E_CUDA = -6,
   BSF_E_OOM = -7,
   BSF_E_NCCL = -8,
@@ -121,8 +123,9 @@ bsf_status bsf_get_sizes(bsf_handle h, int64_t* n_rows, int64_t* nnzb, int64_t* 
 /* Copy the pattern (host buffers): row_ptr[n_rows+1] (int32, starts at 0), col_idx[nnzb]. */
 bsf_status bsf_get_pattern(bsf_handle h, int32_t* row_ptr, int32_t* col_idx);
 
-/* Batched fused pass over nbatch states of the same sheet (e.g. the 100 states of one Newton
- * sequence): item b reads d_x + b*x_stride and writes d_energy[b], d_grad + b*grad_stride,
+/* Batched fused pass over nbatch independent states of the same sheet (e.g. the states of many sheet
+ * instances, or the line-search candidates of one Newton iteration; successive Newton iterates depend on
+ * each other and are separate calls): item b reads d_x + b*x_stride and writes d_energy[b], d_grad + b*grad_stride,
  * d_vals + b*vals_stride (strides in doubles, >= one item's size).  One kernel launch covers all
  * items on the tile path.  Outputs may be NULL. */
 bsf_status bsf_eval_all_batch(bsf_handle h, int nbatch, const double* d_x, int64_t x_stride,
@@ -138,6 +141,13 @@ bsf_status bsf_eval_all_batch_params(bsf_handle h, int nbatch, const double* d_x
                                      const double* d_params, double* d_energy, double* d_grad,
                                      int64_t grad_stride, double* d_vals, int64_t vals_stride, int flags,
                                      bsf_stream stream);
+
+/* Step a2 of a flat affine sheet (J = dX/d(u,v), G = J^-1, w = what det J) for one item of
+ * bsf_eval_all_batch_params: the rest map (rest_xy: host, [n_v][n_u][2]) is evaluated at the centre of every
+ * knot span and must have one constant J (to 1e-11 of |J|) and vanishing second derivatives.
+ * out9: host, G00 G01 G10 G11 det J mu_st1 mu_st2 mu_sh mu_bd.  Host call.  Errors: BSF_E_TOO_SMALL (< 3
+ * control points per direction), BSF_E_DEGENERATE_GEOMETRY (det J <= 0), BSF_E_INVALID_ARG (not affine). */
+bsf_status bsf_affine_params(int n_u, int n_v, const double* rest_xy, const bsf_material* mat, double* out9);
 
 /* Host-buffer variant (end-to-end use): the positions of the nbatch states come from HOST memory h_x
  * (item b at h_x + b*x_stride; page-locked memory lets the upload overlap the computation) and are
@@ -224,6 +234,14 @@ bsf_status bsf_nccl_get_unique_id(void* out128);
 bsf_status bsf_nccl_comm_init(int nranks, const void* id128, int rank, int device, void** comm);
 bsf_status bsf_nccl_comm_destroy(void* comm);
 
+/* The halo exchange plan of this slab as rank `rank` of `nranks` (row slabs in order): plan8[4 d + k] for
+ * d = 0 (the peer below, rank-1) and d = 1 (the peer above, rank+1): k = 0 peer rank (-1: no exchange on that
+ * side), 1 send offset, 2 receive offset, 3 count, all in doubles of the slab's position buffer d_x.  The
+ * slab sends its first / last (<= 2) owned rows and receives the peer's into its halo rows.  bsf_halo_exchange
+ * executes exactly this plan over NCCL; other transports (e.g. torch.distributed) can execute it too.  Host
+ * call; works on host-only handles. */
+bsf_status bsf_halo_plan(bsf_handle h, int rank, int nranks, int64_t* plan8);
+
 /* Halo exchange: sends the 2 first / last owned rows to the previous / next slab and receives
  * theirs into d_x's halo rows (layout as above), as one NCCL group on `stream`.  Every slab must
  * own >= 2 rows.  No Hessian data is communicated (each slab recomputes the <= 2 rows of shared
@@ -257,6 +275,13 @@ int bsf_get_kernel_timing(bsf_handle h, float* core_ms, float* band_ms, int n);
 
 /* Number of kernel launches the most recent compute call enqueued (for the bench's claim). */
 int bsf_last_launch_count(bsf_handle h);
+
+/* BSF_E_SINGULAR_STRETCH (with bsf_last_error naming the quadrature point: its anchor knot span and batch
+ * item) if a COMPLETED earlier call on this handle met |F e_beta| < 1e-12 at a membrane point whose energy
+ * it owns, else BSF_OK.  The report is consumed (the next compute call would otherwise return it and
+ * enqueue nothing).  Host read of mapped memory: no synchronisation, so synchronise the call's stream first
+ * to be sure to see it. */
+bsf_status bsf_poll_status(bsf_handle h);
 
 /* Thread-local description of the most recent failure; never NULL. */
 const char* bsf_last_error(void);

@@ -31,7 +31,7 @@ SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_mate
            "bsf_allreduce_sum", "bsf_get_core_rect", "bsf_eval_all_batch_host", "bsf_set_inertia",
            "bsf_get_lumped_mass", "bsf_eval_ip_batch", "bsf_bsr_spmv", "bsf_gershgorin", "bsf_pcg",
            "bsf_eval_all_slab", "bsf_set_kernel_timing", "bsf_get_kernel_timing",
-           "bsf_last_launch_count", "bsf_last_error"]
+           "bsf_last_launch_count", "bsf_poll_status", "bsf_affine_params", "bsf_halo_plan", "bsf_last_error"]
 
 
 class BsfError(RuntimeError):
@@ -94,6 +94,9 @@ def lib():
         L.bsf_bsr_spmv.argtypes = [vp, vp, vp, vp, vp]
         L.bsf_gershgorin.argtypes = [vp, vp, dp, dp, vp]
         L.bsf_pcg.argtypes = [vp, vp, vp, vp, C.c_int, C.c_double, C.POINTER(C.c_int), dp, vp]
+        L.bsf_poll_status.argtypes = [vp]
+        L.bsf_halo_plan.argtypes = [vp, C.c_int, C.c_int, i64p]
+        L.bsf_affine_params.argtypes = [C.c_int, C.c_int, dp, C.POINTER(Material), dp]
         for s in SYMBOLS:
             getattr(L, s).restype = C.c_int if s not in ("bsf_last_error",) else C.c_char_p
         _lib = L
@@ -149,18 +152,17 @@ def _stream(stream):
 
 
 def affine_params(rest_xy, material) -> np.ndarray:
-    """Per-item parameters of bsf_eval_all_batch_params for a flat Greville rest grid.  The affine map
-    X(u, v) advances by one interior Greville spacing per knot span, so dX/du and dX/dv are the
-    interior control-point spacings (exact for Greville placement)."""
-    rest_xy = np.asarray(rest_xy, dtype=np.float64)
-    du = rest_xy[0, 3] - rest_xy[0, 2]
-    dv = rest_xy[3, 0] - rest_xy[2, 0]
-    J = np.array([[du[0], dv[0]], [du[1], dv[1]]])
-    G = np.linalg.inv(J)
+    """Per-item parameters of bsf_eval_all_batch_params (G00 G01 G10 G11 det J mu_st1 mu_st2 mu_sh mu_bd)
+    of a flat affine rest sheet rest_xy [n_v, n_u, 2], computed by the library (bsf_affine_params)."""
+    rest = np.ascontiguousarray(rest_xy, dtype=np.float64)
+    if rest.ndim != 3 or rest.shape[2] != 2:
+        raise ValueError("rest_xy must be [n_v, n_u, 2]")
     if not isinstance(material, Material):
         material = Material(*[float(v) for v in material])
-    return np.array([G[0, 0], G[0, 1], G[1, 0], G[1, 1], np.linalg.det(J), material.mu_st1, material.mu_st2,
-                     material.mu_sh, material.mu_bd])
+    out = np.zeros(9)
+    _check(lib().bsf_affine_params(rest.shape[1], rest.shape[0], rest.ctypes.data_as(C.POINTER(C.c_double)),
+                                   C.byref(material), out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
 
 
 class Sheet:
@@ -352,6 +354,18 @@ class Sheet:
 
     def assemble_hessian(self, x, vals, flags=0, stream=None):
         _check(lib().bsf_assemble_hessian(self._h, _ptr(x), _ptr(vals), int(flags), _stream(stream)))
+
+    def halo_plan(self, rank, nranks):
+        """The library's halo exchange plan [(peer, send_off, recv_off, count) below, (...) above], offsets and
+        counts in doubles of the position buffer (bsf_halo_plan)."""
+        p = (C.c_int64 * 8)()
+        _check(lib().bsf_halo_plan(self._h, int(rank), int(nranks), p))
+        return [tuple(p[0:4]), tuple(p[4:8])]
+
+    def poll_status(self):
+        """Raise BsfError(SINGULAR_STRETCH) if a completed earlier call met |F e_beta| < 1e-12 at a membrane point
+        (synchronise its stream first); the report is consumed."""
+        _check(lib().bsf_poll_status(self._h))
 
     def last_launch_count(self) -> int:
         return int(lib().bsf_last_launch_count(self._h))

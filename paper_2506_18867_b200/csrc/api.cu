@@ -69,11 +69,15 @@ struct bsf_sheet {
   std::vector<void*> allocs;
   int last_launches = 0;
   bool host_only = false;
+  // singular-stretch word (fbw.cuh fbw_flag_singular): page-locked, mapped host memory the kernels store to
+  unsigned long long* sflag_host = nullptr;
+  unsigned long long* sflag_dev = nullptr;
   ~bsf_sheet() {
     if (host_only) return;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
+    if (sflag_host) cudaFreeHost(sflag_host);
     if (tt.side) cudaStreamDestroy(tt.side);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ev_copy) cudaEventDestroy(ev_copy);
@@ -225,6 +229,27 @@ bsf_status build_generic(bsf_sheet* h) {
   return BSF_OK;
 }
 
+// Sets the singular-stretch word of the handle for the launches enqueued in this scope (dev.hpp call_sflag).
+struct SflagScope {
+  explicit SflagScope(unsigned long long* p) { bsf::call_sflag() = p; }
+  ~SflagScope() { bsf::call_sflag() = nullptr; }
+};
+
+// A completed earlier call found a singular stretch (|F e_beta| < 1e-12 at a membrane point; SURVEY §8(b),
+// SPEC.md:290): report it once, naming the point, and clear the word.  Host read, no synchronisation.
+bsf_status take_singular(bsf_sheet* h) {
+  if (!h->sflag_host) return BSF_OK;
+  const unsigned long long c = *(volatile unsigned long long*)h->sflag_host;
+  if (!(c >> 63)) return BSF_OK;
+  *(volatile unsigned long long*)h->sflag_host = 0ull;
+  const int item = (int)((c >> 44) & 0x7FFFF), t = (int)((c >> 22) & 0x3FFFFF), s = (int)(c & 0x3FFFFF);
+  std::string where = t == 0x3FFFFF ? "membrane point #" + std::to_string(s) + " of the generic path"
+                                    : "a membrane point anchored at knot span (" + std::to_string(s) + ", " +
+                                          std::to_string(t) + ") of batch item " + std::to_string(item);
+  return fail(BSF_E_SINGULAR_STRETCH, "singular stretch |F e_beta| < 1e-12 (FBW undefined) at " + where +
+                                          " in an earlier call; its outputs hold inf / NaN there");
+}
+
 bsf_status check_cuda(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(BSF_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -281,7 +306,16 @@ bsf_status bsf_create(int n_u, int n_v, const double* knots_u, const double* kno
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  bsf_status s = build_generic(h);
+  bsf_status s = BSF_OK;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&h->sflag_host), sizeof(unsigned long long), cudaHostAllocMapped) !=
+          cudaSuccess ||
+      cudaHostGetDevicePointer(reinterpret_cast<void**>(&h->sflag_dev), h->sflag_host, 0) != cudaSuccess) {
+    cudaGetLastError();
+    s = fail(BSF_E_CUDA, "mapped host allocation failed");
+  } else {
+    *h->sflag_host = 0ull;
+  }
+  if (s == BSF_OK) s = build_generic(h);
   if (s == BSF_OK) {
     std::string terr;
     const int trc = bsf::build_tiles(h->sh, h->tt, terr, h->dalloc());
@@ -353,6 +387,8 @@ bsf_status bsf_eval_all(bsf_handle h, const double* d_x, double* d_energy, doubl
   if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
   cudaError_t pe = cudaGetLastError();
   if (pe != cudaSuccess) return fail(BSF_E_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(pe));
+  if (bsf_status ss = take_singular(h)) return ss;
+  SflagScope sfs(h->sflag_dev);
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != h->device) cudaSetDevice(h->device);
@@ -395,6 +431,8 @@ static bsf_status eval_batch_impl(bsf_handle h, int nbatch, const double* d_x, i
     return fail(BSF_E_INVALID_ARG, "batch strides smaller than one item");
   cudaError_t pe = cudaGetLastError();
   if (pe != cudaSuccess) return fail(BSF_E_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(pe));
+  if (bsf_status ss = take_singular(h)) return ss;
+  SflagScope sfs(h->sflag_dev);
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != h->device) cudaSetDevice(h->device);
@@ -736,6 +774,19 @@ bsf_status bsf_assemble_hessian(bsf_handle h, const double* d_x, double* d_vals,
 
 int bsf_last_launch_count(bsf_handle h) { return h ? h->last_launches : 0; }
 
+bsf_status bsf_poll_status(bsf_handle h) {
+  if (!h) return fail(BSF_E_INVALID_ARG, "null handle");
+  return take_singular(h);
+}
+
+bsf_status bsf_affine_params(int n_u, int n_v, const double* rest_xy, const bsf_material* mat, double* out9) {
+  if (!rest_xy || !mat || !out9) return fail(BSF_E_INVALID_ARG, "null argument");
+  const double mu[4] = {mat->mu_st1, mat->mu_st2, mat->mu_sh, mat->mu_bd};
+  std::string err;
+  const int rc = bsf::affine_params(n_u, n_v, rest_xy, mu, out9, err);
+  return rc ? fail((bsf_status)rc, err) : BSF_OK;
+}
+
 bsf_status bsf_get_core_rect(bsf_handle h, int32_t* rect4) {
   if (!h || !rect4) return fail(BSF_E_INVALID_ARG, "null argument");
   const bool on = h->core_ok;
@@ -755,7 +806,16 @@ int nccl_comm_destroy(void* comm, std::string& err);
 int nccl_halo_exchange(double* d_x, int n_u, int r0, int r1, int xlo, int xhi, int rank, int nranks, void* comm,
                        void* stream, std::string& err);
 int nccl_allreduce_sum(double* d_buf, size_t n, void* comm, void* stream, std::string& err);
+void halo_plan(int n_u, int r0, int r1, int xlo, int xhi, int rank, int nranks, int64_t plan[8]);
 }  // namespace bsf
+
+extern "C" bsf_status bsf_halo_plan(bsf_handle h, int rank, int nranks, int64_t* plan8) {
+  if (!h || !plan8 || nranks < 1 || rank < 0 || rank >= nranks) return fail(BSF_E_INVALID_ARG, "bad plan arguments");
+  const bsf::Sheet& sh = h->sh;
+  if (nranks > 1 && sh.r1 - sh.r0 < 2) return fail(BSF_E_INVALID_ARG, "every slab must own at least 2 rows");
+  bsf::halo_plan(sh.n_u, sh.r0, sh.r1, sh.xlo, sh.xhi, rank, nranks, plan8);
+  return BSF_OK;
+}
 
 extern "C" bsf_status bsf_nccl_get_unique_id(void* out128) {
   if (!out128) return fail(BSF_E_INVALID_ARG, "null id buffer");
@@ -802,6 +862,8 @@ extern "C" bsf_status bsf_eval_all_slab(bsf_handle h, double* d_x, void* nccl_co
   const bool exchange = nranks > 1;
   if (exchange && !nccl_comm) return fail(BSF_E_INVALID_ARG, "null communicator");
   if (exchange && sh.r1 - sh.r0 < 2) return fail(BSF_E_INVALID_ARG, "every slab must own at least 2 rows");
+  if (bsf_status ss = take_singular(h)) return ss;
+  SflagScope sfs(h->sflag_dev);
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != h->device) cudaSetDevice(h->device);

@@ -56,6 +56,7 @@ struct BandArgs {
   const double* params;
   int n_u, xlo, xhi, r0;
   int project, flags, dbg;
+  unsigned long long* sflag;   // singular-stretch word (fbw.cuh)
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
   const double2* mcf;
   const int2* mcls;
@@ -237,6 +238,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
       const double a11 = wG00 * kc[0], a12 = wG00 * kc[1], a22 = wG01 * kc[1];
       const double b11 = wG10 * kc[2], b12 = wG10 * kc[3], b22 = wG11 * kc[3];
       const double c11 = wG00 * kc[2], c12 = wG00 * kc[3], c21 = wG01 * kc[2], c22 = wG01 * kc[3];
+      double i5 = 1.0;
       const double psi = fbw_emit(f1, f2, kc[5], kc[6], kc[7], A.project != 0, emit_p,
                                   [&](int r3, int c3, double A11, double A22, double A12rc, double A12cr) {
         const int e6 = sym3(r3, c3);
@@ -244,8 +246,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
         r[rec_pos(6 + e6)] = b11 * A11 + b12 * (A12rc + A12cr) + b22 * A22;
         r[rec_pos(12 + 3 * r3 + c3)] = c11 * A11 + c12 * A12rc + c21 * A12cr + c22 * A22;
         if (r3 != c3) r[rec_pos(12 + 3 * c3 + r3)] = c11 * A11 + c12 * A12cr + c21 * A12rc + c22 * A22;
-      });
-      if (own) e_acc += wq * psi;
+      }, &i5);
+      if (own) {
+        e_acc += wq * psi;
+        fbw_flag_singular(A.sflag, i5, item, axis ? od : oa, axis ? oa : od);
+      }
     } else {
       const double* l9 = lw + 9 * cls;
       double lap[3] = {0, 0, 0};
@@ -673,6 +678,7 @@ int band_eval(const BandTables& bt, const Sheet& sh, const double* d_x, int64_t 
   if (!bt.ok || bt.nctas == 0) return 0;
   static_assert(sizeof(BandArgs) <= 32000, "kernel parameter budget");
   BandArgs A;
+  A.sflag = call_sflag();
   A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride;
   A.epart = e_part; A.e_stride = e_stride; A.e_off = e_off;
   A.row_ptr = d_row_ptr; A.params = d_params;

@@ -55,6 +55,7 @@ struct CoreArgs {
   int CI0, CI1, RJ0, RJ1, nstrips, nchunks;
   int JA, JB;              // rows of this launch ([RJ0, RJ1) or a sub-range; addressing stays relative to RJ0)
   int project, flags, dbg;
+  unsigned long long* sflag;   // singular-stretch word (fbw.cuh)
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
   const double* tabs;      // device [104]: S[4][9][2] | LA[9] | LB[9] | LC[9] | what[5]
   double what[5];
@@ -243,6 +244,8 @@ struct PointCtx {
   int i0, i1, ja, jb;
   bool project;
   bool diagG;      // G01 == G10 == 0 (axis-aligned rest sheet): F, A~ and P~ by scaling
+  unsigned long long* sflag;
+  int item;
 };
 
 // Quadrature points of two consecutive knot rows q0, q0+1: item it in [0, 6 kKC) =
@@ -309,7 +312,7 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
     for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * cst[kCstP + 0] + Fv[c] * cst[kCstP + 2]; f2[c] = Fu[c] * cst[kCstP + 1] + Fv[c] * cst[kCstP + 3]; }
   }
   double* rec = row + set * kSetD + k;
-  double psi;
+  double psi, i5 = 1.0;
   // P~_mu = w sum_beta G_mu,beta P_beta;  A~_mu,nu = w sum_{beta,gamma} G_mu,beta G_nu,gamma A_beta,gamma,
   // streamed into the record as fbw_emit forms each F-space entry
   const auto emit_p = [&](int c, double P1c, double P2c) {
@@ -326,7 +329,7 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
       rec[(6 + e6) * kKH] = avv * A22;
       rec[(12 + 3 * r3 + c3) * kKH] = auv * A12rc;
       if (r3 != c3) rec[(12 + 3 * c3 + r3) * kKH] = auv * A12cr;
-    });
+    }, &i5);
   } else {
     psi = fbw_emit(f1, f2, cst[kCstP + 5], cst[kCstP + 6], cst[kCstP + 7], P.project, emit_p,
                    [&](int r3, int c3, double A11, double A22, double A12rc, double A12cr) {
@@ -338,9 +341,12 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
       rec[(12 + 3 * r3 + c3) * kKH] = wq * (G00 * G10 * A11 + G00 * G11 * A12rc + G01 * G10 * A12cr + G01 * G11 * A22);
       if (r3 != c3)
         rec[(12 + 3 * c3 + r3) * kKH] = wq * (G00 * G10 * A11 + G00 * G11 * A12cr + G01 * G10 * A12rc + G01 * G11 * A22);
-    });
+    }, &i5);
   }
-  if (s >= P.i0 && s < P.i1 && tq >= P.ja && tq < P.jb) return wq * psi;
+  if (s >= P.i0 && s < P.i1 && tq >= P.ja && tq < P.jb) {
+    fbw_flag_singular(P.sflag, i5, P.item, s, tq);
+    return wq * psi;
+  }
   return 0.0;
 }
 
@@ -378,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
     P.mubd = (A.flags & 4) ? 0.0 : pp[8];
   }
   P.i0 = i0; P.i1 = i1; P.ja = ja; P.jb = jb; P.project = A.project != 0;
+  P.sflag = A.sflag; P.item = item;
   P.diagG = (P.G01 == 0.0 && P.G10 == 0.0);
   const double cuu = P.G00 * P.G00 + P.G01 * P.G01, cvv = P.G10 * P.G10 + P.G11 * P.G11;
   const double cuv = 2.0 * (P.G00 * P.G10 + P.G01 * P.G11);
@@ -883,7 +890,7 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
   A.row_ptr = ct.row_ptr; A.rp_base = ct.rp_base; A.rp_stride = ct.rp_stride; A.params = d_params;
   A.n_u = sh.n_u; A.xlo = sh.xlo; A.xhi = sh.xhi; A.r0 = sh.r0;
   A.CI0 = ct.CI0; A.CI1 = ct.CI1; A.RJ0 = ct.RJ0; A.RJ1 = ct.RJ1; A.nstrips = ct.nstrips; A.nchunks = nchunks;
-  A.project = (flags & 1) ? 1 : 0; A.flags = flags;
+  A.project = (flags & 1) ? 1 : 0; A.flags = flags; A.sflag = call_sflag();
   {   // profiling switches (read once per process): 1 no points, 2 no gather, 4 no stores
     static const int dbg = getenv("BSF_CORE_DEBUG") ? atoi(getenv("BSF_CORE_DEBUG")) : 0;
     A.dbg = dbg;

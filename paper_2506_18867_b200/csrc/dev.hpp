@@ -31,7 +31,16 @@ struct GenericTables {
   uint32_t* g_inc = nullptr;       // packed (kind:1 | point:23 | la:4 | 0:4)
   double* e_part = nullptr;        // energy partial sums
   int e_nblocks = 0;
+  unsigned long long* sflag = nullptr;   // singular-stretch word of the call (set per launch)
 };
+
+// Singular-stretch word of the handle whose call is being enqueued (mapped host memory, device address;
+// fbw.cuh fbw_flag_singular).  Set by the C-ABI layer around each dispatch on the calling thread; every
+// launch function copies it into its kernel's arguments.
+inline unsigned long long*& call_sflag() {
+  static thread_local unsigned long long* p = nullptr;
+  return p;
+}
 
 constexpr uint32_t kIncBend = 1u << 31;
 inline __host__ __device__ uint32_t pack_inc(bool bend, uint32_t pt, uint32_t la, uint32_t lb) {

@@ -48,6 +48,7 @@ struct FrameArgs {
   int n_u, xlo, xhi, r0;
   int maxM, maxB;
   int project, flags, dbg;
+  unsigned long long* sflag;   // singular-stretch word (fbw.cuh)
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
   const int4* tile;
   const int32_t* tpm;
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_frame(const FrameArgs A) {
       double f1[3], f2[3];
 #pragma unroll
       for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * kc[0] + Fv[c] * kc[2]; f2[c] = Fu[c] * kc[1] + Fv[c] * kc[3]; }
-      double psi;
+      double psi, i5 = 1.0;
       const auto emit_p = [&](int c, double P1c, double P2c) {   // P~_mu = w sum_beta G_mu,beta P_beta
         rec[21 + c] = wq * (kc[0] * P1c + kc[1] * P2c);
         rec[24 + c] = wq * (kc[2] * P1c + kc[3] * P2c);
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_frame(const FrameArgs A) {
           rec[6 + e6] = avv * A22;
           rec[12 + 3 * r3 + c3] = auv * A12rc;
           if (r3 != c3) rec[12 + 3 * c3 + r3] = auv * A12cr;
-        });
+        }, &i5);
       } else {
         const double wG00 = wq * kc[0], wG01 = wq * kc[1], wG10 = wq * kc[2], wG11 = wq * kc[3];
         const double a11 = wG00 * kc[0], a12 = wG00 * kc[1], a22 = wG01 * kc[1];
@@ -180,9 +181,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_frame(const FrameArgs A) {
           rec[6 + e6] = b11 * A11 + b12 * (A12rc + A12cr) + b22 * A22;
           rec[12 + 3 * r3 + c3] = c11 * A11 + c12 * A12rc + c21 * A12cr + c22 * A22;
           if (r3 != c3) rec[12 + 3 * c3 + r3] = c11 * A11 + c12 * A12cr + c21 * A12rc + c22 * A22;
-        });
+        }, &i5);
       }
-      if (A.m_own[p]) e_acc += wq * psi;
+      if (A.m_own[p]) {
+        e_acc += wq * psi;
+        fbw_flag_singular(A.sflag, i5, item, an.x, an.y);
+      }
     } else {
       const int tb = t - M, q = b0 + tb;
       const int2 an = A.b_anc[q];
@@ -517,6 +521,7 @@ int frame_eval(const FrameTables& ft, const Sheet& sh, const double* d_x, int64_
                cudaStream_t st, const IpFused* ip) {
   if (ft.ntiles == 0) return 0;
   FrameArgs A;
+  A.sflag = call_sflag();
   A.xhat = ip ? ip->xhat : nullptr; A.xhs = ip ? ip->xhs : 0; A.mass = ip ? ip->mass : nullptr;
   A.ipk = ip ? ip->k : 0.0;
   for (int c = 0; c < 3; ++c) A.grav[c] = ip ? ip->grav[c] : 0.0;

@@ -49,7 +49,8 @@ struct G3Args {
   int64_t vs;
   double* epart;
   int64_t e_stride, e_off;
-  const int4* ctas;
+  const int4* ctas;       // frame CTAs: (i0, i1, ja, jb); interior: the strips (i0, i1, -, -)
+  int nch, uj0, uj1;       // interior: row chunks per strip and the interior rows [uj0, uj1)
   const int32_t* row_ptr;
   const double* params;
   const double* tabs;     // [2][kMaxCls * 27]
@@ -58,6 +59,7 @@ struct G3Args {
   const double* beta;
   int n_u, n_v, Su, Sv, r0, xlo, xhi, tlo, thi, cint_u, cint_v;
   int project, flags, dbg;
+  unsigned long long* sflag;   // singular-stretch word (fbw.cuh)
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
   double what[kNG];
 };
@@ -138,6 +140,7 @@ __device__ __forceinline__ double span_rows(const G3Args& A, const double* __res
       R[(21 + c) * kCS] = w * (G00 * P1c + G01 * P2c);
       R[(24 + c) * kCS] = w * (G10 * P1c + G11 * P2c);
     };
+    double i5 = 1.0;
     const double psi = fbw_emit(f1, f2, kc[kKMu], kc[kKMu + 1], kc[kKMu + 2], A.project != 0, emit_p,
                                 [&](int r3, int c3, double A11, double A22, double A12rc, double A12cr) {
       const int e6 = sym3(r3, c3);
@@ -147,12 +150,14 @@ __device__ __forceinline__ double span_rows(const G3Args& A, const double* __res
       R[(12 + 3 * r3 + c3) * kCS] = w * (G00 * G10 * A11 + G00 * G11 * A12rc + G01 * G10 * A12cr + G01 * G11 * A22);
       if (r3 != c3)
         R[(12 + 3 * c3 + r3) * kCS] = w * (G00 * G10 * A11 + G00 * G11 * A12cr + G01 * G10 * A12rc + G01 * G11 * A22);
-    });
+    }, &i5);
     const double wm = w * kc[kKMu + 3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) R[(27 + c) * kCS] = wm * lap[c];
-    if (s >= i0 && s < i1 && t >= ja && t < jb)
+    if (s >= i0 && s < i1 && t >= ja && t < jb) {
       e = w * psi + 0.5 * wm * (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
+      fbw_flag_singular(A.sflag, i5, blockIdx.y, s, t);
+    }
   }
   return e;
 }
@@ -183,8 +188,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_g3(const G3Args A) {
   double* kc = tab + 2 * kTabD;                // [kKN]
   double* red = kc + kKN;                      // [16]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int4 cta = A.ctas[blockIdx.x];
+  // interior CTAs derive their chunk from blockIdx.x and the launch's chunk count (nothing batch-size
+  // dependent lives in device memory, so graphs captured at any batch size replay correctly)
+  int4 cta;
+  if constexpr (UNI) {
+    const int s = blockIdx.x / A.nch, c = blockIdx.x - s * A.nch, rows = A.uj1 - A.uj0;
+    const int4 sp = A.ctas[s];
+    cta = make_int4(sp.x, sp.y, A.uj0 + ((rows * c / A.nch) & ~1),
+                    (c + 1 == A.nch) ? A.uj1 : A.uj0 + ((rows * (c + 1) / A.nch) & ~1));
+  } else {
+    cta = A.ctas[blockIdx.x];
+  }
   const int item = blockIdx.y;
+  if (cta.z >= cta.w) {   // empty chunk: its energy slot is still written
+    if (threadIdx.x == 0) A.epart[item * A.e_stride + A.e_off + blockIdx.x] = 0.0;
+    return;
+  }
   const int i0 = cta.x, i1 = cta.y, ja = cta.z, jb = cta.w;
   const double* __restrict__ x = A.x + item * A.xs;
   if (tid == 0) {
@@ -551,7 +570,7 @@ int build_g3(const Sheet& sh, G3Tables& gt, std::string& err, const std::functio
   double* d_tabs = nullptr;
   if (!upload_vec(dalloc, &d_tabs, tabs) || !upload_vec(dalloc, &gt.ucls, ucls) || !upload_vec(dalloc, &gt.vcls, vcls) ||
       !upload_vec(dalloc, &gt.beta, beta) || !upload_vec(dalloc, &gt.row_ptr, rp) ||
-      !upload_vec(dalloc, &gt.cta_gen, gt.h_gen)) {
+      !upload_vec(dalloc, &gt.cta_gen, gt.h_gen) || !upload_vec(dalloc, &gt.cta_uni, gt.h_uni_strips)) {
     err = "g3 tables: device allocation failed";
     return -7;
   }
@@ -571,35 +590,19 @@ int g3_eval(G3Tables& gt, const double* d_x, int64_t x_stride, const Mat& mat, i
             int* launches, const std::function<void*(size_t)>& dalloc) {
   int nl = 0;
   // interior row chunks for this batch size: minimise (waves of 1 CTA per SM) x (rows per chunk + 1 prologue
-  // step), chunks of >= 8 rows
-  if (!gt.h_uni_strips.empty() && gt.chunk_key != nbatch) {
+  // step), chunks of >= 8 rows.  The chunk count is a launch argument (no per-batch device list).
+  int nch = 1;
+  if (!gt.h_uni_strips.empty()) {
     const int rows = gt.uni_j1 - gt.uni_j0;
     const long long per = (long long)gt.h_uni_strips.size() * nbatch, gen = (long long)gt.n_gen * nbatch;
-    int best = 1;
     double bc = 1e300;
-    for (int nch = 1; nch <= std::max(1, rows / 8); ++nch) {
-      const long long waves = (per * nch + gen + 147) / 148;
-      const double cost = (double)waves * ((double)rows / nch + 2.0);
-      if (cost < bc - 1e-9) { bc = cost; best = nch; }
+    for (int c = 1; c <= std::max(1, rows / 8); ++c) {
+      const long long waves = (per * c + gen + 147) / 148;
+      const double cost = (double)waves * ((double)rows / c + 2.0);
+      if (cost < bc - 1e-9) { bc = cost; nch = c; }
     }
-    gt.h_uni.clear();
-    for (const int4& s : gt.h_uni_strips)
-      for (int c = 0; c < best; ++c) {
-        const int a = gt.uni_j0 + ((rows * c / best) & ~1), b = (c + 1 == best) ? gt.uni_j1 : gt.uni_j0 + ((rows * (c + 1) / best) & ~1);
-        if (b > a) gt.h_uni.push_back(make_int4(s.x, s.y, a, b));
-      }
-    if ((int)gt.h_uni.size() > gt.uni_cap) {
-      void* p = dalloc(sizeof(int4) * gt.h_uni.size());
-      if (!p) return -7;
-      gt.cta_uni = static_cast<int4*>(p);
-      gt.uni_cap = (int)gt.h_uni.size();
-    }
-    if (cudaMemcpyAsync(gt.cta_uni, gt.h_uni.data(), sizeof(int4) * gt.h_uni.size(), cudaMemcpyHostToDevice, st) !=
-        cudaSuccess)
-      return -6;
-    gt.n_uni = (int)gt.h_uni.size();
-    gt.chunk_key = nbatch;
   }
+  gt.n_uni = (int)gt.h_uni_strips.size() * nch;
   const int64_t nct = gt.n_uni + gt.n_gen;
   if ((int64_t)nbatch * nct > gt.e_cap) {
     void* p = dalloc(sizeof(double) * (size_t)nbatch * nct);
@@ -608,6 +611,7 @@ int g3_eval(G3Tables& gt, const double* d_x, int64_t x_stride, const Mat& mat, i
     gt.e_cap = (int64_t)nbatch * nct;
   }
   G3Args A;
+  A.sflag = call_sflag();
   A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride;
   A.epart = gt.e_part; A.e_stride = nct;
   A.row_ptr = gt.row_ptr; A.params = d_params; A.tabs = gt.d_tabs; A.ucls = gt.ucls; A.vcls = gt.vcls; A.beta = gt.beta;
@@ -630,7 +634,7 @@ int g3_eval(G3Tables& gt, const double* d_x, int64_t x_stride, const Mat& mat, i
     ++nl;
   }
   if (gt.n_uni > 0) {
-    A.ctas = gt.cta_uni; A.e_off = gt.n_gen;
+    A.ctas = gt.cta_uni; A.e_off = gt.n_gen; A.nch = nch; A.uj0 = gt.uni_j0; A.uj1 = gt.uni_j1;
     k_g3<true><<<dim3(gt.n_uni, nbatch), kThreads, gt.smem, st>>>(A);
     ++nl;
   }

@@ -36,14 +36,11 @@ struct G3Tables {
   int8_t* vcls = nullptr;          // device [Sv]: of each span row (-1 outside the slab window)
   double* beta = nullptr;          // device [9 x 9 cp classes][6][25]: parametric bending Hessian parts
   int32_t* row_ptr = nullptr;      // device [owned rows * n_u + 1]
-  int4* cta_uni = nullptr;         // device CTA lists (i0, i1, ja, jb): all spans interior / the rest
-  int4* cta_gen = nullptr;
+  int4* cta_uni = nullptr;         // device: interior strips (i0, i1, -, -), row chunks from the launch
+  int4* cta_gen = nullptr;         // device: frame CTAs (i0, i1, ja, jb)
   int n_uni = 0, n_gen = 0;
   std::vector<int4> h_uni_strips, h_gen;   // interior strips (rows chunked per call) and the frame CTAs
   int uni_j0 = 0, uni_j1 = 0;
-  int chunk_key = -1;              // nbatch the interior list was last chunked for
-  std::vector<int4> h_uni;
-  int uni_cap = 0;
   double* e_part = nullptr;        // energy partials [nbatch][n_uni + n_gen]
   int64_t e_cap = 0;
   size_t smem = 0;

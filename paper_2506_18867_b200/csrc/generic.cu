@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(128) k_membrane_points(GenericTables t, const 
   fbw_point(f1, f2, mat.mu_st1, mat.mu_st2, mat.mu_sh, project != 0, o);
   const double w = t.m_w[q];
   t.s_E[q] = t.m_eown[q] ? w * o.psi : 0.0;
+  if (t.m_eown[q]) fbw_flag_singular(t.sflag, o.i5min, 0, (int)(q & 0x3FFFFF), 0x3FFFFF);   // t field: point index marker
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     t.s_P[c * M + q] = w * o.P1[c];
@@ -162,6 +163,7 @@ int generic_eval(const GenericTables& t, const double* d_x, const Mat& mat, int 
   const bool proj = flags & 1, nomem = flags & 2, nobend = flags & 4;
   int nl = 0;
   GenericTables tt = t;
+  tt.sflag = call_sflag();
   Mat m = mat;
   if (nomem) { m.mu_st1 = m.mu_st2 = m.mu_sh = 0.0; }
   if (nobend) { m.mu_bd = 0.0; }

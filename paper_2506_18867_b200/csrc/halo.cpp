@@ -5,6 +5,7 @@
 // previous / next slab and receives their rows into the halo, all inside one NCCL group.
 #include <dlfcn.h>
 
+#include <cstdint>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -95,21 +96,36 @@ int nccl_comm_destroy(void* comm, std::string& err) {
   return a.commDestroy(comm) ? -8 : 0;
 }
 
-// rows: owned [r0, r1), buffer rows [xlo, xhi), n_u cps per row, 3 doubles per cp.
+// The exchange plan of a slab: rows owned [r0, r1), buffer rows [xlo, xhi), n_u cps per row,
+// 3 doubles per cp.  plan[4 d + 0..3] for d = 0 (peer rank-1, below) and d = 1 (peer rank+1, above):
+// peer rank (-1: none), send offset, receive offset, count — offsets and count in doubles of the buffer.
+// The slab sends its first / last nlo / nhi owned rows and receives the peer's into its halo rows.
+void halo_plan(int n_u, int r0, int r1, int xlo, int xhi, int rank, int nranks, int64_t plan[8]) {
+  const int64_t row = (int64_t)n_u * 3;
+  const int nlo = r0 - xlo, nhi = xhi - r1;   // halo rows below / above (0..2)
+  for (int k = 0; k < 8; ++k) plan[k] = 0;
+  plan[0] = plan[4] = -1;
+  if (rank > 0 && nlo > 0) {
+    plan[0] = rank - 1; plan[1] = (int64_t)(r0 - xlo) * row; plan[2] = 0; plan[3] = (int64_t)nlo * row;
+  }
+  if (rank < nranks - 1 && nhi > 0) {
+    plan[4] = rank + 1; plan[5] = (int64_t)(r1 - nhi - xlo) * row; plan[6] = (int64_t)(r1 - xlo) * row;
+    plan[7] = (int64_t)nhi * row;
+  }
+}
+
 int nccl_halo_exchange(double* d_x, int n_u, int r0, int r1, int xlo, int xhi, int rank, int nranks, void* comm,
                        void* stream, std::string& err) {
   const auto& a = bsf_nccl::api();
   if (!a.ok) { err = a.err; return -8; }
-  const size_t row = (size_t)n_u * 3;
-  const int nlo = r0 - xlo, nhi = xhi - r1;   // halo rows below / above (0..2)
+  int64_t plan[8];
+  halo_plan(n_u, r0, r1, xlo, xhi, rank, nranks, plan);
   int rc = a.groupStart();
-  if (rank > 0 && nlo > 0) {
-    rc |= a.send(d_x + (size_t)(r0 - xlo) * row, (size_t)nlo * row, kNcclFloat64, rank - 1, comm, stream);
-    rc |= a.recv(d_x, (size_t)nlo * row, kNcclFloat64, rank - 1, comm, stream);
-  }
-  if (rank < nranks - 1 && nhi > 0) {
-    rc |= a.send(d_x + (size_t)(r1 - nhi - xlo) * row, (size_t)nhi * row, kNcclFloat64, rank + 1, comm, stream);
-    rc |= a.recv(d_x + (size_t)(r1 - xlo) * row, (size_t)nhi * row, kNcclFloat64, rank + 1, comm, stream);
+  for (int d = 0; d < 2; ++d) {
+    const int64_t* p = plan + 4 * d;
+    if (p[0] < 0) continue;
+    rc |= a.send(d_x + p[1], (size_t)p[3], kNcclFloat64, (int)p[0], comm, stream);
+    rc |= a.recv(d_x + p[2], (size_t)p[3], kNcclFloat64, (int)p[0], comm, stream);
   }
   rc |= a.groupEnd();
   if (rc) { err = "NCCL halo exchange failed"; return -8; }

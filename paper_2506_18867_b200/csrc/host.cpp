@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <string>
 
 namespace bsf {
 
@@ -339,6 +340,57 @@ int build_sheet(int n_u, int n_v, const double* ku, const double* kv, const doub
   }
   sh.col_idx.resize(sh.row_ptr[nrows]);
   for (int a = 0; a < nrows; ++a) std::copy(cols[a].begin(), cols[a].end(), sh.col_idx.begin() + sh.row_ptr[a]);
+  return 0;
+}
+
+// Step a2 for a flat affine rest sheet (J = dX/d(u,v), G = J^-1, w = what det J): the rest
+// map evaluated at the centre of every knot span must have one constant J (to 1e-11 of |J|, the test
+// build_sheet applies) and vanishing second derivatives (no Laplacian coefficients c_u, c_v).  out[9] =
+// G00 G01 G10 G11 det J mu_st1 mu_st2 mu_sh mu_bd, the per-item layout of bsf_eval_all_batch_params.
+int affine_params(int n_u, int n_v, const double* rest_xy, const double mu[4], double out[9], std::string& err) {
+  if (n_u < 3 || n_v < 3) { err = "need at least 3 control points per direction"; return -3; }
+  const int Su = n_u - 2, Sv = n_v - 2;
+  double J0[2][2] = {{0, 0}, {0, 0}}, jn = 0.0;
+  for (int t = 0; t < Sv; ++t)
+    for (int s = 0; s < Su; ++s) {
+      Basis1 bu, bv;
+      basis1(Su, s + 0.5, bu);
+      basis1(Sv, t + 0.5, bv);
+      double Xu[2] = {0, 0}, Xv[2] = {0, 0}, X2[3][2] = {{0, 0}, {0, 0}, {0, 0}};
+      for (int jv = 0; jv < 3; ++jv)
+        for (int iu = 0; iu < 3; ++iu) {
+          const double* X = &rest_xy[2 * ((size_t)(bv.span + jv) * n_u + (bu.span + iu))];
+          for (int c = 0; c < 2; ++c) {
+            Xu[c] += bu.d1[iu] * bv.N[jv] * X[c];
+            Xv[c] += bu.N[iu] * bv.d1[jv] * X[c];
+            X2[0][c] += bu.d2[iu] * bv.N[jv] * X[c];
+            X2[1][c] += bu.N[iu] * bv.d2[jv] * X[c];
+            X2[2][c] += bu.d1[iu] * bv.d1[jv] * X[c];
+          }
+        }
+      const double det = Xu[0] * Xv[1] - Xv[0] * Xu[1];
+      if (!(det > 0.0)) {
+        err = "degenerate rest geometry: det(dX/d(u,v)) <= 0 in span (" + std::to_string(s) + ", " + std::to_string(t) + ")";
+        return -4;
+      }
+      if (s == 0 && t == 0) {
+        J0[0][0] = Xu[0]; J0[1][0] = Xu[1]; J0[0][1] = Xv[0]; J0[1][1] = Xv[1];
+        jn = std::fabs(Xu[0]) + std::fabs(Xu[1]) + std::fabs(Xv[0]) + std::fabs(Xv[1]);
+        continue;
+      }
+      bool ok = std::fabs(Xu[0] - J0[0][0]) <= 1e-11 * jn && std::fabs(Xu[1] - J0[1][0]) <= 1e-11 * jn &&
+                std::fabs(Xv[0] - J0[0][1]) <= 1e-11 * jn && std::fabs(Xv[1] - J0[1][1]) <= 1e-11 * jn;
+      for (int k = 0; k < 3 && ok; ++k) ok = std::fabs(X2[k][0]) + std::fabs(X2[k][1]) <= 1e-11 * jn;
+      if (!ok) {
+        err = "rest map is not affine (span (" + std::to_string(s) + ", " + std::to_string(t) + ") differs)";
+        return -1;
+      }
+    }
+  const double det = J0[0][0] * J0[1][1] - J0[0][1] * J0[1][0];
+  out[0] = J0[1][1] / det;  out[1] = -J0[0][1] / det;
+  out[2] = -J0[1][0] / det; out[3] = J0[0][0] / det;
+  out[4] = det;
+  for (int k = 0; k < 4; ++k) out[5 + k] = mu[k];
   return 0;
 }
 

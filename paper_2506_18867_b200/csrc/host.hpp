@@ -72,6 +72,10 @@ int build_sheet(int n_u, int n_v, const double* ku, const double* kv, const doub
 // m: [owned rows][n_u].  Returns 0 or -4 (det J <= 0 at a mass point, message in err).
 int lumped_mass(const Sheet& sh, double R0, std::vector<double>& m, std::string& err);
 
+// Per-item parameters of a flat affine rest sheet (step a2; bsf_affine_params): out[9] = G00 G01 G10 G11
+// det J mu[0..3].  Returns 0, -3 (too small), -4 (det J <= 0) or -1 (the rest map is not affine).
+int affine_params(int n_u, int n_v, const double* rest_xy, const double mu[4], double out[9], std::string& err);
+
 // Index helpers
 inline int win_entry(int iu, int jv) { return 3 * jv + iu; }
 

@@ -56,6 +56,7 @@ struct TileArgs {
   int n_u, n_v, Su, Sv, r0, r1, xlo, xhi;
   int capm, capb, nchunks_total, nstrips, chunk_base;
   int affine, project;
+  unsigned long long* sflag;   // singular-stretch word (fbw.cuh)
   double G00, G01, G10, G11, detJ;
   double mu1, mu2, mush, mubd;
   const int32_t* m_aoff;
@@ -234,8 +235,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
         FSpace o;
         fbw_point(f1, f2, pmu1, pmu2, pmush, A.project != 0, o);
         if (ou >= i0 && ou < i0 + kTX && t >= ra && t < rb &&
-            !(ou >= A.ex_i0 && ou < A.ex_i1 && t >= A.ex_j0 && t < A.ex_j1))
+            !(ou >= A.ex_i0 && ou < A.ex_i1 && t >= A.ex_j0 && t < A.ex_j1)) {
           e_acc += w * o.psi;
+          fbw_flag_singular(A.sflag, o.i5min, item, ou, t);
+        }
         // P~_mu = w sum_beta G_mu,beta P_beta
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -979,7 +982,7 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     if (need > tt.e_core_cap || core_slots != tt.core_ctas) {
       void* p = dalloc(need * sizeof(double));
       if (!p) return -7;
-      if (cudaMemset(p, 0, need * sizeof(double)) != cudaSuccess) return -6;
+      if (cudaMemsetAsync(p, 0, need * sizeof(double), st) != cudaSuccess) return -6;
       tt.e_part_core = static_cast<double*>(p);
       tt.e_core_cap = need;
       tt.core_ctas = core_slots;
@@ -996,6 +999,7 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     epart = tt.e_part;
   }
   TileArgs A;
+  A.sflag = call_sflag();
   A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride; A.epart = epart;
   A.e_stride = e_stride;
   A.n_u = tt.n_u; A.n_v = tt.n_v; A.Su = tt.Su; A.Sv = tt.Sv; A.r0 = tt.r0; A.r1 = tt.r1;

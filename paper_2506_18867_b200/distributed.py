@@ -29,16 +29,15 @@ def slab_bounds(n_v: int, world: int, edge_discount: int = 0):
         raise ValueError("edge_discount must be >= 0")
     base = n_v // world
     d = min(edge_discount, max(0, base - 2)) if world >= 3 else 0
-    sizes = [0] * world
-    sizes[0] = sizes[-1] = base - d
-    rest = n_v - 2 * (base - d)
-    mb, mx = divmod(rest, world - 2) if world >= 3 else (0, 0)
-    if world >= 3:
-        for k in range(1, world - 1):
-            sizes[k] = mb + (1 if k - 1 < mx else 0)
-    else:
+    if d == 0:   # balanced: the plain divmod split (slab sizes differ by at most one row)
         b2, e2 = divmod(n_v, world)
         sizes = [b2 + (1 if k < e2 else 0) for k in range(world)]
+    else:
+        sizes = [0] * world
+        sizes[0] = sizes[-1] = base - d
+        mb, mx = divmod(n_v - 2 * (base - d), world - 2)
+        for k in range(1, world - 1):
+            sizes[k] = mb + (1 if k - 1 < mx else 0)
     out, r = [], 0
     for n in sizes:
         out.append((r, r + n))
@@ -77,6 +76,24 @@ def torch_halo_exchange(x_local, r0: int, r1: int, n_v: int, rank: int, world: i
         ops.append(dist.P2POp(dist.isend, x_local[r1 - nhi - lo:r1 - lo].contiguous(), rank + 1, group))
         recv_hi = x_local[r1 - lo:r1 - lo + nhi]
         ops.append(dist.P2POp(dist.irecv, recv_hi, rank + 1, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return x_local
+
+
+def plan_halo_exchange(x_local, plan, group=None):
+    """Execute the LIBRARY's halo plan (bsf_halo_plan: [(peer, send_off, recv_off, count)] x 2, in doubles of the
+    position buffer) with torch.distributed point-to-point ops on any backend (gloo in the CPU tests; the NCCL
+    path executes the same plan inside bsf_halo_exchange)."""
+    import torch.distributed as dist
+    flat = x_local.view(-1)
+    ops = []
+    for peer, so, ro, n in plan:
+        if peer < 0 or n == 0:
+            continue
+        ops.append(dist.P2POp(dist.isend, flat[so:so + n].contiguous(), int(peer), group))
+        ops.append(dist.P2POp(dist.irecv, flat[ro:ro + n], int(peer), group))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
@@ -138,7 +155,7 @@ class SlabSheet:
         if self.world == 1:
             return
         if self.comm is None:
-            torch_halo_exchange(self.x, self.r0, self.r1, self.n_v, self.rank, self.world)
+            plan_halo_exchange(self.x, self.h.halo_plan(self.rank, self.world))
             return
         _check(lib().bsf_halo_exchange(self.h._h, C.c_void_p(self.x.data_ptr()), self.comm.comm, self.rank,
                                        self.world, _stream(stream)))

@@ -5,8 +5,9 @@ The step minimises the incremental potential (Eq. `eq:incremen
 with the paper's solver structure: the per-term PSD-projected Hessian (projected Newton), a linear solve for
 the search direction (here block-Jacobi PCG on the device instead of the paper's Cholesky), and a
 backtracking line search on the energy; it stops when the search direction is small.
-Every number is computed by the library's kernels (bsf_eval_ip_batch, bsf_pcg); this module only
-sequences the calls and reads back scalars.  Pinned control points (set_inertia(pinned=...)) stay fixed:
+Energies, gradients, Hessians and the linear solve come from the library's kernels (bsf_eval_ip_batch,
+bsf_pcg); this module sequences the calls and does the line search's vector updates (x + alpha d) and its
+scalar logic with plain torch operations on the device (SURVEY §8(f) #3 is a driver around the hot path).  Pinned control points (set_inertia(pinned=...)) stay fixed:
 their gradient rows are zero and their Hessian rows are identity, so the direction vanishes there.
 """
 from __future__ import annotations

@@ -30,13 +30,12 @@ GRAD_FLOOR = 1e-4
 def diag_block_norms(vals, row_ptr, col_idx, row_begin, n_u):
     """|H_aa|_F of the diagonal block of every (owned) block row."""
     vals = np.asarray(vals).reshape(-1, 9)
+    row_ptr, col_idx = np.asarray(row_ptr, np.int64), np.asarray(col_idx, np.int64)
     nrows = len(row_ptr) - 1
-    out = np.zeros(nrows)
-    for a in range(nrows):
-        lo, hi = row_ptr[a], row_ptr[a + 1]
-        k = lo + np.searchsorted(col_idx[lo:hi], a + row_begin * n_u)
-        out[a] = np.linalg.norm(vals[k])
-    return out
+    rows = np.repeat(np.arange(nrows, dtype=np.int64), np.diff(row_ptr))
+    k = np.flatnonzero(col_idx == rows + row_begin * n_u)   # one diagonal block per row, in row order
+    assert len(k) == nrows, "pattern without a diagonal block"
+    return np.linalg.norm(vals[k], axis=1)
 
 
 def rel_grad(g, gref, hdiag, cmax):

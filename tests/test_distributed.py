@@ -17,7 +17,8 @@ from paper_2506_18867_b200 import distributed as D
 
 
 def test_slab_bounds():
-    for n_v, world in [(16, 1), (16, 2), (16, 3), (128, 8), (1024, 8), (9, 4)]:
+    for n_v, world in [(16, 1), (16, 2), (16, 3), (128, 8), (1024, 8), (9, 4), (1024, 5), (11, 3), (1024, 7),
+                       (13, 6)]:
         b = D.partition_check(n_v, world)
         sizes = [r1 - r0 for r0, r1 in b]
         assert max(sizes) - min(sizes) <= 1
@@ -33,6 +34,9 @@ def test_slab_bounds_edge_discount():
         b = D.slab_bounds(n_v, world, d)
         assert b[0][0] == 0 and b[-1][1] == n_v and all(b[k][1] == b[k + 1][0] for k in range(world - 1))
         sizes = [r1 - r0 for r0, r1 in b]
+        if d == 0:   # no discount: the balanced split
+            assert b == D.slab_bounds(n_v, world)
+            continue
         assert min(sizes) >= 2 and sizes[0] == sizes[-1] <= min(sizes[1:-1])
         mid = sizes[1:-1]
         assert max(mid) - min(mid) <= 1
@@ -66,8 +70,14 @@ def _worker(rank, world, port, outdir, cfg):
         x = torch.from_numpy(D.numpy_slab(sh.x, r0, r1)).clone()
         x[: r0 - lo] = 0.0          # halos unknown before the exchange
         x[r1 - lo:] = 0.0
+        x2 = x.clone()
         D.torch_halo_exchange(x, r0, r1, sh.n_v, rank, world)
         halo_ok = bool(np.array_equal(x.numpy(), sh.x[lo:hi]))
+        # the library's own exchange plan (host-only handle of this slab; bsf_halo_plan), executed over gloo
+        import paper_2506_18867_b200 as B
+        hh = B.Sheet.from_sheet(sh, row_begin=r0, row_end=r1, device=-1)
+        D.plan_halo_exchange(x2, hh.halo_plan(rank, world))
+        halo_ok = halo_ok and bool(np.array_equal(x2.numpy(), sh.x[lo:hi]))
         o = O.Oracle.from_sheet(sh, r0=r0, r1=r1)
         E, g, v = o.eval(x.numpy(), flags=O.FLAG_PROJECT, threads=1)
         Et = torch.tensor([E], dtype=torch.float64)

@@ -157,6 +157,44 @@ def test_g3_cuda_graph_capture_and_replay():
     assert torch.equal(G, G2) and torch.equal(V, V2) and torch.equal(E, E2)
 
 
+def test_g3_graph_replay_after_other_batch_size():
+    """a graph captured at batch size A must replay correctly after a direct call at batch size B
+    (the interior row chunking differs between the two; nothing batch-size dependent lives in device memory)."""
+    n, A, Bn = 64, 2, 48
+    s = B.Sheet.from_sheet(W.make_sheet(n, 1.0, 50, n_modes=3, amp=5e-3), G3, G3)
+    mk = lambda seeds: torch.stack([torch.from_numpy(W.make_sheet(n, 1.0, k, n_modes=3, amp=5e-3).x)
+                                    for k in seeds]).cuda()
+    X = mk(range(60, 60 + A))
+    E = torch.zeros(A, dtype=torch.float64, device="cuda")
+    G = torch.zeros_like(X)
+    V = torch.zeros((A, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        s.eval_all_batch(X, E, G, V, B.PROJECT_PSD, st)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        s.eval_all_batch(X, E, G, V, B.PROJECT_PSD, st)
+    XB = mk([70 + (k % 5) for k in range(Bn)])   # direct call at another batch size between capture and replay
+    EB = torch.zeros(Bn, dtype=torch.float64, device="cuda")
+    VB = torch.zeros((Bn, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    s.eval_all_batch(XB, EB, None, VB, B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    X.copy_(mk(range(80, 80 + A)))
+    g.replay()
+    torch.cuda.synchronize()
+    E2, G2, V2 = torch.zeros_like(E), torch.zeros_like(G), torch.zeros_like(V)
+    s.eval_all_batch(X, E2, G2, V2, B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    assert torch.equal(G, G2) and torch.equal(V, V2) and torch.equal(E, E2)
+    # and the B-sized call itself is the per-item call
+    e1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    v1 = torch.zeros((1, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    s.eval_all_batch(XB[7:8].contiguous(), e1, None, v1, B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    assert torch.equal(v1[0], VB[7]) and torch.equal(e1[0], EB[7])
+
+
 @pytest.mark.parametrize("n,slab", [(5, None), (6, None), (40, (20, 22)), (40, (0, 2)), (40, (38, 40))])
 def test_g3_smallest_sheets_and_two_row_slabs(n, slab):
     """Edge cases: the smallest G3 sheets (S = 3, 4: every span is a boundary span, no interior class) and

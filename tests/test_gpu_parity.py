@@ -123,30 +123,26 @@ def test_deterministic_and_partial_outputs():
         assert s.last_launch_count() > 0
 
 
-def test_c4_full_size_sampled_rows():
-    """C4 (1024^2) in the bench's launch configuration; sampled block rows / gradient rows against
-    narrow oracle slabs, and the energy against the sum of GPU slab energies (a property that holds
-    at any size) plus one oracle slab energy."""
+def test_c4_full_size():
+    """C4 (1024^2, 1.04 M elements) in the bench's launch configuration against ONE full oracle evaluation:
+    the energy, every control point's gradient and every one of the 24.07 M Hessian blocks, pattern bit-exact
+    (no sampling); then the slab partition property: slab energies sum to the sheet's."""
     sh = W.make_c4()
     s = B.Sheet.from_sheet(sh)
     xd = torch.from_numpy(sh.x).cuda()
     E, g, v = s(xd, B.PROJECT_PSD)
     torch.cuda.synchronize()
-    rp, ci = s.pattern()
     g, v = g.cpu().numpy(), v.cpu().numpy()
     mu = O.material_from_young(sh.E, sh.nu, sh.h)
-    for r0, r1 in [(0, 2), (511, 513), (1022, 1024)]:
-        o = O.Oracle.from_sheet(sh, r0=r0, r1=r1, mu=mu)
-        Er, gr, vr = o.eval(sh.x, flags=O.FLAG_PROJECT)
-        orp, oci = o.pattern()
-        a0, a1 = r0 * sh.n_u, r1 * sh.n_u
-        assert np.array_equal(ci[rp[a0]:rp[a1]], oci)
-        va = o.eval(sh.x, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
-        assert_parity(None, g[r0:r1], v[rp[a0]:rp[a1]], None, gr, vr, what=f"C4 rows {r0}:{r1}",
-                      hdiag=diag_block_norms(vr, orp, oci, r0, sh.n_u), cmax=np.abs(sh.x).max(), vabs=va)
-        sl = B.Sheet.from_sheet(sh, row_begin=r0, row_end=r1)
-        El, _, _ = _gpu(sl, sh.x, B.PROJECT_PSD)
-        assert rel_energy(El, Er) <= TOL
+    o = O.Oracle.from_sheet(sh, mu=mu)
+    rp, ci = o.pattern()
+    assert np.array_equal(s.pattern()[0], rp) and np.array_equal(s.pattern()[1], ci)
+    assert len(ci) == 23 * 1022 ** 2 + 48 * 1022 + 8
+    Er, gr, vr = o.eval(sh.x, flags=O.FLAG_PROJECT)
+    hd = diag_block_norms(vr, rp, ci, 0, sh.n_u)
+    va = o.eval(sh.x, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
+    assert_parity(float(E.item()), g, v, Er, gr, vr, what="C4 full", hdiag=hd, cmax=np.abs(sh.x).max(), vabs=va)
+    del v, vr, va
     # energy: sum over a 4-slab partition equals the full-sheet energy
     parts = 0.0
     for r0, r1 in [(0, 256), (256, 512), (512, 768), (768, 1024)]:
@@ -178,11 +174,10 @@ def test_batch_matches_single_calls():
 
 
 def test_c2_bench_launch_100_states():
-    """C2 in exactly the bench's launch: the 100 seeded states of bench.workload("C2") in one
+    """C2 in exactly the bench's launch (bench.py secondary "C2_batched_100" / --config C2): the 100 seeded states in one
     bsf_eval_all_batch call (one long row chunk per core strip at this batch size).  Three items
     against the oracle; sampled items bit for bit against single-state calls (many short chunks)."""
-    import bench
-    sheets = bench.workload("C2", 100)
+    sheets = [W.make_c2(state=k) for k in range(100)]
     s = B.Sheet.from_sheet(sheets[0])
     X = torch.stack([torch.from_numpy(q.x) for q in sheets]).cuda()
     nb = len(sheets)
@@ -230,6 +225,52 @@ def test_slab_sheet_nccl_single_rank():
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+def _c5_launch(sheets, flags=B.PROJECT_PSD):
+    s = B.Sheet.from_sheet(sheets[0])
+    X = torch.stack([torch.from_numpy(q.x) for q in sheets]).cuda()
+    P = torch.from_numpy(np.stack([B.affine_params(q.rest_xy, B.material_from_young(q.E, q.nu, q.h))
+                                   for q in sheets])).cuda()
+    nb = len(sheets)
+    E = torch.zeros(nb, dtype=torch.float64, device="cuda")
+    G = torch.zeros((nb,) + tuple(X.shape[1:]), dtype=torch.float64, device="cuda")
+    V = torch.zeros((nb, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    s.eval_all_batch_params(X, P, E, G, V, flags)
+    torch.cuda.synchronize()
+    return s, E, G, V
+
+
+def _c5_item_vs_oracle(q, E, G, V, what):
+    o = O.Oracle.from_sheet(q)
+    Er, gr, vr = o.eval(q.x, flags=O.FLAG_PROJECT)
+    rp, ci = o.pattern()
+    va = o.eval(q.x, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
+    assert_parity(float(E), G.cpu().numpy(), V.cpu().numpy(), Er, gr, vr, what=what,
+                  hdiag=diag_block_norms(vr, rp, ci, 0, q.n_u), cmax=np.abs(q.x).max(), vabs=va)
+
+
+def test_c5_bench_launch_8_sheets_256():
+    """C5 at full size in the bench's launch (bench.py --config C5: the 8 sheets of rank 0, 256^2 each, per-sheet
+    L / E / nu, one bsf_eval_all_batch_params launch), every item against its own oracle."""
+    sheets = W.make_c5()[:8]
+    assert sheets[0].n_u == 256
+    s, E, G, V = _c5_launch(sheets)
+    for k, q in enumerate(sheets):
+        _c5_item_vs_oracle(q, E[k], G[k], V[k], f"C5 bench item {k}")
+
+
+def test_c5_all_64_sheets_one_launch():
+    """All 64 C5 sheets (256^2) in ONE launch: 8 sampled items against their own oracle, and the items shared
+    with the 8-sheet launch bit for bit (the per-row arithmetic does not depend on the launch size)."""
+    sheets = W.make_c5()
+    assert len(sheets) == 64
+    s, E, G, V = _c5_launch(sheets)
+    for k in (3, 9, 17, 26, 38, 45, 52, 63):
+        _c5_item_vs_oracle(sheets[k], E[k], G[k], V[k], f"C5 64-launch item {k}")
+    s8, E8, G8, V8 = _c5_launch(sheets[:8])
+    assert torch.equal(G[:8], G8) and torch.equal(V[:8], V8)
+    assert float(((E[:8] - E8).abs() / E8.abs()).max()) <= 1e-13
 
 
 def test_c5_style_batch_of_different_sheets():

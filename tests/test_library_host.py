@@ -120,3 +120,49 @@ def test_host_only_handle_refuses_every_compute_entry_point():
     assert s.lumped_mass().shape == (sh.n_v, sh.n_u)
     assert L.bsf_eval_ip_batch(s._h, 1, p, 0, p, 0, None, p, p, 0, p, 0, 0, None) == no_dev
     assert L.bsf_eval_ip_batch(s._h, 0, None, 0, None, 0, None, None, None, 0, None, 0, 0, None) == 0   # empty batch
+
+
+def test_affine_params_closed_form():
+    """bsf_affine_params (step a2 in the library) against the closed form of a Greville sheet:
+    X(u, v) = R diag(L_u/S_u, L_v/S_v) (u, v) + X0, so J = R diag(.), G = J^-1, det J = L_u L_v / (S_u S_v)."""
+    mu = B.Material(1.0, 2.0, 3.0, 4.0)
+    for n_u, n_v, Lu, Lv, th in [(16, 16, 1.0, 1.0, 0.0), (9, 23, 0.7, 2.5, 0.0), (40, 12, 1.3, 0.4, 0.61)]:
+        rest = W.greville_grid(n_u, n_v, Lu, Lv)
+        R = np.array([[np.cos(th), -np.sin(th)], [np.sin(th), np.cos(th)]])
+        rest = rest @ R.T + np.array([0.3, -1.1])
+        J = R @ np.diag([Lu / (n_u - 2), Lv / (n_v - 2)])
+        G = np.array([[J[1, 1], -J[0, 1]], [-J[1, 0], J[0, 0]]]) / (J[0, 0] * J[1, 1] - J[0, 1] * J[1, 0])
+        p = B.affine_params(rest, mu)
+        np.testing.assert_allclose(p[:4], G.ravel(), rtol=1e-12, atol=1e-12 * np.abs(G).max())
+        np.testing.assert_allclose(p[4], Lu * Lv / ((n_u - 2) * (n_v - 2)), rtol=1e-12)
+        np.testing.assert_array_equal(p[5:], [1.0, 2.0, 3.0, 4.0])
+    # a curved rest grid is not affine; a mirrored one has det J < 0
+    with pytest.raises(B.BsfError) as e:
+        B.affine_params(W.make_curved_rest(16, 16, 3), mu)
+    assert e.value.status == -1
+    with pytest.raises(B.BsfError) as e:
+        B.affine_params(W.greville_grid(16, 16, 1.0, 1.0)[:, ::-1].copy(), mu)
+    assert e.value.status == -4
+
+
+def test_binding_does_no_rest_arithmetic():
+    """The binding marshals arguments only: no inverse-map arithmetic on rest data."""
+    src = open(os.path.join(ROOT, "paper_2506_18867_b200", "__init__.py")).read()
+    assert "np.linalg" not in src and "rest_xy[" not in src and "inv(" not in src
+
+
+def test_halo_plan():
+    """bsf_halo_plan (the rows bsf_halo_exchange sends / receives), on host-only slab handles."""
+    n = 40
+    sh = W.make_sheet(n, 1.0, 0)
+    row = n * 3
+    mid = B.Sheet.from_sheet(sh, row_begin=10, row_end=20, device=-1)   # buffer rows [8, 22)
+    assert mid.halo_plan(1, 3) == [(0, 2 * row, 0, 2 * row), (2, 10 * row, 12 * row, 2 * row)]
+    first = B.Sheet.from_sheet(sh, row_begin=0, row_end=10, device=-1)   # buffer rows [0, 12)
+    assert first.halo_plan(0, 3) == [(-1, 0, 0, 0), (1, 8 * row, 10 * row, 2 * row)]
+    last = B.Sheet.from_sheet(sh, row_begin=20, row_end=40, device=-1)   # buffer rows [18, 40)
+    assert last.halo_plan(2, 3) == [(1, 2 * row, 0, 2 * row), (-1, 0, 0, 0)]
+    whole = B.Sheet.from_sheet(sh, device=-1)
+    assert whole.halo_plan(0, 1) == [(-1, 0, 0, 0), (-1, 0, 0, 0)]
+    with pytest.raises(B.BsfError):
+        B.Sheet.from_sheet(sh, row_begin=10, row_end=11, device=-1).halo_plan(1, 3)
