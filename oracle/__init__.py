@@ -17,7 +17,10 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "bsf_oracle.cpp")
-_LIB = os.path.join(_HERE, "liboracle.so")
+# BSF_ORACLE_SANITIZE=1: an AddressSanitizer + UBSan build (liboracle_asan.so; run the process with
+# LD_PRELOAD of libasan, see profiles/r02_sanitizers.md); otherwise the optimised build.
+_SANITIZE = os.environ.get("BSF_ORACLE_SANITIZE") == "1"
+_LIB = os.path.join(_HERE, "liboracle_asan.so" if _SANITIZE else "liboracle.so")
 _lock = threading.Lock()
 _lib = None
 
@@ -31,6 +34,9 @@ def build(force: bool = False) -> str:
         tmp = _LIB + f".tmp{os.getpid()}"
         cmd = ["g++", "-std=c++17", "-O3", "-march=native", "-fno-fast-math", "-fopenmp", "-fPIC",
                "-shared", "-o", tmp, _SRC]
+        if _SANITIZE:
+            cmd[2:3] = ["-O1", "-g", "-fsanitize=address,undefined", "-fno-sanitize-recover=undefined",
+                        "-fno-omit-frame-pointer"]
         subprocess.check_call(cmd)
         os.replace(tmp, _LIB)
     return _LIB
