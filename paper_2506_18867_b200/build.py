@@ -16,26 +16,33 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-re
          "-cudart", "static"] + os.environ.get("BSF_EXTRA_NVCC_FLAGS", "").split()
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+CHECKED_LIB = os.path.join(HERE, "libbsfem_checked.so")   # -DBSF_CHECKED (shared-memory poisoning)
+
+
+def _stale(lib=LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [__file__]
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    objdir = os.path.join(HERE, "build" + ("_" + os.path.basename(LIB).replace(".so", "") if "BSF_LIB_PATH" in os.environ else ""))
+def build(force: bool = False, verbose: bool = False, lib: str = LIB, extra=()) -> str:
+    if not force and not _stale(lib):
+        return lib
+    if os.path.abspath(lib) == CHECKED_LIB and "-DBSF_CHECKED" not in extra:
+        extra = list(extra) + ["-DBSF_CHECKED"]
+    flags = FLAGS + list(extra)
+    objdir = os.path.join(HERE, "build" + ("_" + os.path.basename(lib).replace(".so", "") if lib != os.path.join(
+        HERE, "libbsfem.so") else ""))
     os.makedirs(objdir, exist_ok=True)
     def compile_one(src):
         obj = os.path.join(objdir, src + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
         else:
-            cmd = [NVCC, *ARCH, *FLAGS, "-x", "c++", "-c", os.path.join(CSRC, src), "-o", obj]
+            cmd = [NVCC, *ARCH, *flags, "-x", "c++", "-c", os.path.join(CSRC, src), "-o", obj]
         return src, obj, subprocess.run(cmd, capture_output=True, text=True)
 
     from concurrent.futures import ThreadPoolExecutor
@@ -48,14 +55,19 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if verbose:
                 sys.stderr.write(r.stderr)
             objs.append(obj)
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-ldl", "-lpthread", "-lrt"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
+
+
+def build_checked(force: bool = False) -> str:
+    """The checked variant (-DBSF_CHECKED): every kernel poisons its shared memory with NaN first."""
+    return build(force=force, lib=CHECKED_LIB, extra=["-DBSF_CHECKED"])
 
 
 if __name__ == "__main__":

@@ -127,6 +127,7 @@ __device__ __forceinline__ void upd_mem(double (&acc)[kSl], const double2* cu, c
 
 __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
   extern __shared__ __align__(16) double bsm[];
+  BSF_POISON_SMEM(bsm);
   const int cta = blockIdx.x, item = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int band = 0;   // uniform (blockIdx and parameters only)
   while (band + 1 < A.nbands && cta >= A.cfirst[band + 1]) ++band;

@@ -82,7 +82,18 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-constexpr int kTma = kThreads - 32;   // bulk-store issuer: lane 0 of the last (point / gradient) warp
+// Bulk-store issuer: lane 0 of gather warp 0.  The issuing thread is the only one that can wait for the
+// store's shared-memory reads (bulk async-groups are per thread), and the gather warps are the ones that
+// overwrite the staging buffer, so the wait sits in a gather warp right before its staging stores (a point
+// warp there would couple the gather to the point phase).
+constexpr int kTma = 0;
+
+// Staged positions: per cp row, the strip's kPosC columns split by column parity ([even | odd] halves of
+// kPosH columns, 3 doubles each), so the lanes of a point set — consecutive knots of one parity, 2 columns
+// apart — read 3 doubles apart (an odd stride: no shared-memory bank conflicts).
+constexpr int kPosH = kPosC / 2;
+static_assert(kPosC % 2 == 0, "even staged column count");
+__device__ __forceinline__ int pos_col(int col) { return (col & 1) * kPosH + (col >> 1); }
 
 __device__ __forceinline__ int ring_slot(int q) { return (unsigned)(q + 7 * kRing) % kRing; }   // q >= -49
 
@@ -158,11 +169,9 @@ __device__ __forceinline__ void gather_grad(const uint32_t (&base0)[4], const ui
 
 template <int PI>
 __device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
-                                            const uint32_t (&base1)[4], const double* const (&bb0)[3],
-                                            const double* const (&bb1)[3], int o_rc, int o_cr,
-                                            int o_pu, int o_pv, bool diag, const double* __restrict__ cst,
-                                            double* st_lane, double* gdst, bool active, uint32_t bar,
-                                            uint32_t parity, double dshift) {
+                                            const uint32_t (&base1)[4], int o_rc, int o_cr, bool diag,
+                                            const double* __restrict__ cst, double* st_lane, bool active,
+                                            uint32_t bar, uint32_t parity, double dshift) {
   double acc[kNB];
 #pragma unroll
   for (int k = 0; k < kNB; ++k) acc[k] = 0.0;
@@ -174,26 +183,42 @@ __device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
     const uint32_t bu = (dp & 1) ? base1[dq + 2] : base0[dq + 2];   // shared byte address (+ role uu)
     const double auu = lds_f64<imm>(bu), avv = lds_f64<imm + 8 * 6 * kKH>(bu);
     const double arc = lds_f64<imm>(bu + o_rc), acr = lds_f64<imm>(bu + o_cr);
+    // (Yu, Yv) = dau (auu, arc) + dav (acr, avv), with the larger of dau, dav factored out into the block
+    // coefficients (compile-time constants): Y = f (Y1, Y2), one DFMA each instead of a DMUL + DFMA
     constexpr double dau = kSetTable.v[set][ea][0], dav = kSetTable.v[set][ea][1];
-    const double Yu = fma(dau, auu, dav * acr), Yv = fma(dau, arc, dav * avv);
+    constexpr bool FU = (dau < 0 ? -dau : dau) >= (dav < 0 ? -dav : dav);
+    constexpr double f = FU ? dau : dav, ra = FU ? dav / dau : dau / dav;
+    const double Y1 = FU ? fma(ra, acr, auu) : fma(ra, auu, acr);
+    const double Y2 = FU ? fma(ra, avv, arc) : fma(ra, arc, avv);
     static_for<T.s_c0[s], T.s_c0[s] + T.s_nc[s]>([&](auto CI) {
       constexpr int c = decltype(CI)::value;
       constexpr Template T2 = make_template(PI);
       constexpr int k = T2.c_blk[c], eb = T2.c_eb[c];
-      constexpr double bu = kSetTable.v[set][eb][0], bv = kSetTable.v[set][eb][1];
-      acc[k] = fma(bu, Yu, fma(bv, Yv, acc[k]));
+      constexpr double bu = kSetTable.v[set][eb][0] * f, bv = kSetTable.v[set][eb][1] * f;
+      acc[k] = fma(bu, Y1, fma(bv, Y2, acc[k]));
     });
   });
-  if (diag) {
+  if (diag) {   // the state-independent bending blocks beta_ab I3 (+ inertia m_a/dt^2)
 #pragma unroll
     for (int k = 0; k < kNB; ++k) acc[k] += cst[kCstBeta + k];
-    acc[block_index(0, 0)] += dshift;   // inertia m_a/dt^2 (0 without the incremental potential)
+    acc[block_index(0, 0)] += dshift;
   }
   if (!st_lane) return;
+  if (PI == 0 && threadIdx.x == kTma) {   // the previous step's bulk store has read the staging buffer
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(bar) : "memory");
+  }
   mbar_wait(bar, parity);
   if (!active) return;
+  // Lanes m and m + 8 of a half-warp are 8 control points (an even multiple of 207 doubles) apart, i.e. on the
+  // same bank: lanes 8-15 store block (k + 1) mod 23 when the others store block k (9 doubles further: an odd
+  // bank offset), so every store wavefront is conflict-free.
+  const bool rot = (threadIdx.x & 8) != 0;
 #pragma unroll
-  for (int k = 0; k < kNB; ++k) st_lane[k * 9] = acc[k];
+  for (int k = 0; k < kNB; ++k) {
+    const int k1 = (k + 1) % kNB;
+    st_lane[(rot ? k1 : k) * 9] = rot ? acc[k1] : acc[k];
+  }
 }
 
 // Stage the positions of cp rows [prow0, prow0 + nrows), cols [i0-3, i0+kW+3) (zero outside the array)
@@ -207,7 +232,8 @@ __device__ __forceinline__ void load_pos_async(double* pos, const double* __rest
     const int R = prow0 + row, Cc = i0 - 3 + col;
     const bool in = R >= A.xlo && R < A.xhi && Cc >= 0 && Cc < A.n_u;
     const double* src = in ? &x[((int64_t)(R - A.xlo) * A.n_u + Cc) * 3 + c] : x;
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(pos + k)), "l"(src),
+    double* dst = pos + (row * kPosC + pos_col(col)) * 3 + c;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src),
                  "r"(in ? 8 : 0)
                  : "memory");
   }
@@ -270,7 +296,7 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
         const int e = 3 * jv + iu;
         if (e == 8) continue;
         const double L = cst[kCstL + e];
-        const double* C = pos + ((q + jv - prow0) * kPosC + (p + iu - (P.i0 - 3))) * 3;
+        const double* C = pos + ((q + jv - prow0) * kPosC + pos_col(p + iu - (P.i0 - 3))) * 3;
         lap[0] = fma(L, C[0], lap[0]); lap[1] = fma(L, C[1], lap[1]); lap[2] = fma(L, C[2], lap[2]);
       }
     double* rec = row + 4 * kSetD + (lp & 1) * kBendD + (lp >> 1);
@@ -298,7 +324,7 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
     for (int iu = 0; iu < 3; ++iu) {
       const int e = 3 * jv + iu;
       const double du = Sset[2 * e], dv = Sset[2 * e + 1];
-      const double* C = pos + ((tq + jv - prow0) * kPosC + (s + iu - (P.i0 - 3))) * 3;
+      const double* C = pos + ((tq + jv - prow0) * kPosC + pos_col(s + iu - (P.i0 - 3))) * 3;
 #pragma unroll
       for (int c = 0; c < 3; ++c) { Fu[c] = fma(C[c], du, Fu[c]); Fv[c] = fma(C[c], dv, Fv[c]); }
     }
@@ -357,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
   double* stage = ring + kRing * kRowD;                  // [2][kStageRow]  (16-B aligned: kRing*kRowD even)
   double* posb = stage + 2 * kStageRow;                  // [kPosD]
   double* cst = posb + kPosD;                            // [kCstN]
+  BSF_POISON_SMEM(smem_raw);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(cst + kCstN);
   const int tid = threadIdx.x;
   CT_MARK(TK0);
@@ -418,15 +445,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
   }
 
   double e_acc = 0.0;
-  // ---- warp roles: warps 0-8 gather block entry (r, c) = (warp / 3, warp % 3) for both parities;
-  // warps 9-15 evaluate the quadrature points of the next step (7 x 30 lanes = the 210 points)
+  // ---- warp roles: warps 0-8 gather block entry (r, c) = (warp / 3, warp % 3) for both parities (warp 0,
+  // entry (0, 0), also waits for the bulk stores); warps 9-15 evaluate the quadrature points of the next step
+  // (7 x 30 lanes = the 210 points).  (Measured alternative, slower: one warp per entry pair (r,c) + (c,r) and
+  // parity, sharing the record loads (A~uu, A~vv symmetric, A~vu[rc] = A~uv[cr]); 46 accumulators per lane and
+  // twice the gather code: 705 vs 495 us on C4.  Also slower: a separate diagonal-role variant loading
+  // A~uv[rr] once, 562 us, from the register allocation of the extra instantiations.)
   const int warp = tid >> 5, lane = tid & 31;
   const int role = warp < kGatherWarps ? warp : 0;
   const int rr = role / 3, cc = role - 3 * (role / 3);
   const bool diag = rr == cc;
-  const int o_uu = sym3(rr, cc) * kKH, o_vv = (6 + sym3(rr, cc)) * kKH;
+  const int o_uu = sym3(rr, cc) * kKH;
   const int o_rc = (12 + 3 * rr + cc) * kKH, o_cr = (12 + 3 * cc + rr) * kKH;
-  const int o_pu = (21 + rr) * kKH, o_pv = (24 + rr) * kKH;
   const int h = lane >> 4, m = lane & 15;
   const int pw = warp - kGatherWarps;   // point warp index
 
@@ -445,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
         const int Cc = i0 - 3 + col;
         pm.row[e] = row;
         pm.off[e] = (Cc >= 0 && Cc < A.n_u) ? (row * A.n_u + col) * 3 + c : -1;
-        pm.dst[e] = kk * 8;
+        pm.dst[e] = ((row * kPosC + pos_col(col)) * 3 + c) * 8;
         pm.n = e + 1;
       }
     }
@@ -465,8 +495,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
         e_acc += eval_item(ring, posb + (mi & 1) * kPosStep, q0 - 1, cst, P, q0, pw * 30 + lane);
       CT_MARK(T1);
       if (k >= 0) {
-        // (b) the issuing thread releases the staging buffer once the previous bulk store has read it
-        if (tid == kTma) {
+        // (b) profiling mode without the gather: the issuing thread releases the staging buffer here (else the
+        // gather warp 0 does, right before its staging stores)
+        if (tid == kTma && (A.dbg & 6)) {
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(bar) : "memory");
         }
@@ -494,14 +525,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
               base0[d] = smem_u32(rowp[d]) + 8 * o_uu;
               base1[d] = base0[d] + 8 * sigma;
             }
-            const double* bb0[3];
-            const double* bb1[3];
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-              const double* rb = rowp[d] + 4 * kSetD + rr * kKH;
-              bb0[d] = rb + sigma * kBendD;
-              bb1[d] = rb + (1 - sigma) * kBendD + sigma;
-            }
             // staging: row h of the step; base parity matched to the global address (TMA needs equal
             // alignment mod 16 on both sides)
             double* st_lane = nullptr;
@@ -510,24 +533,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
               const int pad = (int)(((uintptr_t)(vals + g0) >> 3) & 1);
               st_lane = stage + h * kStageRow + pad + (i - i0) * (kNB * 9) + 3 * rr + cc;
             }
-            double* gdst = nullptr;
             const uint32_t par = k & 1;
             const double dshift = (IP && diag && active) ? ipk_m * A.mass[(int64_t)(jr - A.r0) * A.n_u + i] : 0.0;
-            if (PI == 0)
-              gather_role<0>(base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
-                             8 * (o_pv - o_uu), diag, cst, st_lane,
-                             gdst, active, bar, par, dshift);
-            else
-              gather_role<1>(base0, base1, bb0, bb1, 8 * (o_rc - o_uu), 8 * (o_cr - o_uu), 8 * (o_pu - o_uu),
-                             8 * (o_pv - o_uu), diag, cst, st_lane,
-                             gdst, active, bar, par, dshift);
+            const int orc = 8 * (o_rc - o_uu), ocr = 8 * (o_cr - o_uu);
+            if (PI == 0) gather_role<0>(base0, base1, orc, ocr, diag, cst, st_lane, active, bar, par, dshift);
+            else gather_role<1>(base0, base1, orc, ocr, diag, cst, st_lane, active, bar, par, dshift);
           }
         }
       }
-      // (c') gradient rows of step k: the last two point warps (bending-only point work) take the 6
-      // (parity, component) rounds
-      if (k >= 0 && (gout || IP) && warp >= kThreads / 32 - 2 && !(A.dbg & 2)) {
-        const int PI = warp - (kThreads / 32 - 2);
+      // (c') gradient rows of step k: six point warps take one (parity, component) round each
+      if (k >= 0 && (gout || IP) && warp >= kGatherWarps && warp < kGatherWarps + 6 && !(A.dbg & 2)) {
+        const int PI = (warp - kGatherWarps) / 3, rg = (warp - kGatherWarps) % 3;
         const int jr = j + h;
         const int sigma = (PI + jr + i0) & 1;
         const int i = i0 + 2 * m + sigma;
@@ -540,8 +556,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
             gb1[d] = gb0[d] + 8 * sigma;
             sl = (sl == kRing - 1) ? 0 : sl + 1;
           }
-#pragma unroll 1
-          for (int r = 0; r < 3; ++r) {
+          {
+            const int r = rg;
             const double* bb0[3];
             const double* bb1[3];
             int s2 = ring_slot(jr - 2);
@@ -857,15 +873,19 @@ int core_pick_chunks(const CoreTables& ct, int nbatch, int rows_override) {
   // row chunks per (strip, item): minimise (waves of 1 CTA per SM) x (rows per chunk + the 6-row prologue
   // of a chunk); chunks of >= 16 rows.  The band / corner kernels run beside k_core and fill a partial
   // last wave, so large batches prefer few long chunks and small ones many.
+  // experiment switches (read once): BSF_CORE_MINROWS (shortest chunk, rows), BSF_CORE_PROLOGUE (row cost of
+  // a chunk's prologue)
+  static const int min_rows = getenv("BSF_CORE_MINROWS") ? std::max(2, atoi(getenv("BSF_CORE_MINROWS"))) : 16;
+  static const double prologue = getenv("BSF_CORE_PROLOGUE") ? atof(getenv("BSF_CORE_PROLOGUE")) : 6.0;
   const int rows = rows_override >= 0 ? rows_override : ct.RJ1 - ct.RJ0;
   const int per = std::max(1, ct.nstrips * std::max(1, nbatch));
-  const int maxch = std::max(1, rows / 16);
+  const int maxch = std::max(1, rows / min_rows);
   int best = 1;
   double bcost = 1e300;
   for (int nch = 1; nch <= maxch; ++nch) {
     const long long nctas = (long long)per * nch;
     const long long waves = (nctas + 147) / 148;
-    const double cost = (double)waves * ((double)rows / nch + 6.0);
+    const double cost = (double)waves * ((double)rows / nch + prologue);
     if (cost < bcost - 1e-9) { bcost = cost; best = nch; }
   }
   return best;

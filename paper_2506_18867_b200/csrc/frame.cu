@@ -83,6 +83,7 @@ constexpr int kBRec = 13;           // 12 bending channels + pad
 
 __global__ void __launch_bounds__(kThreads, 3) k_frame(const FrameArgs A) {
   extern __shared__ __align__(16) double fsm[];
+  BSF_POISON_SMEM(fsm);
   const int tile = blockIdx.x, item = blockIdx.y, tid = threadIdx.x;
   const int4 ti = A.tile[tile];
   const int i0 = ti.x, j0 = ti.y, tw = ti.z & 255, th = ti.z >> 8, ncp = ti.w;

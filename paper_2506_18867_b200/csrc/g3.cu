@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_g3(const G3Args A) {
     if (threadIdx.x == 0) A.epart[item * A.e_stride + A.e_off + blockIdx.x] = 0.0;
     return;
   }
+  BSF_POISON_SMEM(sm);
   const int i0 = cta.x, i1 = cta.y, ja = cta.z, jb = cta.w;
   const double* __restrict__ x = A.x + item * A.xs;
   if (tid == 0) {

@@ -112,6 +112,7 @@ __device__ __forceinline__ void warp_store_block(double* wb, const double (&blk)
 
 __global__ void __launch_bounds__(kThreads, 2) k_tile(const TileArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  BSF_POISON_SMEM(smem_raw);
   const int tid = threadIdx.x;
   int strip = blockIdx.x, cl = blockIdx.y;
   if (A.work) { const int2 w = A.work[blockIdx.x]; strip = w.x; cl = w.y; }
