@@ -79,6 +79,8 @@ struct bsf_sheet {
     cudaSetDevice(device);
     if (sflag_host) cudaFreeHost(sflag_host);
     if (tt.side) cudaStreamDestroy(tt.side);
+    if (tt.side2) cudaStreamDestroy(tt.side2);
+    if (tt.ev_join2) cudaEventDestroy(tt.ev_join2);
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ev_copy) cudaEventDestroy(ev_copy);
     if (ev_start) cudaEventDestroy(ev_start);

@@ -869,16 +869,28 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
 
 int core_ctas_per_item(const CoreTables& ct, int nchunks) { return ct.nstrips * nchunks; }
 
-int core_pick_chunks(const CoreTables& ct, int nbatch, int rows_override) {
+int core_pick_chunks(const CoreTables& ct, int nbatch, int rows_override, int reserved_sms) {
   // row chunks per (strip, item): minimise (waves of 1 CTA per SM) x (rows per chunk + the 6-row prologue
   // of a chunk); chunks of >= 16 rows.  The band / corner kernels run beside k_core and fill a partial
   // last wave, so large batches prefer few long chunks and small ones many.
+  // Small problems (one strip row of CTAs fits beside the band / corner kernels, e.g. one C2 or C3 sheet): the
+  // most chunks that still run in ONE wave on the SMs the band / corner kernels leave free, chunks of >= 6
+  // rows (measured on C2 / C3: more chunks starve the band kernel, shorter chunks pay the prologue again).
+  static const int nsm = [] {
+    int d = 0, n = 0;
+    cudaGetDevice(&d);
+    return cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) == cudaSuccess && n > 0 ? n : 148;
+  }();
   // experiment switches (read once): BSF_CORE_MINROWS (shortest chunk, rows), BSF_CORE_PROLOGUE (row cost of
   // a chunk's prologue)
   static const int min_rows = getenv("BSF_CORE_MINROWS") ? std::max(2, atoi(getenv("BSF_CORE_MINROWS"))) : 16;
   static const double prologue = getenv("BSF_CORE_PROLOGUE") ? atof(getenv("BSF_CORE_PROLOGUE")) : 6.0;
+  static const int force_nch = getenv("BSF_CORE_NCH") ? atoi(getenv("BSF_CORE_NCH")) : 0;
+  if (force_nch > 0) return std::min(force_nch, std::max(1, (rows_override >= 0 ? rows_override : ct.RJ1 - ct.RJ0) / 2));
   const int rows = rows_override >= 0 ? rows_override : ct.RJ1 - ct.RJ0;
   const int per = std::max(1, ct.nstrips * std::max(1, nbatch));
+  if (reserved_sms > 0 && per <= 16 && per + reserved_sms < nsm)
+    return std::max(1, std::min((nsm - reserved_sms) / per, rows / 6));
   const int maxch = std::max(1, rows / min_rows);
   int best = 1;
   double bcost = 1e300;

@@ -168,6 +168,8 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
               cudaStream_t st, const struct IpFused* ip = nullptr, int row_begin = -1, int row_end = -1);
 
 int core_ctas_per_item(const CoreTables& ct, int nchunks);
-int core_pick_chunks(const CoreTables& ct, int nbatch, int rows = -1);
+// Row chunks per (strip, item).  reserved_sms: SMs the band / corner kernels beside k_core occupy (a small
+// problem runs one wave of k_core next to them).
+int core_pick_chunks(const CoreTables& ct, int nbatch, int rows = -1, int reserved_sms = 0);
 
 }  // namespace bsf

@@ -903,7 +903,11 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     // halo overlap: the interior core rows [ja, jb) first (own chunking), then the two boundary row
     // ranges with one chunk each; energy slots [frame tiles | band CTAs | core CTAs of each launch]
     const bool ov = halo && halo->jb > halo->ja && halo->ja >= ct->RJ0 && halo->jb <= ct->RJ1;
-    const int core_nch = ov ? core_pick_chunks(*ct, nbatch, halo->jb - halo->ja) : core_pick_chunks(*ct, nbatch);
+    // SMs held by the band (2 CTAs per SM) and corner kernels running beside k_core
+    const int reserved = (int)std::min<int64_t>(1 << 20, ((int64_t)ft->band.nctas * nbatch + 1) / 2 +
+                                                            (int64_t)ft->ntiles * nbatch);
+    const int core_nch = ov ? core_pick_chunks(*ct, nbatch, halo->jb - halo->ja, reserved)
+                            : core_pick_chunks(*ct, nbatch, -1, reserved);
     const int64_t nfb = ft->ntiles + ft->band.nctas;   // energy slots: [frame tiles | band CTAs | core CTAs]
     const int64_t nb_lo = (ov && halo->ja > ct->RJ0) ? core_ctas_per_item(*ct, 1) : 0;   // boundary launches
     const int64_t nb_hi = (ov && halo->jb < ct->RJ1) ? core_ctas_per_item(*ct, 1) : 0;
@@ -919,8 +923,10 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     // (event fork-join, CUDA-graph capturable)
     if (!tt.side) {
       if (cudaStreamCreateWithFlags(&tt.side, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaStreamCreateWithFlags(&tt.side2, cudaStreamNonBlocking) != cudaSuccess ||
           cudaEventCreateWithFlags(&tt.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-          cudaEventCreateWithFlags(&tt.ev_join, cudaEventDisableTiming) != cudaSuccess)
+          cudaEventCreateWithFlags(&tt.ev_join, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&tt.ev_join2, cudaEventDisableTiming) != cudaSuccess)
         return -6;
     }
     int rc = 0;
@@ -930,10 +936,16 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
       if (rc) return rc;
       if (cudaStreamWaitEvent(st, halo->ready, 0) != cudaSuccess) return -6;
     }
-    if (cudaEventRecord(tt.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(tt.side, tt.ev_fork, 0) != cudaSuccess)
+    // corners (k_frame) and bands (k_band) run beside the core on side streams.  Small problems (a few core
+    // strips: one C2 / C3 sheet) put them on two streams, since the three kernels have similar latencies;
+    // large ones queue the corners before the bands on one stream (fewer SMs held back from k_core at its start)
+    const bool small = (int64_t)ct->nstrips * nbatch <= 16;
+    cudaStream_t fst = small ? tt.side2 : tt.side;
+    if (cudaEventRecord(tt.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(tt.side, tt.ev_fork, 0) != cudaSuccess ||
+        (small && cudaStreamWaitEvent(tt.side2, tt.ev_fork, 0) != cudaSuccess))
       return -6;
     rc = frame_eval(*ft, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
-                        tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, tt.side, ip);
+                        tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, fst, ip);
     if (rc) return rc;
     cudaEvent_t* tv = nullptr;   // [core start, core end, band start, band end] of this call
     if (tt.tev_n > 0) {
@@ -960,6 +972,9 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     if (rc) return rc;
     if (tv && cudaEventRecord(tv[1], st) != cudaSuccess) return -6;
     if (cudaEventRecord(tt.ev_join, tt.side) != cudaSuccess || cudaStreamWaitEvent(st, tt.ev_join, 0) != cudaSuccess)
+      return -6;
+    if (small && (cudaEventRecord(tt.ev_join2, tt.side2) != cudaSuccess ||
+                  cudaStreamWaitEvent(st, tt.ev_join2, 0) != cudaSuccess))
       return -6;
     int nl = 1 + (ft->ntiles > 0) + (ft->band.ok && ft->band.nctas > 0);
     if (d_E) {

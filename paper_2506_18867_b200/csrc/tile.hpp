@@ -59,8 +59,9 @@ struct TileTables {
   int core_nchunks = 0;
   double* e_part_core = nullptr;   // [item][tile slots | core slots], tile slots of dropped pairs stay 0
   int64_t e_core_cap = 0;
-  cudaStream_t side = nullptr;     // frame kernel stream (fork / join with the caller's stream)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t side = nullptr;     // band kernel stream (fork / join with the caller's stream)
+  cudaStream_t side2 = nullptr;    // corner (frame) kernel stream: runs beside the band and core kernels
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
   // live per-kernel timing (bsf_set_kernel_timing): per call, event pairs around the core launch (caller's
   // stream) and the band launch (side stream), in a ring of tev_n calls
   std::vector<cudaEvent_t> tev;

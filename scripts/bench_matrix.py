@@ -11,7 +11,11 @@ rules, G3-FULL}, one B200, device-resident inputs, CUDA events around K back-to-
 Per row: ms per call, elements/s, algorithmic bytes per call (24 N_cp + 24 N_cp + 72 nnzb + 8
 per sheet) / time as a fraction of the measured HBM copy peak.  G3-FULL rows are FP64-bound:
 their fraction is also given against the FP64 peak measured by scripts/ubench/fp64 when its JSON is passed.
-usage: python scripts/bench_matrix.py [out.json] [fp64.json]
+Round 2 groups: "g2" = the G2-INTERIOR rule (the paper's ablation (A), 2x2 Gauss on the
+interior spans) beside the reduced rule (B) on C2 and C4; "curved" = a non-affine (curved)
+rest grid of C2 and C4 size on the general path, whose per-point rest tables (G, w: 40 B per membrane point; w and
+the five Laplacian coefficients: 48 B per bending point) are counted as extra algorithmic bytes.
+usage: python scripts/bench_matrix.py [out.json] [fp64.json] [groups: base,g2,curved]
 """
 import json
 import os
@@ -27,7 +31,8 @@ import paper_2506_18867_b200 as B
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HBM = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
-FP64 = json.load(open(sys.argv[2]))["fp64_tflops"] if len(sys.argv) > 2 else None
+FP64 = json.load(open(sys.argv[2]))["fp64_tflops"] if len(sys.argv) > 2 and sys.argv[2] != "-" else None
+GROUPS = (sys.argv[3] if len(sys.argv) > 3 else "base").split(",")
 
 
 def alg_bytes(n_cp, nnzb):
@@ -41,7 +46,7 @@ def g3_flops_per_call(n_cp, n_u, n_v):
     return 9 * S2 * (24 * 9 + 194 + 76 * 45) + 9 * S2 * (10 * 9 + 6 + 4 * 45)
 
 
-def run(name, sheets, rule, flags, steps=10, warmup=3, params=None):
+def run(name, sheets, rule, flags, steps=10, warmup=3, params=None, tables=False):
     s = B.Sheet.from_sheet(sheets[0], rule, rule)
     nb = len(sheets)
     X = torch.stack([torch.from_numpy(q.x) for q in sheets]).cuda()
@@ -74,11 +79,16 @@ def run(name, sheets, rule, flags, steps=10, warmup=3, params=None):
     n_cp = q.n_u * q.n_v
     el = (q.n_u - 2) * (q.n_v - 2) * nb
     byt = alg_bytes(n_cp, s.nnzb) * nb
-    row = {"config": name, "rule": "reduced" if rule == B.RULE_REDUCED else "g3_full",
+    tb = (40 * s.n_membrane + 48 * s.n_bending) * nb if tables else 0
+    rule_name = {B.RULE_REDUCED: "reduced", B.RULE_G2_INTERIOR: "g2_interior", B.RULE_G3_FULL: "g3_full"}[rule]
+    row = {"config": name, "rule": rule_name,
            "flags": "psd" if flags & B.PROJECT_PSD else "exact", "sheets": nb, "ms_per_call": round(ms, 4),
            "elements_per_s": el / ms * 1e3, "alg_bytes": byt, "hbm_frac": byt / (ms * 1e-3) / (HBM * 1e9),
-           "launches": s.last_launch_count(), "core": s.core_rect() is not None}
-    if rule != B.RULE_REDUCED:
+           "launches": s.last_launch_count(), "core": s.core_rect()[1] > 0}
+    if tables:
+        row["table_bytes"] = tb
+        row["hbm_frac_with_tables"] = (byt + tb) / (ms * 1e-3) / (HBM * 1e9)
+    if rule == B.RULE_G3_FULL:
         fl = g3_flops_per_call(n_cp, q.n_u, q.n_v) * nb
         row["model_gflop"] = fl / 1e9
         if FP64:
@@ -99,14 +109,32 @@ def main():
              ("C3", [W.make_c3(1e5)], None),
              ("C4", [W.make_c4()], None),
              ("C5", c5, c5p)]
-    for name, sheets, params in cases:
-        for rule in (B.RULE_REDUCED, B.RULE_G3_FULL):
-            for flags in (B.PROJECT_PSD, 0):
+
+    def emit(r, t0):
+        r["wall_s"] = round(time.time() - t0, 1)
+        print(json.dumps(r), flush=True)
+        rows.append(r)
+    if "base" in GROUPS:
+        for name, sheets, params in cases:
+            for rule in (B.RULE_REDUCED, B.RULE_G3_FULL):
+                for flags in (B.PROJECT_PSD, 0):
+                    t0 = time.time()
+                    emit(run(name, sheets, rule, flags, params=params), t0)
+    if "g2" in GROUPS:   # ablation (A) G2-INTERIOR vs (B) reduced
+        for name, sheets, params in (cases[1], cases[3]):
+            for rule in (B.RULE_G2_INTERIOR, B.RULE_REDUCED):
                 t0 = time.time()
-                r = run(name, sheets, rule, flags, params=params)
-                r["wall_s"] = round(time.time() - t0, 1)
-                print(json.dumps(r), flush=True)
-                rows.append(r)
+                emit(run(name, sheets, rule, B.PROJECT_PSD), t0)
+    if "curved" in GROUPS:   # non-affine rest grids on the general path (per-point rest tables)
+        for name, n, nst in (("C2-curved", 128, 100), ("C4-curved", 1024, 1)):
+            rest = W.make_curved_rest(n, n, seed=7)
+            ku = W.open_uniform_knots(n)
+            rng = np.random.default_rng(11)
+            base = np.concatenate([rest, np.zeros((n, n, 1))], -1)
+            sheets = [W.Sheet(n, n, ku, ku, rest, base * 1.01 + rng.normal(0, 1e-3 / n * 16, (n, n, 3)), 1e5, 0.3, 3e-4)
+                      for _ in range(nst)]
+            t0 = time.time()
+            emit(run(name, sheets, B.RULE_REDUCED, B.PROJECT_PSD, tables=True), t0)
     if out:
         with open(out, "w") as f:
             json.dump({"hbm_gbs": HBM, "fp64_tflops": FP64, "rows": rows}, f, indent=1)

@@ -12,6 +12,9 @@ import paper_2506_18867_b200 as B  # noqa: E402
 import workloads as W  # noqa: E402
 
 
+FLAGS = B.PROJECT_PSD | (B.TILE_ONLY if os.environ.get("PROBE_TILE") else 0)
+
+
 def probe(sh, n=50, tag=""):
     h = B.Sheet.from_sheet(sh)
     x = torch.from_numpy(sh.x).cuda()
@@ -19,19 +22,19 @@ def probe(sh, n=50, tag=""):
     st = torch.cuda.Stream()
     with torch.cuda.stream(st):
         for k in range(3):
-            h.eval_all(x, *outs[k % 4], B.PROJECT_PSD, st)
+            h.eval_all(x, *outs[k % 4], FLAGS, st)
         torch.cuda.synchronize()
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         t0.record(st)
         for k in range(n):
-            h.eval_all(x, *outs[k % 4], B.PROJECT_PSD, st)
+            h.eval_all(x, *outs[k % 4], FLAGS, st)
         t1.record(st)
         torch.cuda.synchronize()
         direct = t0.elapsed_time(t1) / n
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=st):
             for k in range(n):
-                h.eval_all(x, *outs[k % 4], B.PROJECT_PSD, st)
+                h.eval_all(x, *outs[k % 4], FLAGS, st)
         g.replay()
         torch.cuda.synchronize()
         t0.record(st)
@@ -42,7 +45,7 @@ def probe(sh, n=50, tag=""):
     h.set_kernel_timing(n)
     with torch.cuda.stream(st):
         for k in range(n):
-            h.eval_all(x, *outs[k % 4], B.PROJECT_PSD, st)
+            h.eval_all(x, *outs[k % 4], FLAGS, st)
     torch.cuda.synchronize()
     c, b = h.kernel_timing(n)
     h.set_kernel_timing(0)
@@ -51,6 +54,6 @@ def probe(sh, n=50, tag=""):
             "core": h.core_rect(), "k_core_us": statistics.median(c) * 1e3, "k_band_us": statistics.median(b) * 1e3}
 
 
-env = {k: os.environ.get(k) for k in ("BSF_CORE_MINROWS", "BSF_CORE_PROLOGUE")}
+env = {k: os.environ.get(k) for k in ("BSF_CORE_MINROWS", "BSF_CORE_PROLOGUE", "PROBE_TILE")}
 for name, sh in (("C2", W.make_c2(state=0)), ("C3", W.make_c3())):
     print(json.dumps({"env": env, **probe(sh, tag=name)}), flush=True)

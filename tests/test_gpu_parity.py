@@ -152,7 +152,9 @@ def test_c4_full_size():
 
 
 def test_batch_matches_single_calls():
-    """bsf_eval_all_batch over several C2 states equals per-state calls bit for bit, and the oracle."""
+    """bsf_eval_all_batch over several C2 states equals per-state calls bit for bit (gradient, Hessian; the energy to
+    rounding: its per-CTA partial sums follow the launch's row chunking, which depends on the batch size), and the
+    oracle."""
     sheets = [W.make_c2(state=k) for k in (0, 7, 42)]
     s = B.Sheet.from_sheet(sheets[0])
     X = torch.stack([torch.from_numpy(q.x) for q in sheets]).cuda()
@@ -164,7 +166,8 @@ def test_batch_matches_single_calls():
         s.eval_all_batch(X, E, G, V, B.PROJECT_PSD | path)
         for k in range(nb):
             E1, g1, v1 = s(X[k].contiguous(), B.PROJECT_PSD | path)
-            assert torch.equal(E1[0], E[k]) and torch.equal(g1, G[k]) and torch.equal(v1, V[k])
+            assert torch.equal(g1, G[k]) and torch.equal(v1, V[k])
+            assert rel_energy(float(E1[0]), float(E[k])) <= 1e-13
     o = O.Oracle.from_sheet(sheets[1])
     Er, gr, vr = o.eval(sheets[1].x, flags=O.FLAG_PROJECT)
     rp, ci = o.pattern()
