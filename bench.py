@@ -354,13 +354,35 @@ def bench_c4(args, rank, world, local_rank):
         slab.assemble(flags, stream)
     torch.cuda.synchronize()
     launches = slab.h.last_launch_count()
-    core_timed = not (flags & B.GENERIC_PATH) and slab.h.core_rect()[1] > 0
+    # N > 1: the step (halo exchange on the library's NCCL communicator, the slab's kernels, the energy
+    # all-reduce) is captured once into a CUDA graph and replayed, so the ~10 host launches per step do not pace
+    # a ~70 us step; any capture failure falls back to direct calls (reported in config.graph)
+    graph = None
+    if world > 1:
+        try:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                slab.assemble(flags, stream)
+            g.replay()
+            torch.cuda.synchronize()
+            graph = g
+        except Exception as e:   # noqa: BLE001 - fall back to direct calls
+            print(f"[bench] rank {rank}: graph capture failed ({e}); direct calls", file=sys.stderr, flush=True)
+            torch.cuda.synchronize()
+            graph = None
+        ok = torch.tensor([1.0 if graph is not None else 0.0], device=dev)
+        torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
+        if ok.item() < 1.0:
+            graph = None
+    step = (lambda i: graph.replay()) if graph is not None else (lambda i: slab.assemble(flags, stream))
+    core_timed = not (flags & B.GENERIC_PATH) and slab.h.core_rect()[1] > 0 and graph is None
     if core_timed:
         slab.h.set_kernel_timing(args.steps)
     if world > 1:
         torch.distributed.barrier()
     with Clocks(local_rank) as clk:
-        ms, call_ms = _timed(torch, lambda i: slab.assemble(flags, stream), args.steps, stream, per_call=True)
+        ms, call_ms = _timed(torch, step, args.steps, stream, per_call=True)
     core_ms, band_ms = slab.h.kernel_timing(args.steps) if core_timed else ([], [])
     if core_timed:
         slab.h.set_kernel_timing(0)
@@ -441,6 +463,7 @@ def bench_c4(args, rank, world, local_rank):
                                   "+ 1-double energy all-reduce"),
                    "elements": el, "nnzb": reduced_nnzb(sh.n_u), "slab_rows": [slab.r0, slab.r1],
                    "path": "generic" if (flags & B.GENERIC_PATH) else "core+band+corners",
+                   "graph": graph is not None,
                    "l2": "1.78 GB of outputs per step > 126 MB L2 (no flush needed)",
                    "energy_check": (None if E_whole is None else
                                     {"allreduced": E_slabs, "whole_sheet": E_whole,
