@@ -204,6 +204,26 @@ bsf_status bsf_eval_ip_batch(bsf_handle h, int nbatch, const double* d_x, int64_
  *   stops at |b - Hx| <= rtol |b| or after max_iter iterations (check *relres); *iters, *relres: host (may
  *   be NULL).  BSF_E_INVALID_ARG if H is found not SPD.  Synchronises `stream` every 16 iterations. */
 bsf_status bsf_bsr_spmv(bsf_handle h, const double* d_vals, const double* d_x, double* d_y, bsf_stream stream);
+
+/* Direct solve (the paper factorises) and its Neumann split (Eq. `eq: Neumann
+ * expansion`).  Whole-sheet handles only.  In control-point-major DOF order the Hessian is banded (half-bandwidth
+ * 6 n_u + 5 DOFs for the reduced rules) and Cholesky keeps the band, so the factor is a device band matrix of
+ * 3 n_v n_u x (half-bandwidth + 129) doubles (C2 128^2: 0.3 GB; C3 226^2: 1.9 GB); BSF_E_OOM if that exceeds
+ * half the free device memory (e.g. C4).
+ * bsf_chol_factor: factorises the SPD matrix D given by d_vals (the handle's pattern), e.g. the PSD-projected
+ *   Hessian plus inertia, with cuSOLVER potrf / cuBLAS trsm + syrk panels (loaded at run time), and records the
+ *   Gershgorin lower bound of D's spectrum.  Synchronises `stream`.  BSF_E_INVALID_ARG if D is not positive
+ *   definite (names the pivot).
+ * bsf_chol_solve: d_x = D^-1 d_b (device [n_v][n_u][3]; d_x may equal d_b).  Asynchronous.
+ * bsf_neumann_solve: solves (D + B) x = b with the factorised D and B = d_vals_B (same pattern, symmetric) by the
+ *   Neumann series x = sum_k (-D^-1 B)^k D^-1 b (as the fixed point x <- D^-1 (b - B x)), after the paper's gate:
+ *   |D^-1 B| <= lambda_max(B) / lambda_min(D), both from Gershgorin discs; *gate (host) receives that bound and
+ *   BSF_E_INVALID_ARG is returned if it is >= 1 (factorise D + B instead).  Stops when the step is <= rtol |x| or
+ *   after max_terms terms (*terms, host, may be NULL).  Synchronises `stream` once per term. */
+bsf_status bsf_chol_factor(bsf_handle h, const double* d_vals, bsf_stream stream);
+bsf_status bsf_chol_solve(bsf_handle h, const double* d_b, double* d_x, bsf_stream stream);
+bsf_status bsf_neumann_solve(bsf_handle h, const double* d_vals_B, const double* d_b, double* d_x, int max_terms,
+                             double rtol, double* gate, int* terms, bsf_stream stream);
 bsf_status bsf_gershgorin(bsf_handle h, const double* d_vals, double* lo, double* hi, bsf_stream stream);
 bsf_status bsf_pcg(bsf_handle h, const double* d_vals, const double* d_b, double* d_x, int max_iter, double rtol,
                    int* iters, double* relres, bsf_stream stream);

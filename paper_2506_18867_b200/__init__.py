@@ -31,7 +31,8 @@ SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_mate
            "bsf_allreduce_sum", "bsf_get_core_rect", "bsf_eval_all_batch_host", "bsf_set_inertia",
            "bsf_get_lumped_mass", "bsf_eval_ip_batch", "bsf_bsr_spmv", "bsf_gershgorin", "bsf_pcg",
            "bsf_eval_all_slab", "bsf_set_kernel_timing", "bsf_get_kernel_timing",
-           "bsf_last_launch_count", "bsf_poll_status", "bsf_affine_params", "bsf_halo_plan", "bsf_last_error"]
+           "bsf_last_launch_count", "bsf_poll_status", "bsf_affine_params", "bsf_halo_plan", "bsf_chol_factor",
+           "bsf_chol_solve", "bsf_neumann_solve", "bsf_last_error"]
 
 
 class BsfError(RuntimeError):
@@ -95,6 +96,9 @@ def lib():
         L.bsf_gershgorin.argtypes = [vp, vp, dp, dp, vp]
         L.bsf_pcg.argtypes = [vp, vp, vp, vp, C.c_int, C.c_double, C.POINTER(C.c_int), dp, vp]
         L.bsf_poll_status.argtypes = [vp]
+        L.bsf_chol_factor.argtypes = [vp, vp, vp]
+        L.bsf_chol_solve.argtypes = [vp, vp, vp, vp]
+        L.bsf_neumann_solve.argtypes = [vp, vp, vp, vp, C.c_int, C.c_double, dp, C.POINTER(C.c_int), vp]
         L.bsf_halo_plan.argtypes = [vp, C.c_int, C.c_int, i64p]
         L.bsf_affine_params.argtypes = [C.c_int, C.c_int, dp, C.POINTER(Material), dp]
         for s in SYMBOLS:
@@ -317,6 +321,27 @@ class Sheet:
         _check(lib().bsf_pcg(self._h, _ptr(vals), _ptr(b), _ptr(x), int(max_iter), float(rtol), C.byref(it),
                              C.byref(rr), _stream(stream)))
         return x, it.value, rr.value
+
+    def chol_factor(self, vals, stream=None):
+        """Banded Cholesky of the SPD matrix with BSR values `vals` [nnzb, 3, 3] (whole-sheet handle); synchronises."""
+        _check(lib().bsf_chol_factor(self._h, _ptr(vals), _stream(stream)))
+
+    def chol_solve(self, b, x=None, stream=None):
+        """x = D^-1 b with the last factorisation; b, x [n_v, n_u, 3] (CUDA float64)."""
+        import torch
+        x = torch.empty_like(b) if x is None else x
+        _check(lib().bsf_chol_solve(self._h, _ptr(b), _ptr(x), _stream(stream)))
+        return x
+
+    def neumann_solve(self, vals_B, b, x=None, max_terms=100, rtol=1e-13, stream=None):
+        """(D + B) x = b by the Gershgorin-gated Neumann series on the factorised D; returns
+        (x, gate bound, terms).  Raises BsfError(INVALID_ARG) if the gate bound is >= 1."""
+        import torch
+        x = torch.empty_like(b) if x is None else x
+        g, t = C.c_double(), C.c_int()
+        _check(lib().bsf_neumann_solve(self._h, _ptr(vals_B), _ptr(b), _ptr(x), int(max_terms), float(rtol),
+                                       C.byref(g), C.byref(t), _stream(stream)))
+        return x, g.value, t.value
 
     def eval_all_batch_host(self, x_host, x_stage, energy=None, energy_host=None, grad=None, vals=None, params=None,
                             flags=0, chunk=0, stream=None):

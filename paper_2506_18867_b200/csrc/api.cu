@@ -18,6 +18,7 @@
 #include "ip.hpp"
 #include "solve.hpp"
 #include "g3.hpp"
+#include "chol.hpp"
 
 namespace bsf {
 int generic_eval(const GenericTables& t, const double* d_x, const Mat& mat, int flags, int64_t nnzb, int64_t nrows,
@@ -63,6 +64,7 @@ struct bsf_sheet {
   int32_t *d_rp = nullptr, *d_ci = nullptr, *d_sdiag = nullptr;
   bsf::CgWork cg{};
   bsf::CgGraph cg_graph;
+  bsf::CholState chol;                  // banded Cholesky of the Newton matrix (chol.cu)
   cudaStream_t comm_stream = nullptr;   // bsf_eval_all_slab: halo exchange
   cudaEvent_t ev_halo0 = nullptr, ev_halo = nullptr;
   bool solve_ready = false, cg_ready = false;
@@ -78,6 +80,7 @@ struct bsf_sheet {
     cudaGetDevice(&prev);
     cudaSetDevice(device);
     if (sflag_host) cudaFreeHost(sflag_host);
+    bsf::chol_free(chol);
     if (tt.side) cudaStreamDestroy(tt.side);
     if (tt.side2) cudaStreamDestroy(tt.side2);
     if (tt.ev_join2) cudaEventDestroy(tt.ev_join2);
@@ -679,6 +682,78 @@ bsf_status bsf_pcg(bsf_handle h, const double* d_vals, const double* d_b, double
   if (relres) *relres = rr;
   if (status == 2) return fail(BSF_E_INVALID_ARG, "matrix not SPD (p.Hp <= 0 or a diagonal block not positive definite)");
   return BSF_OK;
+}
+
+bsf_status bsf_chol_factor(bsf_handle h, const double* d_vals, bsf_stream stream) {
+  if (!h || !d_vals) return fail(BSF_E_INVALID_ARG, "null argument");
+  if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
+  if (h->sh.r0 != 0 || h->sh.r1 != h->sh.n_v) return fail(BSF_E_INVALID_ARG, "bsf_chol_factor needs a whole-sheet handle");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  auto st = static_cast<cudaStream_t>(stream);
+  bsf::SolveArgs A;
+  bsf_status s = solve_setup(h, false, A);
+  std::string err;
+  if (s == BSF_OK && !h->chol.ready) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const int rc = bsf::chol_setup(h->chol, h->sh.row_ptr, h->sh.col_idx, A.nrows, fr / 2, err);
+    if (rc) s = fail(rc == -7 ? BSF_E_OOM : BSF_E_CUDA, err);
+  }
+  // the spectrum's Gershgorin lower bound of the factorised matrix (the Neumann gate's denominator)
+  double lo = 0.0, hi = 0.0;
+  if (s == BSF_OK && bsf::gershgorin(A, d_vals, h->cg.part, &lo, &hi, st)) s = fail(BSF_E_CUDA, "gershgorin failed");
+  if (s == BSF_OK) {
+    const int rc = bsf::chol_factor(h->chol, h->d_ci, d_vals, st, err);
+    if (rc) s = fail(rc == -1 ? BSF_E_INVALID_ARG : BSF_E_CUDA, err);
+    h->chol.lam_min_D = lo;
+  }
+  if (prev != h->device) cudaSetDevice(prev);
+  return s;
+}
+
+bsf_status bsf_chol_solve(bsf_handle h, const double* d_b, double* d_x, bsf_stream stream) {
+  if (!h || !d_b || !d_x) return fail(BSF_E_INVALID_ARG, "null argument");
+  if (!h->chol.factored) return fail(BSF_E_INVALID_ARG, "no factorisation (bsf_chol_factor)");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  std::string err;
+  const int rc = bsf::chol_solve(h->chol, d_b, d_x, static_cast<cudaStream_t>(stream), err);
+  if (prev != h->device) cudaSetDevice(prev);
+  return rc ? fail(BSF_E_CUDA, err) : BSF_OK;
+}
+
+bsf_status bsf_neumann_solve(bsf_handle h, const double* d_vals_B, const double* d_b, double* d_x, int max_terms,
+                             double rtol, double* gate, int* terms, bsf_stream stream) {
+  if (!h || !d_vals_B || !d_b || !d_x || max_terms < 0 || !(rtol > 0.0)) return fail(BSF_E_INVALID_ARG, "bad arguments");
+  if (!h->chol.factored) return fail(BSF_E_INVALID_ARG, "no factorisation of D (bsf_chol_factor)");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  auto st = static_cast<cudaStream_t>(stream);
+  bsf::SolveArgs A;
+  bsf_status s = solve_setup(h, false, A);
+  double lo = 0.0, hi = 0.0;
+  if (s == BSF_OK && bsf::gershgorin(A, d_vals_B, h->cg.part, &lo, &hi, st)) s = fail(BSF_E_CUDA, "gershgorin failed");
+  // |D^-1 B|_op <= lambda_max(B) / lambda_min(D), both bounded by Gershgorin discs
+  const double lmaxB = std::max(std::fabs(lo), std::fabs(hi)), lminD = h->chol.lam_min_D;
+  const double g = lminD > 0.0 ? lmaxB / lminD : INFINITY;
+  if (gate) *gate = g;
+  if (s == BSF_OK && !(g < 1.0))
+    s = fail(BSF_E_INVALID_ARG, "Neumann gate not met: lambda_max(B) / lambda_min(D) bound = " + std::to_string(g) +
+                                    " >= 1 (factorise D + B instead)");
+  if (s == BSF_OK) {
+    std::string err;
+    const bsf::SpmvFn spmv_b = [&](const double* x, double* y, cudaStream_t ss) {
+      return bsf::spmv(A, d_vals_B, x, y, nullptr, ss);
+    };
+    if (bsf::neumann_solve(h->chol, spmv_b, d_b, d_x, max_terms, rtol, terms, nullptr, st, err))
+      s = fail(BSF_E_CUDA, err);
+  }
+  if (prev != h->device) cudaSetDevice(prev);
+  return s;
 }
 
 bsf_status bsf_eval_all_batch_host(bsf_handle h, int nbatch, const double* h_x, int64_t x_stride, double* d_x_stage,
