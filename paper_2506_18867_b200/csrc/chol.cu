@@ -8,7 +8,8 @@
 // ab[(i - j) + j ldab]) with ldab = kd + nb + 1: the nb extra rows of zeros make every panel rectangle of the
 // blocked right-looking algorithm a plain column-major matrix with leading dimension ldab - 1 (the LAPACK
 // dpbtrf view), so the panel steps are the library calls potrf (diagonal block), trsm (the kd rows below it)
-// and syrk (their rank-nb update of the trailing band).  Solves use banded triangular solves (tbsv).
+// and syrk (their rank-nb update of the trailing band).  Solves walk the same panels (trsv on the diagonal
+// block, gemv with the rows below it).
 // cuBLAS / cuSOLVER are loaded at run time from the process (torch ships both), like NCCL (halo.cpp).
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
@@ -17,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -36,6 +38,8 @@ struct Lib {
   decltype(&cublasDtrsm_v2) trsm = nullptr;
   decltype(&cublasDsyrk_v2) syrk = nullptr;
   decltype(&cublasDtbsv_v2) tbsv = nullptr;
+  decltype(&cublasDtrsv_v2) trsv = nullptr;
+  decltype(&cublasDgemv_v2) gemv = nullptr;
   decltype(&cusolverDnCreate) s_create = nullptr;
   decltype(&cusolverDnDestroy) s_destroy = nullptr;
   decltype(&cusolverDnSetStream) s_set_stream = nullptr;
@@ -63,13 +67,16 @@ const Lib& lib() {
     BSF_SYM(hb, trsm, "cublasDtrsm_v2");
     BSF_SYM(hb, syrk, "cublasDsyrk_v2");
     BSF_SYM(hb, tbsv, "cublasDtbsv_v2");
+    BSF_SYM(hb, trsv, "cublasDtrsv_v2");
+    BSF_SYM(hb, gemv, "cublasDgemv_v2");
     BSF_SYM(hs, s_create, "cusolverDnCreate");
     BSF_SYM(hs, s_destroy, "cusolverDnDestroy");
     BSF_SYM(hs, s_set_stream, "cusolverDnSetStream");
     BSF_SYM(hs, potrf_buf, "cusolverDnDpotrf_bufferSize");
     BSF_SYM(hs, potrf, "cusolverDnDpotrf");
 #undef BSF_SYM
-    L.ok = L.create && L.destroy && L.set_stream && L.trsm && L.syrk && L.tbsv && L.s_create && L.s_destroy &&
+    L.ok = L.create && L.destroy && L.set_stream && L.trsm && L.syrk && L.tbsv && L.trsv && L.gemv && L.s_create &&
+           L.s_destroy &&
            L.s_set_stream && L.potrf_buf && L.potrf;
     if (!L.ok) L.err = "cuBLAS / cuSOLVER lack a required symbol";
   });
@@ -138,7 +145,8 @@ int chol_setup(CholState& C, const std::vector<int32_t>& row_ptr, const std::vec
     }
   C.n = 3 * (int64_t)nrows;
   C.kd = kd;
-  C.nb = 128;
+  static const int nb_env = getenv("BSF_CHOL_NB") ? atoi(getenv("BSF_CHOL_NB")) : 0;
+  C.nb = nb_env > 0 ? nb_env : 256;
   C.ldab = kd + C.nb + 1;
   const size_t bytes = sizeof(double) * (size_t)C.n * (size_t)C.ldab;
   if (bytes > max_bytes) {
@@ -242,13 +250,35 @@ int chol_solve(CholState& C, const double* d_b, double* d_x, cudaStream_t st, st
     err = "copy";
     return -6;
   }
-  if (L.set_stream(hb, st) != CUBLAS_STATUS_SUCCESS ||
-      L.tbsv(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)C.n, (int)C.kd, C.ab, (int)C.ldab, d_x,
-             1) != CUBLAS_STATUS_SUCCESS ||
-      L.tbsv(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)C.n, (int)C.kd, C.ab, (int)C.ldab, d_x,
-             1) != CUBLAS_STATUS_SUCCESS) {
-    err = "tbsv failed";
-    return -6;
+  if (L.set_stream(hb, st) != CUBLAS_STATUS_SUCCESS) { err = "set stream"; return -6; }
+  // blocked banded triangular solves over the factor's panels (the dense views of the factorisation): forward
+  // L y = b: y1 = L11^-1 y1, y2 -= A21 y1; backward L^T x = y: x1 -= A21^T x2, x1 = L11^-T x1
+  const int lda = (int)(C.ldab - 1);
+  const double one = 1.0, mone = -1.0;
+  for (int64_t j0 = 0; j0 < C.n; j0 += C.nb) {
+    const int jb = (int)std::min<int64_t>(C.nb, C.n - j0);
+    const int i2 = (int)std::min<int64_t>(C.kd, C.n - j0 - jb);
+    const double* a11 = C.ab + j0 * C.ldab;
+    if (L.trsv(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, jb, a11, lda, d_x + j0, 1) !=
+            CUBLAS_STATUS_SUCCESS ||
+        (i2 > 0 && L.gemv(hb, CUBLAS_OP_N, i2, jb, &mone, a11 + jb, lda, d_x + j0, 1, &one, d_x + j0 + jb, 1) !=
+                       CUBLAS_STATUS_SUCCESS)) {
+      err = "forward solve failed";
+      return -6;
+    }
+  }
+  for (int64_t p = (C.n + C.nb - 1) / C.nb - 1; p >= 0; --p) {
+    const int64_t j0 = p * C.nb;
+    const int jb = (int)std::min<int64_t>(C.nb, C.n - j0);
+    const int i2 = (int)std::min<int64_t>(C.kd, C.n - j0 - jb);
+    const double* a11 = C.ab + j0 * C.ldab;
+    if ((i2 > 0 && L.gemv(hb, CUBLAS_OP_T, i2, jb, &mone, a11 + jb, lda, d_x + j0 + jb, 1, &one, d_x + j0, 1) !=
+                       CUBLAS_STATUS_SUCCESS) ||
+        L.trsv(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, jb, a11, lda, d_x + j0, 1) !=
+            CUBLAS_STATUS_SUCCESS) {
+      err = "backward solve failed";
+      return -6;
+    }
   }
   return 0;
 }

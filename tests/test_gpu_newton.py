@@ -42,7 +42,8 @@ def _oracle_step(sh, x, v, dt, R0, grav, pinned, tol, max_iter=50):
 
 
 @pytest.mark.parametrize("n", [16, 24])
-def test_hanging_sheet_step_matches_oracle(n):
+@pytest.mark.parametrize("solver", ["chol", "pcg"])
+def test_hanging_sheet_step_matches_oracle(n, solver):
     sh = W.make_sheet(n, 1.0, 5, n_modes=3, amp=2e-3, lam=0.3)
     R0, dt, grav = 0.2, 1e-2, np.array([0.0, 0.0, -9.81])
     pinned = np.zeros((n, n), bool)
@@ -53,7 +54,7 @@ def test_hanging_sheet_step_matches_oracle(n):
     s = B.Sheet.from_sheet(sh)
     s.set_inertia(R0, dt, gravity=grav, pinned=pinned)
     x_gpu, v_gpu, st = implicit_euler_step(s, torch.from_numpy(sh.x).cuda(), torch.from_numpy(v).cuda(), dt,
-                                           tol=1e-7)
+                                           tol=1e-7, solver=solver)
     assert st.converged and st.iterations < 10, st
     assert all(e1 <= e0 + 1e-12 * abs(e0) for e0, e1 in zip(st.energies, st.energies[1:])), st.energies
     x_ref = _oracle_step(sh, sh.x, v, dt, R0, grav, pinned, tol=1e-7)
