@@ -208,7 +208,7 @@ bsf_status bsf_bsr_spmv(bsf_handle h, const double* d_vals, const double* d_x, d
 /* Direct solve (the paper factorises) and its Neumann split (Eq. `eq: Neumann
  * expansion`).  Whole-sheet handles only.  In control-point-major DOF order the Hessian is banded (half-bandwidth
  * 6 n_u + 5 DOFs for the reduced rules) and Cholesky keeps the band, so the factor is a device band matrix of
- * 3 n_v n_u x (half-bandwidth + 129) doubles (C2 128^2: 0.3 GB; C3 226^2: 1.9 GB); BSF_E_OOM if that exceeds
+ * 3 n_v n_u x (half-bandwidth + 513) doubles (C2 128^2: 0.5 GB; C3 226^2: 2.3 GB); BSF_E_OOM if that exceeds
  * half the free device memory (e.g. C4).
  * bsf_chol_factor: factorises the SPD matrix D given by d_vals (the handle's pattern), e.g. the PSD-projected
  *   Hessian plus inertia, with cuSOLVER potrf / cuBLAS trsm + syrk panels (loaded at run time), and records the
