@@ -57,6 +57,7 @@ struct BandArgs {
   int n_u, xlo, xhi, r0;
   int project, flags, dbg;
   unsigned long long* sflag;   // singular-stretch word (fbw.cuh)
+  EFinal ef;                   // fused energy reduction of the call
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
   const double2* mcf;
   const int2* mcls;
@@ -383,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
     for (int w = 0; w < kThreads / 32; ++w) sum += red[w];
     A.epart[item * A.e_stride + A.e_off + cta] = sum;
   }
+  energy_final_fused(A.ef, A.epart, item);
 }
 
 template <class T>
@@ -680,6 +682,7 @@ int band_eval(const BandTables& bt, const Sheet& sh, const double* d_x, int64_t 
   static_assert(sizeof(BandArgs) <= 32000, "kernel parameter budget");
   BandArgs A;
   A.sflag = call_sflag();
+  A.ef = call_efinal();
   A.x = d_x; A.xs = x_stride; A.g = d_g; A.gs = g_stride; A.vals = d_vals; A.vs = v_stride;
   A.epart = e_part; A.e_stride = e_stride; A.e_off = e_off;
   A.row_ptr = d_row_ptr; A.params = d_params;

@@ -56,6 +56,7 @@ struct CoreArgs {
   int JA, JB;              // rows of this launch ([RJ0, RJ1) or a sub-range; addressing stays relative to RJ0)
   int project, flags, dbg;
   unsigned long long* sflag;   // singular-stretch word (fbw.cuh)
+  EFinal ef;                   // fused energy reduction of the call
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
   const double* tabs;      // device [104]: S[4][9][2] | LA[9] | LB[9] | LC[9] | what[5]
   double what[5];
@@ -646,6 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
     for (int w = 0; w < kThreads / 32; ++w) s += cst[kCstRed + w];
     A.epart[item * A.e_stride + A.e_off + (int64_t)chunk * A.nstrips + strip] = s;
   }
+  energy_final_fused(A.ef, A.epart, item);
 }
 
 }  // namespace
@@ -922,7 +924,7 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
   A.row_ptr = ct.row_ptr; A.rp_base = ct.rp_base; A.rp_stride = ct.rp_stride; A.params = d_params;
   A.n_u = sh.n_u; A.xlo = sh.xlo; A.xhi = sh.xhi; A.r0 = sh.r0;
   A.CI0 = ct.CI0; A.CI1 = ct.CI1; A.RJ0 = ct.RJ0; A.RJ1 = ct.RJ1; A.nstrips = ct.nstrips; A.nchunks = nchunks;
-  A.project = (flags & 1) ? 1 : 0; A.flags = flags; A.sflag = call_sflag();
+  A.project = (flags & 1) ? 1 : 0; A.flags = flags; A.sflag = call_sflag(); A.ef = call_efinal();
   {   // profiling switches (read once per process): 1 no points, 2 no gather, 4 no stores
     static const int dbg = getenv("BSF_CORE_DEBUG") ? atoi(getenv("BSF_CORE_DEBUG")) : 0;
     A.dbg = dbg;

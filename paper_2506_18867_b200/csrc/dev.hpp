@@ -42,6 +42,19 @@ inline unsigned long long*& call_sflag() {
   return p;
 }
 
+// Fused energy reduction of a call (fbw.cuh energy_final_fused): the launch functions of the core / band / corner
+// kernels copy the calling thread's current value into their kernel arguments.
+struct EFinal {
+  unsigned* cnt = nullptr;   // [nbatch] CTAs done (zeroed at the start of every call)
+  double* out = nullptr;     // [nbatch] energies (nullptr: no fused reduction)
+  int total = 0;             // CTAs per item over all kernels of the call (= energy slots per item)
+  int per_item = 0;          // energy slots per item
+};
+inline EFinal& call_efinal() {
+  static thread_local EFinal e;
+  return e;
+}
+
 constexpr uint32_t kIncBend = 1u << 31;
 inline __host__ __device__ uint32_t pack_inc(bool bend, uint32_t pt, uint32_t la, uint32_t lb) {
   return (bend ? kIncBend : 0u) | (pt << 8) | (la << 4) | lb;

@@ -49,6 +49,7 @@ struct FrameArgs {
   int maxM, maxB;
   int project, flags, dbg;
   unsigned long long* sflag;   // singular-stretch word (fbw.cuh)
+  EFinal ef;                   // fused energy reduction of the call
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
   const int4* tile;
   const int32_t* tpm;
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_frame(const FrameArgs A) {
     for (int w = 0; w < kThreads / 32; ++w) sum += red[w];
     A.epart[item * A.e_stride + A.e_off + tile] = sum;
   }
+  energy_final_fused(A.ef, A.epart, item);
 }
 
 template <class T>
@@ -523,6 +525,7 @@ int frame_eval(const FrameTables& ft, const Sheet& sh, const double* d_x, int64_
   if (ft.ntiles == 0) return 0;
   FrameArgs A;
   A.sflag = call_sflag();
+  A.ef = call_efinal();
   A.xhat = ip ? ip->xhat : nullptr; A.xhs = ip ? ip->xhs : 0; A.mass = ip ? ip->mass : nullptr;
   A.ipk = ip ? ip->k : 0.0;
   for (int c = 0; c < 3; ++c) A.grav[c] = ip ? ip->grav[c] : 0.0;

@@ -919,6 +919,19 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
       tt.e_part = static_cast<double*>(p);
       tt.e_cap = need;
     }
+    // fused energy reduction: the last CTA of the call's core / band / corner kernels writes each item's energy
+    // (no separate reduction launch after the join); its counters are zeroed first on the caller's stream
+    if (d_E && nbatch > tt.e_cnt_cap) {
+      void* p = dalloc(sizeof(unsigned) * (size_t)nbatch);
+      if (!p) return -7;
+      tt.e_cnt = static_cast<unsigned*>(p);
+      tt.e_cnt_cap = nbatch;
+    }
+    if (d_E && cudaMemsetAsync(tt.e_cnt, 0, sizeof(unsigned) * (size_t)nbatch, st) != cudaSuccess) return -6;
+    struct EfScope {   // the launch functions below read call_efinal(); reset on every exit path
+      explicit EfScope(const EFinal& e) { call_efinal() = e; }
+      ~EfScope() { call_efinal() = EFinal(); }
+    } ef_scope(d_E ? EFinal{tt.e_cnt, d_E, (int)e_stride, (int)e_stride} : EFinal());
     // the two kernels write disjoint rows: the frame runs on a side stream forked from / joined to st
     // (event fork-join, CUDA-graph capturable)
     if (!tt.side) {
@@ -976,11 +989,8 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     if (small && (cudaEventRecord(tt.ev_join2, tt.side2) != cudaSuccess ||
                   cudaStreamWaitEvent(st, tt.ev_join2, 0) != cudaSuccess))
       return -6;
-    int nl = 1 + (ft->ntiles > 0) + (ft->band.ok && ft->band.nctas > 0);
-    if (d_E) {
-      k_energy_final<<<nbatch, 256, 0, st>>>(tt.e_part, (int)e_stride, d_E);
-      ++nl;
-    }
+    const int nl = 1 + (ft->ntiles > 0) + (ft->band.ok && ft->band.nctas > 0) + (ov && halo->ja > ct->RJ0) +
+                   (ov && halo->jb < ct->RJ1);
     if (launches) *launches = nl;
     return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
   }

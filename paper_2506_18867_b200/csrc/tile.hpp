@@ -48,6 +48,8 @@ struct TileTables {
   int32_t* row_ptr = nullptr;      // owned rows' pattern (device copy)
   double* e_part = nullptr;        // per-CTA energy partials (grown on demand)
   int64_t e_cap = 0;
+  unsigned* e_cnt = nullptr;       // [nbatch] fused energy reduction counters (core path; grown on demand)
+  int64_t e_cnt_cap = 0;
   // frame mode (the interior core kernel covers a rectangle): CTAs of the tile kernel
   // restricted to the (strip, chunk) pairs that touch the frame, per chunk list
   int core = 0;
