@@ -93,7 +93,13 @@ __device__ __forceinline__ void static_for(F&& f) {
 // by exhaustive search over the 12 (channel group, load) combinations and both pair offsets) puts every
 // such load at the 2-wavefront minimum (no bank conflicts).
 constexpr int kRecP = 30, kRecC = kMS * kRecP;
-__host__ __device__ __forceinline__ constexpr int rec_pos(int ch) {
+// Run-time channels (the gather's per-task offsets) read a constant-bank table: the switch below becomes a jump
+// table there, which the compiler rematerialised inside the gather loops (5 % of the band kernel's stall samples).
+struct RecPosTable { unsigned char p[27]; };
+constexpr RecPosTable kRecPos = {{5, 15, 0, 27, 23, 24, 9, 14, 19, 2, 26, 8, 1, 20, 13, 4, 16, 21, 7, 18, 12, 25, 29, 28, 11,
+                                  3, 10}};
+__constant__ RecPosTable kRecPosDev = kRecPos;
+__host__ __device__ __forceinline__ constexpr int rec_pos(int ch) {   // compile-time channels
   switch (ch) {
     case 0: return 5;   case 1: return 15;  case 2: return 0;   case 3: return 27;  case 4: return 23;
     case 5: return 24;  case 6: return 9;   case 7: return 14;  case 8: return 19;  case 9: return 2;
@@ -103,6 +109,7 @@ __host__ __device__ __forceinline__ constexpr int rec_pos(int ch) {
     case 25: return 3;  default: return 10;
   }
 }
+__device__ __forceinline__ int rec_pos_rt(int ch) { return kRecPosDev.p[ch]; }   // run-time channels
 
 constexpr int kPA = kNA + 4;                       // staged along cps: [S0 - 2, S0 + kNA + 2)
 constexpr int kPosMax = (kMaxD + 4) * kPA * 3;     // staged depth rows: [od0, od1 + 1]
@@ -284,10 +291,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
     const bool hess = lc < 9;
     // record channels of this lane: Hessian lanes A~uu[rc], A~uv[cr], A~uv[rc], A~vv[rc]; gradient lanes
     // P~u[c], P~v[c] (their Y_u is the gradient contribution; their block accumulators are not used)
-    const int o_uu = rec_pos(hess ? sym3(r3, c3) : 21 + lc - 9) + kRecP * l;
-    const int o_cr = rec_pos(hess ? 12 + 3 * c3 + r3 : 24 + lc - 9) + kRecP * l;
-    const int o_rc = hess ? rec_pos(12 + 3 * r3 + c3) + kRecP * l : o_uu;
-    const int o_vv = hess ? rec_pos(6 + sym3(r3, c3)) + kRecP * l : o_cr;
+    const int o_uu = rec_pos_rt(hess ? sym3(r3, c3) : 21 + lc - 9) + kRecP * l;
+    const int o_cr = rec_pos_rt(hess ? 12 + 3 * c3 + r3 : 24 + lc - 9) + kRecP * l;
+    const int o_rc = hess ? rec_pos_rt(12 + 3 * r3 + c3) + kRecP * l : o_uu;
+    const int o_vv = hess ? rec_pos_rt(6 + sym3(r3, c3)) + kRecP * l : o_cr;
     double acc[kSl];
 #pragma unroll
     for (int k = 0; k < kSl; ++k) acc[k] = 0.0;
