@@ -481,10 +481,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
       }
     }
     const uint32_t pos_s = smem_u32(posb);
-    load_pos_async(posb, x, A, i0, ja - 4, 5, tid);
+    // Prologue (pairs 0-2) in ONE phase on all 16 warps (round 2; it took three point-only iterations on the 7
+    // point warps): the 9 cp rows [ja-4, ja+5) of its positions go to the staging buffer, idle until the first
+    // bulk store, while pair 3's rows go to position buffer 1 as the main loop expects.
+    double* ppos = stage;
+    load_pos_async(ppos, x, A, i0, ja - 4, 9, tid);
+    if (nst >= 2) load_pos_async(posb + kPosStep, x, A, i0, ja + 2, 5, tid);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
-    for (int mi = 0; mi <= nst + 2; ++mi) {
+    for (int it = tid; it < 3 * 6 * kKC; it += kThreads) {
+      const int pr = it / (6 * kKC), item = it - pr * (6 * kKC);
+      e_acc += eval_item(ring, ppos + 2 * pr * (kPosC * 3), ja - 4 + 2 * pr, cst, P, ja - 3 + 2 * pr, item);
+    }
+    __syncthreads();
+    for (int mi = 3; mi <= nst + 2; ++mi) {
       const int q0 = ja - 3 + 2 * mi, k = mi - 3, j = ja + kRows * k;
       CT_MARK(T0);
 #ifdef BSF_PHASE_TIMERS
