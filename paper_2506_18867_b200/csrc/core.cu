@@ -58,6 +58,13 @@ struct CoreArgs {
   unsigned long long* sflag;   // singular-stretch word (fbw.cuh)
   EFinal ef;                   // fused energy reduction of the call
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
+  // curved rest map (CoreTables): per-point / per-cp tables, knot pitch, core columns
+  const double* mtab;
+  const double* btab;
+  const double* beta;
+  const double* gw;
+  int64_t kp, cw;
+  int Su, Sv;
   const double* tabs;      // device [104]: S[4][9][2] | LA[9] | LB[9] | LC[9] | what[5]
   double what[5];
   // incremental-potential terms (Q13; xhat == nullptr: elastic only)
@@ -144,11 +151,12 @@ __device__ __forceinline__ double lds_f64(uint32_t addr) {
 // over the 12 incident membrane points + sum_q' w mu L_a(q') Lap phi(q')[r] over the 8 bending points.
 // base0/1: shared byte addresses of the knot rows (channel 0) for even / odd dp; bb0/1: bending arrays
 // at channel r.  Run by the point warps with spare time (the gather warps carry the blocks).
-template <int PI>
+template <int PI, bool CURVED>
 __device__ __forceinline__ void gather_grad(const uint32_t (&base0)[4], const uint32_t (&base1)[4],
                                             const double* const (&bb0)[3], const double* const (&bb1)[3],
                                             uint32_t o_pu, uint32_t o_pv, const double* __restrict__ cst,
-                                            double* gdst, double g0) {
+                                            double* gdst, double g0, const double* __restrict__ gw, int64_t gws,
+                                            double mubd) {
   double g = g0;
   static_for<0, make_template(PI).nslot>([&](auto SI) {
     constexpr int s = decltype(SI)::value;
@@ -163,16 +171,18 @@ __device__ __forceinline__ void gather_grad(const uint32_t (&base0)[4], const ui
     constexpr int k = decltype(KI)::value;
     constexpr int dp = bslot_dp(k), dq = bslot_dq(k);
     const double* b = ((dp & 1) ? bb1[dq + 2] : bb0[dq + 2]) + ((dp + 2) >> 1);
-    g = fma(cst[kCstLw + k], b[0], g);
+    // curved: w mu L_a of this cp's own bending slot k (per-cp table); affine: one value per slot
+    g = fma(CURVED ? mubd * __ldg(gw + k * gws) : cst[kCstLw + k], b[0], g);
   });
   if (gdst) *gdst = g;
 }
 
-template <int PI>
+template <int PI, bool CURVED>
 __device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
                                             const uint32_t (&base1)[4], int o_rc, int o_cr, bool diag,
                                             const double* __restrict__ cst, double* st_lane, bool active,
-                                            uint32_t bar, uint32_t parity, double dshift) {
+                                            uint32_t bar, uint32_t parity, double dshift,
+                                            const double* __restrict__ beta, int64_t bs, double mubd) {
   double acc[kNB];
 #pragma unroll
   for (int k = 0; k < kNB; ++k) acc[k] = 0.0;
@@ -201,8 +211,13 @@ __device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
   });
   if (diag) {   // the state-independent bending blocks beta_ab I3 (+ inertia m_a/dt^2); adding them at the end
                 // measured faster than starting the accumulators from them (508 vs 490 us on C4)
+    if constexpr (CURVED) {   // this cp's own bending blocks (per-cp table, w L_a L_b summed over its points)
 #pragma unroll
-    for (int k = 0; k < kNB; ++k) acc[k] += cst[kCstBeta + k];
+      for (int k = 0; k < kNB; ++k) acc[k] = fma(mubd, __ldg(beta + k * bs), acc[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kNB; ++k) acc[k] += cst[kCstBeta + k];
+    }
     acc[block_index(0, 0)] += dshift;
   }
   if (!st_lane) return;
@@ -273,6 +288,11 @@ struct PointCtx {
   bool diagG;      // G01 == G10 == 0 (axis-aligned rest sheet): F, A~ and P~ by scaling
   unsigned long long* sflag;
   int item;
+  // curved rest map: per-point tables (CoreTables::mtab / btab), knot pitch, last knot indices
+  const double* mtab;
+  const double* btab;
+  int64_t kp;
+  int Su, Sv;
 };
 
 // Quadrature points of two consecutive knot rows q0, q0+1: item it in [0, 6 kKC) =
@@ -280,6 +300,7 @@ struct PointCtx {
 // each set ordered by its knot index k = lp >> 1 (conflict-free record writes; membrane items first so
 // that warps do not diverge between the two kinds).  pos holds cp rows from prow0.
 // Returns the point's owned energy.
+template <bool CURVED>
 __device__ __forceinline__ double eval_item(double* ring, const double* pos, int prow0, const double* cst,
                                          const PointCtx& P, int q0, int it) {
   const int nmem = 2 * kKC;
@@ -289,6 +310,9 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
     const int lp = rr < nE ? 2 * rr : 2 * (rr - nE) + 1;
     const int p = P.i0 - 2 + lp;
     double* row = ring + ring_slot(q) * kRowD;
+    // curved: this knot's own Laplacian coefficients and weight (clamped: knots past the sheet feed only lanes
+    // that store nothing)
+    const double* bt = CURVED ? P.btab + (int64_t)min(max(q, 0), P.Sv) * 10 * P.kp + min(max(p, 0), P.Su) : nullptr;
     double lap[3] = {0, 0, 0};
 #pragma unroll
     for (int jv = 0; jv < 3; ++jv)
@@ -296,7 +320,7 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
       for (int iu = 0; iu < 3; ++iu) {
         const int e = 3 * jv + iu;
         if (e == 8) continue;
-        const double L = cst[kCstL + e];
+        const double L = CURVED ? __ldg(bt + e * P.kp) : cst[kCstL + e];
         const double* C = pos + ((q + jv - prow0) * kPosC + pos_col(p + iu - (P.i0 - 3))) * 3;
         lap[0] = fma(L, C[0], lap[0]); lap[1] = fma(L, C[1], lap[1]); lap[2] = fma(L, C[2], lap[2]);
       }
@@ -305,7 +329,8 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
     rec[kKH] = lap[1];
     rec[2 * kKH] = lap[2];
     if (p >= P.i0 && p < P.i1 && q >= P.ja && q < P.jb)
-      return 0.5 * cst[kCstP + 9] * cst[kCstP + 8] * (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
+      return 0.5 * (CURVED ? __ldg(bt + 9 * P.kp) : cst[kCstP + 9]) * cst[kCstP + 8] *
+             (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
     return 0.0;
   }
   const int r = it >= nmem, mi = it - r * nmem, q = q0 + r;
@@ -329,26 +354,34 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
 #pragma unroll
       for (int c = 0; c < 3; ++c) { Fu[c] = fma(C[c], du, Fu[c]); Fv[c] = fma(C[c], dv, Fv[c]); }
     }
-  const double wq = cst[kCstW + set] * cst[kCstP + 4];
+  double wq, G00, G01, G10, G11;
+  if constexpr (CURVED) {   // this point's G = (dX/d(u,v))^-1 and w from the table of its knot (minus / plus point)
+    const double* gm = P.mtab + ((int64_t)min(max(q, 0), P.Sv) * 2 + (set & 1)) * 5 * P.kp + min(max(p, 0), P.Su);
+    G00 = __ldg(gm); G01 = __ldg(gm + P.kp); G10 = __ldg(gm + 2 * P.kp); G11 = __ldg(gm + 3 * P.kp);
+    wq = __ldg(gm + 4 * P.kp);
+  } else {
+    wq = cst[kCstW + set] * cst[kCstP + 4];
+    G00 = cst[kCstP + 0]; G01 = cst[kCstP + 1]; G10 = cst[kCstP + 2]; G11 = cst[kCstP + 3];
+  }
   double f1[3], f2[3];   // F_beta = sum_mu F~_mu G_mu,beta
-  if (P.diagG) {
+  if (!CURVED && P.diagG) {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * cst[kCstP + 0]; f2[c] = Fv[c] * cst[kCstP + 3]; }
+    for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * G00; f2[c] = Fv[c] * G11; }
   } else {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * cst[kCstP + 0] + Fv[c] * cst[kCstP + 2]; f2[c] = Fu[c] * cst[kCstP + 1] + Fv[c] * cst[kCstP + 3]; }
+    for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * G00 + Fv[c] * G10; f2[c] = Fu[c] * G01 + Fv[c] * G11; }
   }
   double* rec = row + set * kSetD + k;
   double psi, i5 = 1.0;
   // P~_mu = w sum_beta G_mu,beta P_beta;  A~_mu,nu = w sum_{beta,gamma} G_mu,beta G_nu,gamma A_beta,gamma,
   // streamed into the record as fbw_emit forms each F-space entry
   const auto emit_p = [&](int c, double P1c, double P2c) {
-    rec[(21 + c) * kKH] = wq * (cst[kCstP + 0] * P1c + cst[kCstP + 1] * P2c);
-    rec[(24 + c) * kKH] = wq * (cst[kCstP + 2] * P1c + cst[kCstP + 3] * P2c);
+    rec[(21 + c) * kKH] = wq * (G00 * P1c + G01 * P2c);
+    rec[(24 + c) * kKH] = wq * (G10 * P1c + G11 * P2c);
   };
-  if (P.diagG) {   // A~uu = w G00^2 A11, A~vv = w G11^2 A22, A~uv = w G00 G11 A12
-    const double auu = wq * cst[kCstP + 0] * cst[kCstP + 0], avv = wq * cst[kCstP + 3] * cst[kCstP + 3];
-    const double auv = wq * cst[kCstP + 0] * cst[kCstP + 3];
+  if (!CURVED && P.diagG) {   // A~uu = w G00^2 A11, A~vv = w G11^2 A22, A~uv = w G00 G11 A12
+    const double auu = wq * G00 * G00, avv = wq * G11 * G11;
+    const double auv = wq * G00 * G11;
     psi = fbw_emit(f1, f2, cst[kCstP + 5], cst[kCstP + 6], cst[kCstP + 7], P.project, emit_p,
                    [&](int r3, int c3, double A11, double A22, double A12rc, double A12cr) {
       const int e6 = sym3(r3, c3);
@@ -360,7 +393,6 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
   } else {
     psi = fbw_emit(f1, f2, cst[kCstP + 5], cst[kCstP + 6], cst[kCstP + 7], P.project, emit_p,
                    [&](int r3, int c3, double A11, double A22, double A12rc, double A12cr) {
-      const double G00 = cst[kCstP + 0], G01 = cst[kCstP + 1], G10 = cst[kCstP + 2], G11 = cst[kCstP + 3];
       const int e6 = sym3(r3, c3);
       const double sym12 = A12rc + A12cr;
       rec[e6 * kKH] = wq * (G00 * G00 * A11 + G00 * G01 * sym12 + G01 * G01 * A22);
@@ -377,7 +409,9 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
   return 0.0;
 }
 
-template <bool IP>   // IP: the incremental-potential terms (compiled out of the elastic kernel)
+// IP: the incremental-potential terms (compiled out of the elastic kernel); CURVED: a non-affine rest map (per-point
+// G, w and Laplacian coefficients and per-cp bending blocks from the CoreTables device tables)
+template <bool IP, bool CURVED>
 __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);   // [kRing][kRowD]
@@ -413,6 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
   }
   P.i0 = i0; P.i1 = i1; P.ja = ja; P.jb = jb; P.project = A.project != 0;
   P.sflag = A.sflag; P.item = item;
+  P.mtab = A.mtab; P.btab = A.btab; P.kp = A.kp; P.Su = A.Su; P.Sv = A.Sv;
   P.diagG = (P.G01 == 0.0 && P.G10 == 0.0);
   const double cuu = P.G00 * P.G00 + P.G01 * P.G01, cvv = P.G10 * P.G10 + P.G11 * P.G11;
   const double cuv = 2.0 * (P.G00 * P.G10 + P.G01 * P.G11);
@@ -491,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
     __syncthreads();
     for (int it = tid; it < 3 * 6 * kKC; it += kThreads) {
       const int pr = it / (6 * kKC), item = it - pr * (6 * kKC);
-      e_acc += eval_item(ring, ppos + 2 * pr * (kPosC * 3), ja - 4 + 2 * pr, cst, P, ja - 3 + 2 * pr, item);
+      e_acc += eval_item<CURVED>(ring, ppos + 2 * pr * (kPosC * 3), ja - 4 + 2 * pr, cst, P, ja - 3 + 2 * pr, item);
     }
     __syncthreads();
     for (int mi = 3; mi <= nst + 2; ++mi) {
@@ -503,7 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
       // (a) positions of the next pair (async) and the quadrature points of this pair
       if (mi + 1 <= nst + 1) load_pos_step(pos_s + ((mi + 1) & 1) * (kPosStep * 8), x, A, pm, i0, q0 + 1);
       if (mi <= nst + 1 && pw >= 0 && lane < 30 && !((A.dbg & 1) && k >= 0))
-        e_acc += eval_item(ring, posb + (mi & 1) * kPosStep, q0 - 1, cst, P, q0, pw * 30 + lane);
+        e_acc += eval_item<CURVED>(ring, posb + (mi & 1) * kPosStep, q0 - 1, cst, P, q0, pw * 30 + lane);
       CT_MARK(T1);
       if (k >= 0) {
         // (b) profiling mode without the gather: the issuing thread releases the staging buffer here (else the
@@ -547,8 +582,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
             const uint32_t par = k & 1;
             const double dshift = (IP && diag && active) ? ipk_m * A.mass[(int64_t)(jr - A.r0) * A.n_u + i] : 0.0;
             const int orc = 8 * (o_rc - o_uu), ocr = 8 * (o_cr - o_uu);
-            if (PI == 0) gather_role<0>(base0, base1, orc, ocr, diag, cst, st_lane, active, bar, par, dshift);
-            else gather_role<1>(base0, base1, orc, ocr, diag, cst, st_lane, active, bar, par, dshift);
+            // curved: the lane's row of the per-cp bending table (a valid row for inactive lanes)
+            const double* bsrc = CURVED ? A.beta + ((int64_t)(active ? jr - A.RJ0 : 0) * kNB) * A.cw + (active ? i - A.CI0 : 0)
+                                        : nullptr;
+            if (PI == 0)
+              gather_role<0, CURVED>(base0, base1, orc, ocr, diag, cst, st_lane, active, bar, par, dshift, bsrc, A.cw,
+                                     P.mubd);
+            else
+              gather_role<1, CURVED>(base0, base1, orc, ocr, diag, cst, st_lane, active, bar, par, dshift, bsrc, A.cw,
+                                     P.mubd);
           }
         }
       }
@@ -591,8 +633,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
             }
             if (gout) {
               const uint32_t opu = 8 * (21 + r) * kKH, opv = 8 * (24 + r) * kKH;
-              if (PI == 0) gather_grad<0>(gb0, gb1, bb0, bb1, opu, opv, cst, gdst, g0);
-              else gather_grad<1>(gb0, gb1, bb0, bb1, opu, opv, cst, gdst, g0);
+              const double* gsrc = CURVED ? A.gw + ((int64_t)(jr - A.RJ0) * kBSlots) * A.cw + (i - A.CI0) : nullptr;
+              if (PI == 0) gather_grad<0, CURVED>(gb0, gb1, bb0, bb1, opu, opv, cst, gdst, g0, gsrc, A.cw, P.mubd);
+              else gather_grad<1, CURVED>(gb0, gb1, bb0, bb1, opu, opv, cst, gdst, g0, gsrc, A.cw, P.mubd);
             }
           }
         }
@@ -689,7 +732,7 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
                const std::function<void*(size_t)>& dalloc) {
   ct = CoreTables();
   ct.row_ptr = const_cast<int32_t*>(d_row_ptr);
-  if (!sh.affine || sh.mrule != RULE_REDUCED || sh.brule != RULE_REDUCED) { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
+  if (sh.mrule != RULE_REDUCED || sh.brule != RULE_REDUCED || (!sh.affine && getenv("BSF_NO_CURVED_CORE"))) { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
   const int nu = sh.n_u, Su = sh.Su, Sv = sh.Sv;
   if (nu < 16 || sh.n_v < 16) { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
   // ---- anchor buckets
@@ -845,6 +888,54 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
     ct.G[0] = ref.G[0][0]; ct.G[1] = ref.G[0][1]; ct.G[2] = ref.G[1][0]; ct.G[3] = ref.G[1][1];
     ct.detJ = ref.detJ;
   }
+  if (!sh.affine) {   // curved rest map: per-point rest tables (see CoreTables)
+    ct.curved = 1;
+    const int64_t kp = Su + 1, nq = Sv + 1;
+    ct.kp = kp;
+    ct.cw = c1 - c0;
+    std::vector<double> mt((size_t)nq * 2 * 5 * kp, 0.0), bt((size_t)nq * 10 * kp, 0.0);
+    for (const Point& P : sh.mem) {
+      const int set = set_of(P);
+      if (set < 0) continue;
+      const int p = P.ou + (set == 2 ? 1 : 0), q = P.ov + (set == 0 ? 1 : 0), pm = set & 1;
+      double* d = &mt[(((size_t)q * 2 + pm) * 5) * kp + p];
+      d[0] = P.G[0][0]; d[kp] = P.G[0][1]; d[2 * kp] = P.G[1][0]; d[3 * kp] = P.G[1][1]; d[4 * kp] = P.w;
+    }
+    std::vector<int32_t> bidx((size_t)nq * kp, -1);   // interior bending point of knot (p, q)
+    for (size_t k = 0; k < sh.bend.size(); ++k) {
+      const Point& P = sh.bend[k];
+      if (P.mask != 0xFF) continue;
+      bidx[(size_t)P.ov * kp + P.ou] = (int32_t)k;
+      for (int e = 0; e < 9; ++e) bt[((size_t)P.ov * 10 + e) * kp + P.ou] = P.L[e];
+      bt[((size_t)P.ov * 10 + 9) * kp + P.ou] = P.w;
+    }
+    const int64_t nr = j1 - j0, cw = c1 - c0;
+    std::vector<double> be((size_t)nr * kNB * cw, 0.0), gwv((size_t)nr * kBSlots * cw, 0.0);
+    for (int j = j0; j < j1; ++j)
+      for (int i = c0; i < c1; ++i)
+        for (int k = 0; k < kBSlots; ++k) {
+          const int p = i + bslot_dp(k), q = j + bslot_dq(k);
+          const int32_t bk = bidx[(size_t)q * kp + p];
+          if (bk < 0) { err = "core: curved tables: missing bending point"; return -1; }
+          const Point& P = sh.bend[bk];
+          gwv[((size_t)(j - j0) * kBSlots + k) * cw + (i - c0)] = P.w * P.L[k];
+          for (int eb = 0; eb < 8; ++eb) {
+            const int blk = block_index(bslot_dp(k) + eb % 3, bslot_dq(k) + eb / 3);
+            if (blk >= 0) be[((size_t)(j - j0) * kNB + blk) * cw + (i - c0)] += P.w * P.L[k] * P.L[eb];
+          }
+        }
+    auto up = [&](double** dst, const std::vector<double>& v) {
+      void* p = dalloc(v.size() * sizeof(double));
+      if (!p || cudaMemcpy(p, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) return false;
+      *dst = static_cast<double*>(p);
+      return true;
+    };
+    if (!up(&ct.mtab, mt) || !up(&ct.btab, bt) || !up(&ct.beta, be) || !up(&ct.gw, gwv)) {
+      err = "core: curved table upload failed";
+      return -7;
+    }
+    ct.table_bytes = sizeof(double) * (mt.size() + bt.size() + be.size() + gwv.size());
+  }
   {
     std::vector<double> tabs(104, 0.0);
     std::memcpy(tabs.data(), ct.S, sizeof(ct.S));
@@ -861,16 +952,18 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
   }
   ct.smem = sizeof(double) * ((size_t)kRing * kRowD + 2 * kStageRow + kPosD + kCstN) + 16;
   if (ct.smem > 227 * 1024) { err = "core: shared memory budget"; return -1; }
-  if (cudaFuncSetAttribute(k_core<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_core<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess) {
+  if (cudaFuncSetAttribute(k_core<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_core<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_core<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess ||
+      cudaFuncSetAttribute(k_core<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess) {
     cudaGetLastError();
     { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
   }
   if (getenv("BSF_CORE_DEBUG")) {
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k_core<false>);
+    cudaFuncGetAttributes(&fa, k_core<false, false>);
     int nb = -1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_core<false>, kThreads, ct.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_core<false, false>, kThreads, ct.smem);
     fprintf(stderr, "k_core: regs %d maxthreads %d local %zu static smem %zu dyn %zu maxdyn %d occ %d\n", fa.numRegs,
             fa.maxThreadsPerBlock, fa.localSizeBytes, fa.sharedSizeBytes, ct.smem, fa.maxDynamicSharedSizeBytes, nb);
   }
@@ -948,8 +1041,15 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
   std::memcpy(A.what, ct.what, sizeof(A.what));
 
   dim3 grid(ct.nstrips, nchunks, nbatch);
-  if (A.xhat) k_core<true><<<grid, kThreads, ct.smem, st>>>(A);
-  else k_core<false><<<grid, kThreads, ct.smem, st>>>(A);
+  A.mtab = ct.mtab; A.btab = ct.btab; A.beta = ct.beta; A.gw = ct.gw; A.kp = ct.kp; A.cw = ct.cw;
+  A.Su = sh.Su; A.Sv = sh.Sv;
+  if (ct.curved) {
+    if (A.xhat) k_core<true, true><<<grid, kThreads, ct.smem, st>>>(A);
+    else k_core<false, true><<<grid, kThreads, ct.smem, st>>>(A);
+  } else {
+    if (A.xhat) k_core<true, false><<<grid, kThreads, ct.smem, st>>>(A);
+    else k_core<false, false><<<grid, kThreads, ct.smem, st>>>(A);
+  }
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
 }
 

@@ -153,6 +153,18 @@ struct CoreTables {
   int32_t* row_ptr = nullptr;                // device copy (owned rows)
   int64_t rp_base = 0, rp_stride = 0;        // row_ptr of (CI0, j) = rp_base + (j - RJ0) * rp_stride
   double* d_tabs = nullptr;                  // device copy of S | LA | LB | LC | what
+  // Curved (non-affine) rest map (round 2): the interior template is the same (it is parametric), but G, w and the
+  // Laplacian coefficients vary per point, and the bending Hessian is no longer one table per CTA.  The kernel
+  // streams them from these device tables ("can be precomputed"):
+  int curved = 0;
+  int64_t kp = 0;                   // knot pitch: Su + 1
+  double* mtab = nullptr;           // [Sv+1][2][5][Su+1]: the two membrane points (minus, plus) of the dual cell of
+                                    // knot (p, q): G00 G01 G10 G11 w
+  double* btab = nullptr;           // [Sv+1][10][Su+1]: the bending point at knot (p, q): L_0..L_8 (G-contracted), w
+  int64_t cw = 0;                   // core columns CI1 - CI0
+  double* beta = nullptr;           // [RJ1-RJ0][23][cw]: sum over the cp's bending points of w L_a L_b (x mu_bd at run time)
+  double* gw = nullptr;             // [RJ1-RJ0][8][cw]: w L_a of the cp's 8 bending slots (x mu_bd at run time)
+  size_t table_bytes = 0;           // bytes of the four tables (read once per call)
 };
 
 // Build (and verify) the interior tables; returns 0 with ok = 1, 1 if the sheet has no usable

@@ -79,7 +79,18 @@ def run(name, sheets, rule, flags, steps=10, warmup=3, params=None, tables=False
     n_cp = q.n_u * q.n_v
     el = (q.n_u - 2) * (q.n_v - 2) * nb
     byt = alg_bytes(n_cp, s.nnzb) * nb
-    tb = (40 * s.n_membrane + 48 * s.n_bending) * nb if tables else 0
+    tb = 0
+    if tables:   # per-point rest tables read per call: the tile kernel's (G, w: 40 B per membrane point; w and five
+        # Laplacian coefficients: 48 B per bending point) on the frame, and k_core's on the interior rectangle
+        # (per knot: two membrane points x 5 doubles and one bending point x 10; per cp: 23 bending blocks + 8
+        # bending weights), chol.hpp-style counts from the pattern sizes
+        i0, i1, j0, j1 = s.core_rect()
+        q = sheets[0]
+        core_cp = (i1 - i0) * (j1 - j0)
+        frac_core = core_cp / (q.n_u * q.n_v)
+        tb = (40 * s.n_membrane + 48 * s.n_bending) * (1.0 - frac_core) + \
+            8 * ((q.n_u - 1) * (q.n_v - 1) * 20 + core_cp * 31)
+        tb = int(tb) * nb
     rule_name = {B.RULE_REDUCED: "reduced", B.RULE_G2_INTERIOR: "g2_interior", B.RULE_G3_FULL: "g3_full"}[rule]
     row = {"config": name, "rule": rule_name,
            "flags": "psd" if flags & B.PROJECT_PSD else "exact", "sheets": nb, "ms_per_call": round(ms, 4),

@@ -72,6 +72,20 @@ def test_curved_rest_general_path():
         _check(sh, x=x, rest=rest, flags=flags, mrule=2, brule=2)
 
 
+@pytest.mark.parametrize("n", [40, 128])
+def test_curved_rest_core_kernel(n):
+    """A curved (non-affine) rest grid runs its interior on k_core with per-point rest tables (G, w, Laplacian
+    coefficients; per-cp bending blocks) and its frame on the tile kernel; parity with the oracle,
+    projected and exact, and the core rectangle is in use."""
+    sh = W.make_sheet(n, 1.0, 5, n_modes=4, amp=5e-3, lam=0.2)
+    rest = W.make_curved_rest(n, n, seed=11)
+    rng = np.random.default_rng(n)
+    x = np.concatenate([rest, np.zeros((n, n, 1))], -1) * 1.02 + rng.normal(0, 0.2 / n, (n, n, 3))
+    for flags in (B.PROJECT_PSD, 0):
+        s, _ = _check(sh, x=x, rest=rest, flags=flags)
+        assert s.core_rect()[1] > 0, s.core_rect()
+
+
 @pytest.mark.parametrize("n_u,n_v", [(5, 5), (7, 6), (37, 19), (130, 9)])
 def test_ragged_and_small(n_u, n_v):
     ku, kv = W.open_uniform_knots(n_u), W.open_uniform_knots(n_v)
