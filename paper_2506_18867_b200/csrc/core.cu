@@ -186,6 +186,10 @@ __device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
   double acc[kNB];
 #pragma unroll
   for (int k = 0; k < kNB; ++k) acc[k] = 0.0;
+  if (CURVED && diag) {   // the per-cp bending blocks are read after the loop: start their trip to L1 now
+#pragma unroll
+    for (int k = 0; k < kNB; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(beta + k * bs));
+  }
   static_for<0, make_template(PI).nslot>([&](auto SI) {
     constexpr int s = decltype(SI)::value;
     constexpr Template T = make_template(PI);
@@ -344,16 +348,18 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
   const int s = p + (set == 2 ? -1 : 0), tq = q + (set == 0 ? -1 : 0);   // anchor
   const double* Sset = cst + kCstS + set * 18;
   double Fu[3] = {0, 0, 0}, Fv[3] = {0, 0, 0};
+  // the 6 structural window entries of the point (V sets: columns iu = 0, 1 x rows jv = 0..2; H sets: iu = 0..2 x
+  // jv = 0, 1); the other 3 entries have d = 0
+  const bool vset = set < 2;
 #pragma unroll
-  for (int jv = 0; jv < 3; ++jv)
+  for (int t = 0; t < 6; ++t) {
+    const int iu = vset ? (t & 1) : (t % 3), jv = vset ? (t >> 1) : (t / 3);
+    const int e = 3 * jv + iu;
+    const double du = Sset[2 * e], dv = Sset[2 * e + 1];
+    const double* C = pos + ((tq + jv - prow0) * kPosC + pos_col(s + iu - (P.i0 - 3))) * 3;
 #pragma unroll
-    for (int iu = 0; iu < 3; ++iu) {
-      const int e = 3 * jv + iu;
-      const double du = Sset[2 * e], dv = Sset[2 * e + 1];
-      const double* C = pos + ((tq + jv - prow0) * kPosC + pos_col(s + iu - (P.i0 - 3))) * 3;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) { Fu[c] = fma(C[c], du, Fu[c]); Fv[c] = fma(C[c], dv, Fv[c]); }
-    }
+    for (int c = 0; c < 3; ++c) { Fu[c] = fma(C[c], du, Fu[c]); Fv[c] = fma(C[c], dv, Fv[c]); }
+  }
   double wq, G00, G01, G10, G11;
   if constexpr (CURVED) {   // this point's G = (dX/d(u,v))^-1 and w from the table of its knot (minus / plus point)
     const double* gm = P.mtab + ((int64_t)min(max(q, 0), P.Sv) * 2 + (set & 1)) * 5 * P.kp + min(max(p, 0), P.Su);
