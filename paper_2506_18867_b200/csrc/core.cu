@@ -90,11 +90,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Bulk-store issuer: lane 0 of gather warp 0.  The issuing thread is the only one that can wait for the
+// Bulk-store issuer: lane 0 of a gather warp.  The issuing thread is the only one that can wait for the
 // store's shared-memory reads (bulk async-groups are per thread), and the gather warps are the ones that
 // overwrite the staging buffer, so the wait sits in a gather warp right before its staging stores (a point
 // warp there would couple the gather to the point phase).
-constexpr int kTma = 0;
+constexpr int kTma = 32;   // warp 1: entry (0, 1), an off-diagonal role (no bending blocks to add, a shorter gather)
 
 // Staged positions: per cp row, the strip's kPosC columns split by column parity ([even | odd] halves of
 // kPosH columns, 3 doubles each), so the lanes of a point set — consecutive knots of one parity, 2 columns
