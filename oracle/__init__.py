@@ -69,6 +69,8 @@ def lib():
             L.oracle_lumped_mass.argtypes = [vp, C.c_double, dp]
             L.oracle_eval_ip.argtypes = [vp, dp, dp, dp, C.c_double, dp, C.POINTER(C.c_uint8), C.c_int, dp, dp, dp,
                                          C.c_int]
+            L.oracle_contact_weights.argtypes = [vp, C.c_int, dp, dp]
+            L.oracle_contact_pullback.argtypes = [vp, C.c_int, dp, C.c_int, ip, dp, dp, dp, dp]
             _lib = L
     return _lib
 
@@ -222,6 +224,28 @@ class Oracle:
                                     _p(E) if energy else None, _p(g) if gradient else None,
                                     _p(vals) if hessian else None, threads))
         return (float(E[0]) if energy else None), g, vals
+
+    def contact_weights(self, uv):
+        """Dense weights W [n_vert, n_v * n_u] of the contact-mesh vertices at parametric points uv [n_vert, 2]
+        (x^alpha = W[alpha] @ C; PAPER.md:588-592)."""
+        uv = np.ascontiguousarray(uv, dtype=np.float64).reshape(-1, 2)
+        W = np.zeros((len(uv), self.n_u * self.n_v))
+        _check(lib().oracle_contact_weights(self._h, len(uv), _p(uv), _p(W)))
+        return W
+
+    def contact_pullback(self, uv, verts, H, g=None):
+        """Chain rule of the contact barrier to the control points: pairs verts [n, 4] (-1 = no
+        DOFs), Hessians H [n, 12, 12], gradients g [n, 12] -> dense Hcp [3 n_cp, 3 n_cp] and gcp [n_v, n_u, 3]."""
+        uv = np.ascontiguousarray(uv, dtype=np.float64).reshape(-1, 2)
+        verts = np.ascontiguousarray(verts, dtype=np.int32).reshape(-1, 4)
+        H = np.ascontiguousarray(H, dtype=np.float64).reshape(-1, 12, 12)
+        n3 = 3 * self.n_u * self.n_v
+        Hcp = np.zeros((n3, n3))
+        gcp = np.zeros((self.n_v, self.n_u, 3))
+        gg = None if g is None else np.ascontiguousarray(g, dtype=np.float64).reshape(-1, 12)
+        _check(lib().oracle_contact_pullback(self._h, len(uv), _p(uv), len(verts), _p(verts, C.c_int32), _p(H),
+                                             None if gg is None else _p(gg), _p(Hcp), _p(gcp)))
+        return Hcp, (gcp if g is not None else None)
 
     def energy_cplx(self, x_re, x_im, flags=0):
         x_re, x_im = self._xslab(x_re), self._xslab(x_im)

@@ -20,8 +20,9 @@
 //   * optional PSD projection of each FBW term by cyclic Jacobi eigen-decomposition (D7);
 //   * scatter into the oracle's own set-union BSR pattern by binary search.
 //
-//  Parity status of each function: see the headers of tests/test_oracle_pins.py and (incremental
-//  potential: lumped mass, inertia, gravity, pinned elimination) tests/test_oracle_ip.py; every function
+//  Parity status of each function: see the headers of tests/test_oracle_pins.py, (incremental
+//  potential: lumped mass, inertia, gravity, pinned elimination) tests/test_oracle_ip.py and (contact pullback)
+//  tests/test_oracle_contact.py; every function
 //  below is pinned (no "parity unpinned" entries) except the membrane stiffness convention
 //  mu_st/mu_sh of oracle_material_from_young (D6, a naming convention: "parity unpinned").
 // =====================================================================================
@@ -857,6 +858,68 @@ int oracle_membrane_A(const double* mu4, const double* f6, int project, double* 
   double f[2][3] = {{f6[0], f6[1], f6[2]}, {f6[3], f6[4], f6[5]}}, A[6][6];
   membrane_A(o, f, project != 0, A);
   for (int i = 0; i < 6; ++i) for (int j = 0; j < 6; ++j) A36[6 * i + j] = A[i][j];
+  return 0;
+}
+
+// ------------------------------------------------------------------ contact pullback
+// A contact-mesh vertex alpha sits at a fixed parametric point (u_alpha, v_alpha) of the sheet and moves with it,
+//   x^alpha = sum_ij N_ij(u_alpha, v_alpha) C^ij       (Eq. `eq: trig mesh node from control
+// points`), so a barrier B(x) on the mesh has, by the chain rule (Eq. `eq: gradient and hessian of
+// contact barrier`; the second-derivative term vanishes because x is linear in C),
+//   dB/dC^i = sum_alpha N_i(alpha) dB/dx^alpha,   d2B/dC^i dC^j = sum_{alpha,beta} N_i(alpha) d2B/dx^alpha dx^beta N_j(beta).
+// The plain route: the dense weight of every control point for every vertex (Cox-de Boor over all bases), and a
+// dense (3 n_cp)^2 Hessian that every pair's 3x3 vertex blocks are scattered into term by term.
+// W: [nvert][n_v * n_u] (row-major, control point a = j n_u + i).
+int oracle_contact_weights(void* h, int nvert, const double* uv, double* W) {
+  auto* o = static_cast<Oracle*>(h);
+  const int nu = o->n_u, nv = o->n_v;
+  std::vector<double> Nu(nu), dNu(nu), ddNu(nu), Nv(nv), dNv(nv), ddNv(nv);
+  for (int a = 0; a < nvert; ++a) {
+    const double u = uv[2 * a], v = uv[2 * a + 1];
+    if (!(u >= 0.0 && u <= o->Su && v >= 0.0 && v <= o->Sv)) return fail("contact vertex outside the parameter domain");
+    cox_de_boor(o->ku.data(), nu + 3, u, Nu.data(), dNu.data(), ddNu.data());
+    cox_de_boor(o->kv.data(), nv + 3, v, Nv.data(), dNv.data(), ddNv.data());
+    for (int j = 0; j < nv; ++j)
+      for (int i = 0; i < nu; ++i) W[(size_t)a * nu * nv + (size_t)j * nu + i] = Nu[i] * Nv[j];
+  }
+  return 0;
+}
+
+// Pairs: verts [npairs][4] (mesh vertex indices, -1 = a slot without control-point DOFs, e.g. an obstacle vertex),
+// H [npairs][12][12] (the barrier Hessian of the pair w.r.t. its 4 vertex slots), gv [npairs][12] (its gradient; may
+// be NULL).  Hcp: dense [3 n_cp][3 n_cp], gcp: [3 n_cp] (may be NULL); both overwritten.
+int oracle_contact_pullback(void* h, int nvert, const double* uv, int npairs, const int32_t* verts, const double* H,
+                            const double* gv, double* Hcp, double* gcp) {
+  auto* o = static_cast<Oracle*>(h);
+  const size_t ncp = (size_t)o->n_u * o->n_v, N3 = 3 * ncp;
+  std::vector<double> W((size_t)nvert * ncp);
+  if (oracle_contact_weights(h, nvert, uv, W.data())) return -1;
+  std::fill(Hcp, Hcp + N3 * N3, 0.0);
+  if (gcp) std::fill(gcp, gcp + N3, 0.0);
+  for (int c = 0; c < npairs; ++c) {
+    for (int sa = 0; sa < 4; ++sa) {
+      const int al = verts[4 * c + sa];
+      if (al < 0) continue;
+      if (al >= nvert) return fail("contact pair vertex out of range");
+      const double* wa = &W[(size_t)al * ncp];
+      for (size_t i = 0; i < ncp; ++i) {
+        if (wa[i] == 0.0) continue;
+        if (gcp && gv)
+          for (int r = 0; r < 3; ++r) gcp[3 * i + r] += wa[i] * gv[12 * c + 3 * sa + r];
+        for (int sb = 0; sb < 4; ++sb) {
+          const int be = verts[4 * c + sb];
+          if (be < 0) continue;
+          const double* wb = &W[(size_t)be * ncp];
+          for (size_t j = 0; j < ncp; ++j) {
+            if (wb[j] == 0.0) continue;
+            for (int r = 0; r < 3; ++r)
+              for (int q = 0; q < 3; ++q)
+                Hcp[(3 * i + r) * N3 + 3 * j + q] += wa[i] * wb[j] * H[(size_t)144 * c + (3 * sa + r) * 12 + 3 * sb + q];
+          }
+        }
+      }
+    }
+  }
   return 0;
 }
 
