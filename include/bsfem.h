@@ -224,6 +224,41 @@ bsf_status bsf_chol_factor(bsf_handle h, const double* d_vals, bsf_stream stream
 bsf_status bsf_chol_solve(bsf_handle h, const double* d_b, double* d_x, bsf_stream stream);
 bsf_status bsf_neumann_solve(bsf_handle h, const double* d_vals_B, const double* d_b, double* d_x, int max_terms,
                              double rtol, double* gate, int* terms, bsf_stream stream);
+
+/* ---- Contact Hessian pullback to the control points (contact.cu) -------------------------
+ * The contact mesh is embedded in the sheet: vertex alpha sits at a fixed parametric point (u_alpha, v_alpha)
+ * and moves as x^alpha = sum_ij N_ij(u_alpha, v_alpha) C^ij (Eq. `eq: trig mesh node from
+ * control points`), so a contact barrier's gradient and Hessian on the mesh pull back by the chain rule
+ * (Eq. `eq: gradient and hessian of contact barrier`), assembled as in Alg. 1 (PAPER.md:
+ * 792-846) in two levels: vertex-pair blocks, then control-point-pair blocks.  Contact detection and the
+ * barrier itself are the caller's.  Whole-sheet device handles only; every output value is summed by one
+ * thread in a fixed order (sorted keys, stable), so results are deterministic.
+ * bsf_contact_mesh: uv: host [n_vert][2] parameters in [0, S_u] x [0, S_v] (the knot-span units of the sheet;
+ *   on a knot line the right limit, as the energies).  Precomputes each vertex's 3x3 control-point window and
+ *   weights.  BSF_E_INVALID_ARG if a vertex lies outside the domain.  Replaces the previous mesh.
+ * bsf_contact_positions: d_xv[n_vert][3] = the vertices' positions for control points d_x [n_v][n_u][3]
+ *   (device).  Asynchronous.
+ * bsf_contact_assemble: n_pairs active pairs; d_verts: device int32 [n_pairs][4] mesh vertex indices (-1 = a slot
+ *   without control-point DOFs, e.g. an obstacle vertex; index >= n_vert -> BSF_E_INVALID_ARG); d_H: device
+ *   [n_pairs][12][12] the barrier Hessian of each pair w.r.t. its 4 vertex slots (row 3 s + r), d_g: device
+ *   [n_pairs][12] its gradient, or NULL.  Outputs: d_grad (device [n_v][n_u][3], or NULL): += the pulled-back
+ *   gradient; d_vals (device, the handle's BSR pattern, or NULL): its diagonal blocks += the pulled-back
+ *   Hessian's diagonal blocks (the paper's H_barrier,d, merged into D); the off-diagonal blocks (H_barrier,od,
+ *   the paper's B) stay in the handle as a BSR matrix of n_v n_u block rows in its own pattern, columns
+ *   ascending, *nnzb_off (host, may be NULL) blocks.  Synchronises `stream` (the pattern's size is data
+ *   dependent).
+ * bsf_contact_get: copies that matrix out: d_row_ptr [n_v n_u + 1], d_col_idx [nnzb_off], d_vals [nnzb_off][9]
+ *   (device; any may be NULL).  Asynchronous.
+ * bsf_contact_neumann_solve: as bsf_neumann_solve with B = that off-diagonal contact matrix and D the matrix of
+ *   the last bsf_chol_factor (e.g. inertia + elasticity + the merged contact diagonal). */
+bsf_status bsf_contact_mesh(bsf_handle h, int n_vert, const double* uv);
+bsf_status bsf_contact_positions(bsf_handle h, const double* d_x, double* d_xv, bsf_stream stream);
+bsf_status bsf_contact_assemble(bsf_handle h, int n_pairs, const int32_t* d_verts, const double* d_H,
+                                const double* d_g, double* d_grad, double* d_vals, int64_t* nnzb_off,
+                                bsf_stream stream);
+bsf_status bsf_contact_get(bsf_handle h, int32_t* d_row_ptr, int32_t* d_col_idx, double* d_vals, bsf_stream stream);
+bsf_status bsf_contact_neumann_solve(bsf_handle h, const double* d_b, double* d_x, int max_terms, double rtol,
+                                     double* gate, int* terms, bsf_stream stream);
 bsf_status bsf_gershgorin(bsf_handle h, const double* d_vals, double* lo, double* hi, bsf_stream stream);
 bsf_status bsf_pcg(bsf_handle h, const double* d_vals, const double* d_b, double* d_x, int max_iter, double rtol,
                    int* iters, double* relres, bsf_stream stream);

@@ -32,7 +32,8 @@ SYMBOLS = ["bsf_material_from_young", "bsf_create", "bsf_destroy", "bsf_set_mate
            "bsf_get_lumped_mass", "bsf_eval_ip_batch", "bsf_bsr_spmv", "bsf_gershgorin", "bsf_pcg",
            "bsf_eval_all_slab", "bsf_set_kernel_timing", "bsf_get_kernel_timing",
            "bsf_last_launch_count", "bsf_poll_status", "bsf_affine_params", "bsf_halo_plan", "bsf_chol_factor",
-           "bsf_chol_solve", "bsf_neumann_solve", "bsf_last_error"]
+           "bsf_chol_solve", "bsf_neumann_solve", "bsf_contact_mesh", "bsf_contact_positions",
+           "bsf_contact_assemble", "bsf_contact_get", "bsf_contact_neumann_solve", "bsf_last_error"]
 
 
 class BsfError(RuntimeError):
@@ -100,6 +101,11 @@ def lib():
         L.bsf_chol_solve.argtypes = [vp, vp, vp, vp]
         L.bsf_neumann_solve.argtypes = [vp, vp, vp, vp, C.c_int, C.c_double, dp, C.POINTER(C.c_int), vp]
         L.bsf_halo_plan.argtypes = [vp, C.c_int, C.c_int, i64p]
+        L.bsf_contact_mesh.argtypes = [vp, C.c_int, dp]
+        L.bsf_contact_positions.argtypes = [vp, vp, vp, vp]
+        L.bsf_contact_assemble.argtypes = [vp, C.c_int, vp, vp, vp, vp, vp, i64p, vp]
+        L.bsf_contact_get.argtypes = [vp, vp, vp, vp, vp]
+        L.bsf_contact_neumann_solve.argtypes = [vp, vp, vp, C.c_int, C.c_double, dp, C.POINTER(C.c_int), vp]
         L.bsf_affine_params.argtypes = [C.c_int, C.c_int, dp, C.POINTER(Material), dp]
         for s in SYMBOLS:
             getattr(L, s).restype = C.c_int if s not in ("bsf_last_error",) else C.c_char_p
@@ -342,6 +348,56 @@ class Sheet:
         _check(lib().bsf_neumann_solve(self._h, _ptr(vals_B), _ptr(b), _ptr(x), int(max_terms), float(rtol),
                                        C.byref(g), C.byref(t), _stream(stream)))
         return x, g.value, t.value
+
+    # ---- contact pullback (Alg. 1)
+    def contact_mesh(self, uv):
+        """Embed a contact mesh: vertex parameters uv [n_vert, 2] (host, in [0, S_u] x [0, S_v])."""
+        uv = np.ascontiguousarray(uv, dtype=np.float64).reshape(-1, 2)
+        self._n_vert = len(uv)
+        _check(lib().bsf_contact_mesh(self._h, len(uv), uv.ctypes.data_as(C.POINTER(C.c_double))))
+
+    def contact_positions(self, x, xv=None, stream=None):
+        """Mesh vertex positions [n_vert, 3] of control points x [n_v, n_u, 3] (CUDA float64)."""
+        import torch
+        xv = torch.empty((self._n_vert, 3), dtype=torch.float64, device=x.device) if xv is None else xv
+        _check(lib().bsf_contact_positions(self._h, _ptr(x), _ptr(xv), _stream(stream)))
+        return xv
+
+    def contact_assemble(self, verts, H, g=None, grad=None, vals=None, stream=None):
+        """Pull the pairs' barrier Hessians H [n, 12, 12] (and gradients g [n, 12]) of mesh vertices verts [n, 4]
+        (CUDA int32, -1 = no DOFs) back to the control points: grad (CUDA [n_v, n_u, 3]) += gradient, vals (the
+        handle's BSR values) diagonal blocks += the diagonal blocks; returns the number of off-diagonal blocks
+        (fetch them with contact_get())."""
+        import torch
+        if verts.dtype != torch.int32 or H.dtype != torch.float64 or (g is not None and g.dtype != torch.float64):
+            raise ValueError("verts must be int32 and H / g float64")
+        n = int(verts.shape[0])
+        nnz = C.c_int64()
+        _check(lib().bsf_contact_assemble(self._h, n, _ptr(verts), _ptr(H), _ptr(g), _ptr(grad), _ptr(vals),
+                                          C.byref(nnz), _stream(stream)))
+        self._contact_nnz = nnz.value
+        return nnz.value
+
+    def contact_get(self, device=None, stream=None):
+        """The off-diagonal contact matrix of the last contact_assemble as CUDA (row_ptr, col_idx, vals[nnz, 3, 3])."""
+        import torch
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        nnz = self._contact_nnz
+        rp = torch.empty(self.n_u * self.n_v + 1, dtype=torch.int32, device=dev)
+        ci = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        va = torch.empty((max(nnz, 1), 3, 3), dtype=torch.float64, device=dev)
+        _check(lib().bsf_contact_get(self._h, _ptr(rp), _ptr(ci), _ptr(va), _stream(stream)))
+        return rp, ci[:nnz], va[:nnz]
+
+    def contact_neumann_solve(self, b, x=None, max_terms=100, rtol=1e-13, stream=None):
+        """(D + B_contact) x = b, D the last chol_factor matrix, B the last contact assembly's off-diagonal blocks
+        (PAPER.md:879-882); returns (x, gate bound, terms)."""
+        import torch
+        x = torch.empty_like(b) if x is None else x
+        gt, t = C.c_double(), C.c_int()
+        _check(lib().bsf_contact_neumann_solve(self._h, _ptr(b), _ptr(x), int(max_terms), float(rtol), C.byref(gt),
+                                               C.byref(t), _stream(stream)))
+        return x, gt.value, t.value
 
     def eval_all_batch_host(self, x_host, x_stage, energy=None, energy_host=None, grad=None, vals=None, params=None,
                             flags=0, chunk=0, stream=None):

@@ -9,9 +9,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("BSF_LIB_PATH", os.path.join(HERE, "libbsfem.so"))
 SOURCES = ["host.cpp", "halo.cpp", "generic.cu", "tile.cu", "core.cu", "frame.cu", "band.cu", "g3.cu", "ip.cu", "solve.cu",
-           "chol.cu", "api.cu"]
+           "chol.cu", "contact.cu", "api.cu"]
 HEADERS = ["host.hpp", "dev.hpp", "fbw.cuh", "tile.hpp", "core.hpp", "frame.hpp", "ip.hpp", "solve.hpp", "g3.hpp",
-           "chol.hpp", "../../include/bsfem.h"]
+           "chol.hpp", "contact.hpp", "../../include/bsfem.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",

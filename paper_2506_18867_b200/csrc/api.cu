@@ -19,6 +19,7 @@
 #include "solve.hpp"
 #include "g3.hpp"
 #include "chol.hpp"
+#include "contact.hpp"
 
 namespace bsf {
 int generic_eval(const GenericTables& t, const double* d_x, const Mat& mat, int flags, int64_t nnzb, int64_t nrows,
@@ -65,6 +66,7 @@ struct bsf_sheet {
   bsf::CgWork cg{};
   bsf::CgGraph cg_graph;
   bsf::CholState chol;                  // banded Cholesky of the Newton matrix (chol.cu)
+  bsf::ContactState contact;            // embedded contact mesh and its pulled-back Hessian (contact.cu)
   cudaStream_t comm_stream = nullptr;   // bsf_eval_all_slab: halo exchange
   cudaEvent_t ev_halo0 = nullptr, ev_halo = nullptr;
   bool solve_ready = false, cg_ready = false;
@@ -81,6 +83,7 @@ struct bsf_sheet {
     cudaSetDevice(device);
     if (sflag_host) cudaFreeHost(sflag_host);
     bsf::chol_free(chol);
+    bsf::contact_free(contact);
     if (tt.side) cudaStreamDestroy(tt.side);
     if (tt.side2) cudaStreamDestroy(tt.side2);
     if (tt.ev_join2) cudaEventDestroy(tt.ev_join2);
@@ -748,6 +751,114 @@ bsf_status bsf_neumann_solve(bsf_handle h, const double* d_vals_B, const double*
     std::string err;
     const bsf::SpmvFn spmv_b = [&](const double* x, double* y, cudaStream_t ss) {
       return bsf::spmv(A, d_vals_B, x, y, nullptr, ss);
+    };
+    if (bsf::neumann_solve(h->chol, spmv_b, d_b, d_x, max_terms, rtol, terms, nullptr, st, err))
+      s = fail(BSF_E_CUDA, err);
+  }
+  if (prev != h->device) cudaSetDevice(prev);
+  return s;
+}
+
+// ---- contact pullback (contact.cu, Alg. 1) ----
+static bsf_status contact_check(bsf_handle h, const char* what) {
+  if (h->host_only) return fail(BSF_E_NO_DEVICE, "host-only handle (device = -1) cannot compute");
+  if (h->sh.r0 != 0 || h->sh.r1 != h->sh.n_v) return fail(BSF_E_INVALID_ARG, std::string(what) + " needs a whole-sheet handle");
+  return BSF_OK;
+}
+
+bsf_status bsf_contact_mesh(bsf_handle h, int n_vert, const double* uv) {
+  if (!h || n_vert < 0 || (n_vert > 0 && !uv)) return fail(BSF_E_INVALID_ARG, "bad arguments");
+  bsf_status s = contact_check(h, "bsf_contact_mesh");
+  if (s != BSF_OK) return s;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  std::string err;
+  const int rc = bsf::contact_mesh(h->contact, h->sh, n_vert, uv, err);
+  if (prev != h->device) cudaSetDevice(prev);
+  return rc ? fail(rc == -7 ? BSF_E_OOM : BSF_E_INVALID_ARG, err) : BSF_OK;
+}
+
+bsf_status bsf_contact_positions(bsf_handle h, const double* d_x, double* d_xv, bsf_stream stream) {
+  if (!h || !d_x || !d_xv) return fail(BSF_E_INVALID_ARG, "null argument");
+  if (!h->contact.ready) return fail(BSF_E_INVALID_ARG, "no contact mesh (bsf_contact_mesh)");
+  if (h->contact.nvert == 0) return BSF_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  const int rc = bsf::contact_positions(h->contact, d_x, d_xv, static_cast<cudaStream_t>(stream));
+  if (prev != h->device) cudaSetDevice(prev);
+  return rc ? fail(BSF_E_CUDA, "contact positions launch failed") : BSF_OK;
+}
+
+bsf_status bsf_contact_assemble(bsf_handle h, int n_pairs, const int32_t* d_verts, const double* d_H,
+                                const double* d_g, double* d_grad, double* d_vals, int64_t* nnzb_off,
+                                bsf_stream stream) {
+  if (!h || n_pairs < 0 || (n_pairs > 0 && (!d_verts || !d_H))) return fail(BSF_E_INVALID_ARG, "bad arguments");
+  if (!h->contact.ready) return fail(BSF_E_INVALID_ARG, "no contact mesh (bsf_contact_mesh)");
+  if ((int64_t)n_pairs * 16 > (int64_t)INT32_MAX) return fail(BSF_E_INVALID_ARG, "too many contact pairs");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  bsf::SolveArgs A;
+  bsf_status s = solve_setup(h, false, A);
+  if (s == BSF_OK) {
+    std::string err;
+    const int rc = bsf::contact_assemble(h->contact, n_pairs, d_verts, d_H, d_g, d_grad, d_vals, h->d_sdiag, nnzb_off,
+                                         static_cast<cudaStream_t>(stream), err);
+    if (rc) s = fail(rc == -7 ? BSF_E_OOM : rc == -1 ? BSF_E_INVALID_ARG : BSF_E_CUDA, err);
+  }
+  if (prev != h->device) cudaSetDevice(prev);
+  return s;
+}
+
+bsf_status bsf_contact_get(bsf_handle h, int32_t* d_row_ptr, int32_t* d_col_idx, double* d_vals, bsf_stream stream) {
+  if (!h) return fail(BSF_E_INVALID_ARG, "null handle");
+  const bsf::ContactState& C = h->contact;
+  if (!C.assembled) return fail(BSF_E_INVALID_ARG, "no contact assembly (bsf_contact_assemble)");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  auto st = static_cast<cudaStream_t>(stream);
+  bool ok = true;
+  if (d_row_ptr)
+    ok &= cudaMemcpyAsync(d_row_ptr, C.row_ptr, sizeof(int32_t) * (C.ncp + 1), cudaMemcpyDeviceToDevice, st) == cudaSuccess;
+  if (d_col_idx && C.nnz)
+    ok &= cudaMemcpyAsync(d_col_idx, C.col, sizeof(int32_t) * C.nnz, cudaMemcpyDeviceToDevice, st) == cudaSuccess;
+  if (d_vals && C.nnz)
+    ok &= cudaMemcpyAsync(d_vals, C.vals, sizeof(double) * 9 * C.nnz, cudaMemcpyDeviceToDevice, st) == cudaSuccess;
+  if (prev != h->device) cudaSetDevice(prev);
+  return ok ? BSF_OK : fail(BSF_E_CUDA, "contact copy failed");
+}
+
+bsf_status bsf_contact_neumann_solve(bsf_handle h, const double* d_b, double* d_x, int max_terms, double rtol,
+                                     double* gate, int* terms, bsf_stream stream) {
+  if (!h || !d_b || !d_x || max_terms < 0 || !(rtol > 0.0)) return fail(BSF_E_INVALID_ARG, "bad arguments");
+  if (!h->chol.factored) return fail(BSF_E_INVALID_ARG, "no factorisation of D (bsf_chol_factor)");
+  if (!h->contact.assembled) return fail(BSF_E_INVALID_ARG, "no contact assembly (bsf_contact_assemble)");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != h->device) cudaSetDevice(h->device);
+  auto st = static_cast<cudaStream_t>(stream);
+  bsf::SolveArgs A;
+  bsf_status s = solve_setup(h, false, A);
+  // B = H_barrier,od in its own pattern (no diagonal blocks: those were merged into D)
+  bsf::SolveArgs B = A;
+  B.row_ptr = h->contact.row_ptr; B.col_idx = h->contact.col; B.diag = nullptr;
+  double lo = 0.0, hi = 0.0;
+  if (s == BSF_OK && h->contact.nnz > 0 && bsf::gershgorin(B, h->contact.vals, h->cg.part, &lo, &hi, st))
+    s = fail(BSF_E_CUDA, "gershgorin failed");
+  const double lmaxB = std::max(std::fabs(lo), std::fabs(hi)), lminD = h->chol.lam_min_D;
+  const double g = lminD > 0.0 ? lmaxB / lminD : INFINITY;
+  if (gate) *gate = g;
+  if (s == BSF_OK && !(g < 1.0))
+    s = fail(BSF_E_INVALID_ARG, "Neumann gate not met: lambda_max(B) / lambda_min(D) bound = " + std::to_string(g) +
+                                    " >= 1 (factorise D + B instead)");
+  if (s == BSF_OK) {
+    std::string err;
+    const double* vb = h->contact.vals;
+    const bsf::SpmvFn spmv_b = [&](const double* x, double* y, cudaStream_t ss) {
+      return bsf::spmv(B, vb, x, y, nullptr, ss);
     };
     if (bsf::neumann_solve(h->chol, spmv_b, d_b, d_x, max_terms, rtol, terms, nullptr, st, err))
       s = fail(BSF_E_CUDA, err);

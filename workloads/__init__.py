@@ -176,3 +176,43 @@ def make_curved_rest(n_u: int, n_v: int, seed: int, L: float = 1.0, bend: float 
 
 def make_config(name: str, **kw):
     return {"C1": make_c1, "C2": make_c2, "C3": make_c3, "C4": make_c4, "C5": make_c5}[name](**kw)
+
+
+@dataclasses.dataclass
+class ContactSet:
+    """Synthetic contact inputs for the pullback: the embedded mesh's vertex parameters uv
+    [n_vert, 2] and the active pairs' vertex slots verts [n, 4] (-1 = an obstacle vertex without DOFs), barrier
+    Hessians H [n, 12, 12] (symmetric PSD) and gradients g [n, 12]."""
+    uv: np.ndarray
+    verts: np.ndarray
+    H: np.ndarray
+    g: np.ndarray
+
+
+def make_contact(sh: Sheet, res: int, n_pairs: int, seed: int, obstacle_frac: float = 0.5,
+                 scale: float = 1.0) -> ContactSet:
+    """The contact mesh of a cloth sheet: a regular triangle mesh with `res` vertices per knot span along each
+    parameter direction (vertex params on a grid, so some lie exactly on knot lines), as when the sheet is
+    tessellated for collision.  Pairs are local, like proximity pairs: self-contact pairs
+    (edge-edge / point-triangle) take 4 vertices within a few mesh steps; a fraction are cloth-vertex vs obstacle
+    (point-triangle with the triangle on a static obstacle: 3 slots -1), as for a sheet falling on a cube."""
+    rng = np.random.default_rng(seed)
+    Su, Sv = sh.n_u - 2, sh.n_v - 2
+    mu, mv = Su * res + 1, Sv * res + 1
+    gu, gv = np.meshgrid(np.linspace(0.0, Su, mu), np.linspace(0.0, Sv, mv))
+    uv = np.stack([gu.reshape(-1), gv.reshape(-1)], axis=1)
+    n_vert = len(uv)
+    a = rng.integers(0, n_vert, n_pairs)
+    ia, ja = a % mu, a // mu
+    verts = np.empty((n_pairs, 4), np.int64)
+    verts[:, 0] = a
+    for s in range(1, 4):
+        di, dj = rng.integers(-3, 4, n_pairs), rng.integers(-3, 4, n_pairs)
+        verts[:, s] = np.clip(ja + dj, 0, mv - 1) * mu + np.clip(ia + di, 0, mu - 1)
+    n_obs = int(round(obstacle_frac * n_pairs))
+    obs = rng.permutation(n_pairs)[:n_obs]
+    verts[obs, 1:] = -1
+    A = rng.normal(size=(n_pairs, 12, 12))
+    H = scale * (A @ A.transpose(0, 2, 1)) / 12.0
+    g = scale * rng.normal(size=(n_pairs, 12))
+    return ContactSet(uv, verts.astype(np.int32), H, g)
