@@ -10,9 +10,11 @@
 // Alg. 1 builds hash maps keyed by vertex pairs, then by control-point pairs, with spatial blocks to limit write
 // conflicts.  The B200 version keeps its two levels but replaces hashing by sorting, which is deterministic and
 // conflict-free: (1) the pairs' vertex-pair blocks are keyed by (alpha, beta), radix-sorted (stable: equal keys
-// keep their emission order) and summed per key in that order (the linear-mesh Hessian H_lin); (2) every H_lin
-// block is spread to the 9 x 9 control-point pairs of the two vertices' windows with weight N_i(alpha) N_j(beta),
-// keyed by (i, j), sorted and summed the same way.  The sorted unique keys ARE the BSR pattern (rows i, columns j
+// keep their emission order) and summed per key in that order (the linear-mesh Hessian H_lin); (1b) the H_lin
+// blocks are grouped by their pair of 3x3 control-point windows (every vertex inside one knot span has the same
+// window), and each window pair's 9 x 9 control-point blocks sum_{vertex pairs} N_i(alpha) N_j(beta) H_lin(alpha,
+// beta) are formed by one CTA; (2) those blocks are keyed by their control-point pair (i, j), sorted and summed the
+// same way.  The sorted unique keys ARE the BSR pattern (rows i, columns j
 // ascending): diagonal blocks (i == j) are added into the elastic matrix's diagonal blocks (the paper's D, which
 // keeps the elastic pattern), the rest is the off-diagonal contact matrix B in its own BSR pattern (the paper's
 // B = H_barrier,od of the Neumann split).  The gradient goes through per-vertex sums and a static control-point
@@ -33,9 +35,15 @@ namespace bsf {
 
 namespace {
 
-constexpr uint64_t kNoKey = ~0ull;
+// Keys are a * m + b with m the number of vertices (control points); the sentinel m^2 (m for the vertex keys) sorts
+// after every valid key, and the radix sort only visits the bits up to it.
+inline int key_bits(uint64_t sentinel) {
+  int b = 1;
+  while (b < 64 && (sentinel >> b)) ++b;
+  return b;
+}
 
-// level 1: (pair, slot a, slot b) -> key (alpha, beta); invalid slots -> kNoKey (sorted to the end)
+// level 1: (pair, slot a, slot b) -> key (alpha, beta); invalid slots -> the sentinel (sorted to the end)
 __global__ void k_emit_lin(const int32_t* __restrict__ verts, int npairs, int nvert, uint64_t* __restrict__ key,
                            uint32_t* __restrict__ val, int* __restrict__ bad) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -44,30 +52,32 @@ __global__ void k_emit_lin(const int32_t* __restrict__ verts, int npairs, int nv
   const int32_t a = verts[4 * c + sa], b = verts[4 * c + sb];
   const bool ok = a < nvert && b < nvert;
   if (!ok && sb == 0) atomicOr(bad, 1);
-  key[t] = (ok && a >= 0 && b >= 0) ? ((uint64_t)(uint32_t)a << 32) | (uint32_t)b : kNoKey;
+  // key a * nvert + b; the sentinel nvert^2 sorts after every valid key within the sorted bit range
+  const uint64_t m = (uint64_t)nvert;
+  key[t] = (ok && a >= 0 && b >= 0) ? (uint64_t)a * m + (uint64_t)b : m * m;
   val[t] = (uint32_t)t;
 }
 
 // run heads of a sorted key array (first of each distinct valid key): flag[t] = 1
-__global__ void k_heads(const uint64_t* __restrict__ key, int64_t n, int32_t* __restrict__ flag) {
+__global__ void k_heads(const uint64_t* __restrict__ key, int64_t n, uint64_t nokey, int32_t* __restrict__ flag) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  flag[t] = (key[t] != kNoKey && (t == 0 || key[t] != key[t - 1])) ? 1 : 0;
+  flag[t] = (key[t] != nokey && (t == 0 || key[t] != key[t - 1])) ? 1 : 0;
 }
 
 // run starts: start[id[t] - 1] = t for heads; start[nruns] = end of the valid keys
 __global__ void k_run_starts(const int32_t* __restrict__ flag, const int32_t* __restrict__ id, int64_t n,
-                             const uint64_t* __restrict__ key, int32_t* __restrict__ start) {
+                             const uint64_t* __restrict__ key, uint64_t nokey, int32_t* __restrict__ start) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   if (flag[t]) start[id[t] - 1] = (int32_t)t;
-  if (key[t] != kNoKey && (t + 1 == n || key[t + 1] == kNoKey)) start[id[t]] = (int32_t)(t + 1);
+  if (key[t] != nokey && (t + 1 == n || key[t + 1] == nokey)) start[id[t]] = (int32_t)(t + 1);
 }
 
 // H_lin[u] = sum over the run of the pairs' (alpha, beta) blocks, in sorted (= emission) order
 __global__ void k_sum_lin(const int32_t* __restrict__ start, int nruns, const uint32_t* __restrict__ val,
-                          const double* __restrict__ H, const uint64_t* __restrict__ key, double* __restrict__ hlin,
-                          int2* __restrict__ ab) {
+                          const double* __restrict__ H, const uint64_t* __restrict__ key, int nvert,
+                          double* __restrict__ hlin, int2* __restrict__ ab) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= nruns) return;
   double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -83,46 +93,81 @@ __global__ void k_sum_lin(const int32_t* __restrict__ start, int nruns, const ui
 #pragma unroll
   for (int e = 0; e < 9; ++e) hlin[9 * (int64_t)u + e] = s[e];
   const uint64_t kk = key[start[u]];
-  ab[u] = make_int2((int)(kk >> 32), (int)(kk & 0xffffffffu));
+  ab[u] = make_int2((int)(kk / (uint64_t)nvert), (int)(kk % (uint64_t)nvert));
 }
 
-// level 2: (u, window entry ea of alpha, eb of beta) -> key (i, j) of the control points; zero weights skipped
-__global__ void k_emit_cp(const int2* __restrict__ ab, int nruns, const int2* __restrict__ vwin,
-                          const double* __restrict__ vw, int nvert, int n_u, uint64_t* __restrict__ key,
-                          uint32_t* __restrict__ val) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int64_t)nruns * 81) return;
-  const int u = (int)(t / 81), e = (int)(t - 81 * (int64_t)u), ea = e / 9, eb = e - 9 * (e / 9);
-  const int2 p = ab[u];
-  const double wa = vw[(int64_t)ea * nvert + p.x], wb = vw[(int64_t)eb * nvert + p.y];
-  if (wa == 0.0 || wb == 0.0) { key[t] = kNoKey; val[t] = (uint32_t)t; return; }
-  const int2 oa = vwin[p.x], ob = vwin[p.y];
-  const uint32_t i = (uint32_t)((oa.y + ea / 3) * n_u + oa.x + ea % 3);
-  const uint32_t j = (uint32_t)((ob.y + eb / 3) * n_u + ob.x + eb % 3);
-  key[t] = ((uint64_t)i << 32) | j;
+// level 1b: the vertex-pair blocks grouped by their pair of control-point windows (all vertices inside one knot
+// span share a window), so that level 2 emits 81 control-point pairs per window pair, not per vertex pair
+__global__ void k_emit_wp(const int2* __restrict__ ab, int nlin, const int2* __restrict__ vwin, int n_u, int ncp,
+                          uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= nlin) return;
+  const int2 p = ab[u], oa = vwin[p.x], ob = vwin[p.y];
+  key[u] = (uint64_t)(oa.y * n_u + oa.x) * (uint64_t)ncp + (uint64_t)(ob.y * n_u + ob.x);
+  val[u] = (uint32_t)u;
+}
+
+// window pair w: its run of vertex pairs [wps[w], wps[w+1]) in wpu, and its two window origins (linear cp index)
+__global__ void k_wp_info(const uint64_t* __restrict__ key, const int32_t* __restrict__ start, int nwp, int ncp,
+                          int32_t* __restrict__ wps, int2* __restrict__ wpo) {
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= nwp) return;
+  const uint64_t kk = key[start[w]];
+  wpo[w] = make_int2((int)(kk / (uint64_t)ncp), (int)(kk % (uint64_t)ncp));
+  wps[w] = start[w];
+  if (w == nwp - 1) wps[nwp] = start[nwp];
+}
+
+// level 2, one CTA per window pair w, one thread per pair of window entries (ea, eb): the 3x3 block
+// sum over w's vertex pairs of N_ea(alpha) N_eb(beta) H_lin(alpha, beta), in run order, and its key (i, j),
+// emitted when some vertex pair of w has both weights nonzero (the oracle's structural pattern)
+__global__ void __launch_bounds__(96) k_wp_blocks(const int32_t* __restrict__ wps, const uint32_t* __restrict__ wpu,
+                                                  const int2* __restrict__ wpo, const int2* __restrict__ ab,
+                                                  const double* __restrict__ hlin, const double* __restrict__ vw,
+                                                  int nvert, int n_u, int ncp, double* __restrict__ wblk,
+                                                  uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+  const int w = blockIdx.x, e = threadIdx.x;
+  if (e >= 81) return;
+  const int ea = e / 9, eb = e - 9 * (e / 9);
+  double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  bool nz = false;
+  for (int k = wps[w]; k < wps[w + 1]; ++k) {
+    const uint32_t u = wpu[k];
+    const int2 p = ab[u];
+    const double wa = vw[(int64_t)ea * nvert + p.x], wb = vw[(int64_t)eb * nvert + p.y];
+    nz |= wa != 0.0 && wb != 0.0;
+    const double wt = wa * wb;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) s[q] = fma(wt, hlin[9 * (int64_t)u + q], s[q]);
+  }
+  const int64_t t = 81 * (int64_t)w + e;
+#pragma unroll
+  for (int q = 0; q < 9; ++q) wblk[9 * t + q] = s[q];
+  const uint64_t m = (uint64_t)ncp;
   val[t] = (uint32_t)t;
+  if (!nz) { key[t] = m * m; return; }
+  const int2 o = wpo[w];
+  const uint32_t i = (uint32_t)(o.x + (ea / 3) * n_u + ea % 3);
+  const uint32_t j = (uint32_t)(o.y + (eb / 3) * n_u + eb % 3);
+  key[t] = (uint64_t)i * m + j;
 }
 
-// Control-point blocks: sum w_i(alpha) w_j(beta) H_lin[u] over the run; diagonal blocks go into the elastic
-// matrix's diagonal (vals_d, nullable), off-diagonal ones into the contact BSR (row counts for the pattern).
+// Control-point blocks: sum of the run's window-pair blocks in sorted order; diagonal blocks go into the elastic
+// matrix's diagonal (vals_d, nullable), off-diagonal ones into the contact BSR at their rank.
 __global__ void k_sum_cp(const int32_t* __restrict__ start, int nruns, const uint32_t* __restrict__ val,
-                         const uint64_t* __restrict__ key, const int2* __restrict__ ab, const double* __restrict__ hlin,
-                         const double* __restrict__ vw, int nvert, const int32_t* __restrict__ offd_rank,
-                         double* __restrict__ bvals, int32_t* __restrict__ bcol, double* __restrict__ vals_d,
-                         const int32_t* __restrict__ diag_pos) {
+                         const uint64_t* __restrict__ key, const double* __restrict__ wblk, int ncp,
+                         const int32_t* __restrict__ offd_rank, double* __restrict__ bvals, int32_t* __restrict__ bcol,
+                         double* __restrict__ vals_d, const int32_t* __restrict__ diag_pos) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nruns) return;
   double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int k = start[r]; k < start[r + 1]; ++k) {
-    const uint32_t v = val[k];
-    const int u = (int)(v / 81), e = (int)(v - 81 * (v / 81)), ea = e / 9, eb = e - 9 * (e / 9);
-    const int2 p = ab[u];
-    const double w = vw[(int64_t)ea * nvert + p.x] * vw[(int64_t)eb * nvert + p.y];
+    const double* b = wblk + 9 * (int64_t)val[k];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) s[q] = fma(w, hlin[9 * (int64_t)u + q], s[q]);
+    for (int q = 0; q < 9; ++q) s[q] += b[q];
   }
   const uint64_t kk = key[start[r]];
-  const int i = (int)(kk >> 32), j = (int)(kk & 0xffffffffu);
+  const int i = (int)(kk / (uint64_t)ncp), j = (int)(kk % (uint64_t)ncp);
   if (i == j) {
     if (vals_d) {
       double* d = vals_d + 9 * (int64_t)diag_pos[i];
@@ -137,28 +182,26 @@ __global__ void k_sum_cp(const int32_t* __restrict__ start, int nruns, const uin
   for (int q = 0; q < 9; ++q) bvals[9 * (int64_t)o + q] = s[q];
 }
 
-__global__ void k_offd_flags(const uint64_t* __restrict__ key, const int32_t* __restrict__ start, int nruns,
-                             int32_t* __restrict__ flag, int32_t* __restrict__ rowcnt) {
+__global__ void k_offd_flags(const uint64_t* __restrict__ key, const int32_t* __restrict__ start, int nruns, int ncp,
+                             int32_t* __restrict__ flag) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nruns) return;
   const uint64_t kk = key[start[r]];
-  const int i = (int)(kk >> 32), j = (int)(kk & 0xffffffffu);
-  flag[r] = i != j;
-  (void)rowcnt;
+  flag[r] = kk / (uint64_t)ncp != kk % (uint64_t)ncp;
 }
 
 // row_ptr of the off-diagonal contact BSR from the sorted unique keys (rows ascending): one thread per row
 // finds its first entry by binary search over the off-diagonal ranks
 __global__ void k_row_ptr(const uint64_t* __restrict__ key, const int32_t* __restrict__ start,
                           const int32_t* __restrict__ flag, const int32_t* __restrict__ rank, int nruns, int nrows,
-                          int32_t* __restrict__ row_ptr) {
+                          int ncp, int32_t* __restrict__ row_ptr) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a > nrows) return;
   // first run whose row is >= a
   int lo = 0, hi = nruns;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if ((int)(key[start[mid]] >> 32) < a) lo = mid + 1; else hi = mid;
+    if ((int)(key[start[mid]] / (uint64_t)ncp) < a) lo = mid + 1; else hi = mid;
   }
   // off-diagonal entries before run lo
   row_ptr[a] = lo < nruns ? rank[lo] : (nruns > 0 ? rank[nruns - 1] + flag[nruns - 1] : 0);
@@ -171,7 +214,7 @@ __global__ void k_emit_vert(const int32_t* __restrict__ verts, int npairs, int n
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)npairs * 4) return;
   const int32_t a = verts[t];
-  key[t] = (a >= 0 && a < nvert) ? (uint64_t)(uint32_t)a : kNoKey;
+  key[t] = (a >= 0 && a < nvert) ? (uint64_t)a : (uint64_t)nvert;
   val[t] = (uint32_t)t;
 }
 
@@ -241,7 +284,8 @@ bool grow(T** p, int64_t* cap, int64_t need) {
 void contact_free(ContactState& S) {
   for (void* p : {(void*)S.vwin, (void*)S.vw, (void*)S.cp_ptr, (void*)S.cp_list, (void*)S.k1, (void*)S.k2,
                   (void*)S.v1, (void*)S.v2, (void*)S.flag, (void*)S.id, (void*)S.start, (void*)S.hlin, (void*)S.ab,
-                  (void*)S.rank, (void*)S.row_ptr, (void*)S.col, (void*)S.vals, (void*)S.gv, (void*)S.tmp, (void*)S.bad})
+                  (void*)S.rank, (void*)S.row_ptr, (void*)S.col, (void*)S.vals, (void*)S.gv, (void*)S.tmp, (void*)S.bad,
+                  (void*)S.wps, (void*)S.wpu, (void*)S.wpo, (void*)S.wblk})
     cudaFree(p);
   S = ContactState();
 }
@@ -296,9 +340,10 @@ int contact_positions(const ContactState& S, const double* d_x, double* d_xv, cu
 // sorts (key, val) of n entries with CUB (stable LSD radix sort), then marks the runs of equal valid keys:
 // returns the number of runs (host), run starts in S.start[0 .. nruns] (device)
 static int sort_runs(ContactState& S, uint64_t* k_in, uint32_t* v_in, uint64_t* k_out, uint32_t* v_out, int64_t n,
-                     cudaStream_t st, int* nruns, std::string& err) {
+                     uint64_t nokey, cudaStream_t st, int* nruns, std::string& err) {
+  const int nbits = key_bits(nokey);
   size_t tb = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, v_in, v_out, (int)n, 0, 64, st);
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, v_in, v_out, (int)n, 0, nbits, st);
   size_t tb2 = 0;
   cub::DeviceScan::InclusiveSum(nullptr, tb2, S.flag, S.id, (int)n, st);
   if (!grow(&S.tmp, &S.tmp_cap, (int64_t)std::max(tb, tb2)) || !grow(&S.flag, &S.flag_cap, n) ||
@@ -307,11 +352,11 @@ static int sort_runs(ContactState& S, uint64_t* k_in, uint32_t* v_in, uint64_t* 
     return -7;
   }
   tb = (size_t)S.tmp_cap;
-  if (cub::DeviceRadixSort::SortPairs(S.tmp, tb, k_in, k_out, v_in, v_out, (int)n, 0, 64, st) != cudaSuccess) {
+  if (cub::DeviceRadixSort::SortPairs(S.tmp, tb, k_in, k_out, v_in, v_out, (int)n, 0, nbits, st) != cudaSuccess) {
     err = "radix sort failed";
     return -6;
   }
-  k_heads<<<nblk(n, 256), 256, 0, st>>>(k_out, n, S.flag);
+  k_heads<<<nblk(n, 256), 256, 0, st>>>(k_out, n, nokey, S.flag);
   tb2 = (size_t)S.tmp_cap;
   if (cub::DeviceScan::InclusiveSum(S.tmp, tb2, S.flag, S.id, (int)n, st) != cudaSuccess) { err = "scan failed"; return -6; }
   int last = 0;
@@ -321,7 +366,7 @@ static int sort_runs(ContactState& S, uint64_t* k_in, uint32_t* v_in, uint64_t* 
     return -6;
   }
   *nruns = last;
-  if (last > 0) k_run_starts<<<nblk(n, 256), 256, 0, st>>>(S.flag, S.id, n, k_out, S.start);
+  if (last > 0) k_run_starts<<<nblk(n, 256), 256, 0, st>>>(S.flag, S.id, n, k_out, nokey, S.start);
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
 }
 
@@ -343,7 +388,7 @@ int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const 
       return -7;
     }
     k_emit_lin<<<nblk(n1, 256), 256, 0, st>>>(d_verts, npairs, S.nvert, S.k1, S.v1, S.bad);
-    if ((rc = sort_runs(S, S.k1, S.v1, S.k2, S.v2, n1, st, &nlin, err))) return rc;
+    if ((rc = sort_runs(S, S.k1, S.v1, S.k2, S.v2, n1, (uint64_t)S.nvert * S.nvert, st, &nlin, err))) return rc;
     int bad = 0;
     if (cudaMemcpy(&bad, S.bad, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) { err = "copy"; return -6; }
     if (bad) { err = "contact pair vertex index >= n_vert"; return -1; }
@@ -351,22 +396,38 @@ int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const 
   }
   if (nlin > 0) {
     if (!grow(&S.hlin, &S.hlin_cap, 9 * (int64_t)nlin) || !grow(&S.ab, &S.ab_cap, nlin)) { err = "allocation"; return -7; }
-    k_sum_lin<<<nblk(nlin, 128), 128, 0, st>>>(S.start, nlin, S.v2, d_H, S.k2, S.hlin, S.ab);
+    k_sum_lin<<<nblk(nlin, 128), 128, 0, st>>>(S.start, nlin, S.v2, d_H, S.k2, S.nvert, S.hlin, S.ab);
+  }
+  // ---- level 1b: window pairs
+  int nwp = 0;
+  if (nlin > 0) {
+    k_emit_wp<<<nblk(nlin, 256), 256, 0, st>>>(S.ab, nlin, S.vwin, S.n_u, S.ncp, S.k1, S.v1);
+    if ((rc = sort_runs(S, S.k1, S.v1, S.k2, S.v2, nlin, (uint64_t)S.ncp * S.ncp, st, &nwp, err))) return rc;
+    if (!grow(&S.wps, &S.wps_cap, nwp + 1) || !grow(&S.wpo, &S.wpo_cap, nwp) || !grow(&S.wpu, &S.wpu_cap, nlin)) {
+      err = "allocation";
+      return -7;
+    }
+    k_wp_info<<<nblk(nwp, 256), 256, 0, st>>>(S.k2, S.start, nwp, S.ncp, S.wps, S.wpo);
+    if (cudaMemcpyAsync(S.wpu, S.v2, sizeof(uint32_t) * nlin, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+      err = "copy";
+      return -6;
+    }
   }
   // ---- level 2: control-point blocks
-  const int64_t n2 = (int64_t)nlin * 81;
+  const int64_t n2 = (int64_t)nwp * 81;
   int ncpb = 0;
   if (n2 > 0) {
     if (!grow(&S.k1, &S.k1_cap, n2) || !grow(&S.v1, &S.v1_cap, n2) || !grow(&S.k2, &S.k2_cap, n2) ||
         !grow(&S.v2, &S.v2_cap, n2)) { err = "allocation"; return -7; }
-    k_emit_cp<<<nblk(n2, 256), 256, 0, st>>>(S.ab, nlin, S.vwin, S.vw, S.nvert, S.n_u, S.k1, S.v1);
-    if ((rc = sort_runs(S, S.k1, S.v1, S.k2, S.v2, n2, st, &ncpb, err))) return rc;
+    if (!grow(&S.wblk, &S.wblk_cap, 9 * n2)) { err = "allocation"; return -7; }
+    k_wp_blocks<<<nwp, 96, 0, st>>>(S.wps, S.wpu, S.wpo, S.ab, S.hlin, S.vw, S.nvert, S.n_u, S.ncp, S.wblk, S.k1, S.v1);
+    if ((rc = sort_runs(S, S.k1, S.v1, S.k2, S.v2, n2, (uint64_t)S.ncp * S.ncp, st, &ncpb, err))) return rc;
   }
   if (ncpb > 0) {
     // off-diagonal ranks (exclusive scan of the off-diagonal flags of the runs), pattern, values
     if (!grow(&S.rank, &S.rank_cap, ncpb + 1)) { err = "allocation"; return -7; }
     int32_t* offflag = S.flag;   // reuse: the run flags of the level-2 sort are no longer needed
-    k_offd_flags<<<nblk(ncpb, 256), 256, 0, st>>>(S.k2, S.start, ncpb, offflag, nullptr);
+    k_offd_flags<<<nblk(ncpb, 256), 256, 0, st>>>(S.k2, S.start, ncpb, S.ncp, offflag);
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, offflag, S.rank, ncpb, st);
     if (!grow(&S.tmp, &S.tmp_cap, (int64_t)tb)) { err = "allocation"; return -7; }
@@ -381,9 +442,9 @@ int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const 
       err = "allocation";
       return -7;
     }
-    k_sum_cp<<<nblk(ncpb, 128), 128, 0, st>>>(S.start, ncpb, S.v2, S.k2, S.ab, S.hlin, S.vw, S.nvert, S.rank, S.vals,
-                                              S.col, d_vals, d_diag_pos);
-    k_row_ptr<<<nblk(S.ncp + 1, 256), 256, 0, st>>>(S.k2, S.start, offflag, S.rank, ncpb, S.ncp, S.row_ptr);
+    k_sum_cp<<<nblk(ncpb, 128), 128, 0, st>>>(S.start, ncpb, S.v2, S.k2, S.wblk, S.ncp, S.rank, S.vals, S.col,
+                                              d_vals, d_diag_pos);
+    k_row_ptr<<<nblk(S.ncp + 1, 256), 256, 0, st>>>(S.k2, S.start, offflag, S.rank, ncpb, S.ncp, S.ncp, S.row_ptr);
   } else if (cudaMemsetAsync(S.row_ptr, 0, sizeof(int32_t) * (S.ncp + 1), st) != cudaSuccess) {
     err = "memset";
     return -6;
@@ -396,7 +457,7 @@ int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const 
     if (cudaMemsetAsync(S.gv, 0, sizeof(double) * 3 * (size_t)S.nvert, st) != cudaSuccess) { err = "memset"; return -6; }
     k_emit_vert<<<nblk(n3, 256), 256, 0, st>>>(d_verts, npairs, S.nvert, S.k1, S.v1);
     int nv = 0;
-    if ((rc = sort_runs(S, S.k1, S.v1, S.k2, S.v2, n3, st, &nv, err))) return rc;
+    if ((rc = sort_runs(S, S.k1, S.v1, S.k2, S.v2, n3, (uint64_t)S.nvert, st, &nv, err))) return rc;
     if (nv > 0) k_sum_vert<<<nblk(nv, 128), 128, 0, st>>>(S.start, nv, S.v2, S.k2, d_g, S.gv);
     k_grad_cp<<<nblk(S.ncp, 128), 128, 0, st>>>(S.cp_ptr, S.cp_list, S.vw, S.nvert, S.gv, S.ncp, d_grad_cp);
   }

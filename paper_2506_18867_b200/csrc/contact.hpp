@@ -23,6 +23,10 @@ struct ContactState {
   int32_t *flag = nullptr, *id = nullptr, *start = nullptr, *rank = nullptr;
   double* hlin = nullptr;      // [unique vertex pairs][9] H_lin blocks
   int2* ab = nullptr;          // [unique vertex pairs] (alpha, beta)
+  int32_t* wps = nullptr;      // [window pairs + 1] run starts into wpu
+  uint32_t* wpu = nullptr;     // [unique vertex pairs] vertex pairs sorted by window pair
+  int2* wpo = nullptr;         // [window pairs] the two window origins (linear control-point index)
+  double* wblk = nullptr;      // [window pairs][81][9] the window pairs' control-point blocks
   int32_t *row_ptr = nullptr, *col = nullptr;
   double* vals = nullptr;
   double* gv = nullptr;        // [nvert][3] per-vertex gradient
@@ -30,7 +34,7 @@ struct ContactState {
   int* bad = nullptr;          // a pair vertex index >= nvert was seen
   int64_t k1_cap = 0, k2_cap = 0, v1_cap = 0, v2_cap = 0, flag_cap = 0, id_cap = 0, start_cap = 0, rank_cap = 0,
           hlin_cap = 0, ab_cap = 0, row_cap = 0, col_cap = 0, vals_cap = 0, gv_cap = 0, tmp_cap = 0,
-          bad_cap = 0;
+          bad_cap = 0, wps_cap = 0, wpu_cap = 0, wpo_cap = 0, wblk_cap = 0;
   int64_t nnz = 0;             // off-diagonal blocks of the last assembly
   int nrows = 0;
 };
