@@ -54,7 +54,7 @@ struct CoreArgs {
   int n_u, xlo, xhi, r0;
   int CI0, CI1, RJ0, RJ1, nstrips, nchunks;
   int JA, JB;              // rows of this launch ([RJ0, RJ1) or a sub-range; addressing stays relative to RJ0)
-  int project, flags, dbg;
+  int project, flags, dbg, layout;
   unsigned long long* sflag;   // singular-stretch word (fbw.cuh)
   EFinal ef;                   // fused energy reduction of the call
   double G00, G01, G10, G11, detJ, mu1, mu2, mush, mubd;
@@ -94,7 +94,36 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // store's shared-memory reads (bulk async-groups are per thread), and the gather warps are the ones that
 // overwrite the staging buffer, so the wait sits in a gather warp right before its staging stores (a point
 // warp there would couple the gather to the point phase).
-constexpr int kTma = 32;   // warp 1: entry (0, 1), an off-diagonal role (no bending blocks to add, a shorter gather)
+// Warp layouts.  Warps are issued by the SM sub-partition (scheduler) warp % 4, so which role sits on which warp
+// decides how the per-step work is spread over the four schedulers.  A layout gives the gather warps' block
+// entries (role = 3 r + c), the warp that issues the bulk stores, the point-item block of each point warp
+// (items 30 pw .. 30 pw + 29: pw 0-3 membrane, 4 mixed, 5-6 bending) and its gradient rounds
+// [g0, g0 + gn) (round = 3 parity + component).  Selected with BSF_CORE_LAYOUT (default 5: C4 k_core 451 us with layout 1, 444 with 0, 431 with 4, 429 with 5;
+// the per-warp busy cycles of scripts/core_timers.py --c4 show the gather warps as the limit from layout 4 on).
+struct CoreLayout {
+  int8_t role[kGatherWarps];
+  int8_t tma_warp;
+  int8_t pw[kPointWarps];
+  int8_t g0[kPointWarps], gn[kPointWarps];
+};
+__constant__ CoreLayout kLayouts[8] = {
+    // 0: diagonal roles on warps 0-2, one gradient round on every point warp but warp 12
+    {{0, 4, 8, 1, 2, 3, 5, 6, 7}, 3, {0, 1, 2, 3, 4, 5, 6}, {0, 1, 2, 0, 3, 4, 5}, {1, 1, 1, 0, 1, 1, 1}},
+    // 1: the round-2 layout: role = warp, bulk stores on warp 1, gradient rounds on warps 9-14
+    {{0, 1, 2, 3, 4, 5, 6, 7, 8}, 1, {0, 1, 2, 3, 4, 5, 6}, {0, 1, 2, 3, 4, 5, 0}, {1, 1, 1, 1, 1, 1, 0}},
+    // 2: as 0, the mixed item block on warp 12, three gradient rounds on each bending warp
+    {{0, 4, 8, 1, 2, 3, 5, 6, 7}, 3, {0, 1, 2, 4, 3, 5, 6}, {0, 0, 0, 0, 0, 0, 3}, {0, 0, 0, 0, 0, 3, 3}},
+    // 3: off-diagonal roles on scheduler 0 (warps 0, 4, 8), diagonal ones on warps 1-3; point warps as 2
+    {{1, 0, 4, 8, 2, 3, 5, 6, 7}, 5, {0, 1, 2, 4, 3, 5, 6}, {0, 0, 0, 0, 0, 0, 3}, {0, 0, 0, 0, 0, 3, 3}},
+    // 4: as 3, two gradient rounds on each bending warp and one on warps 10, 11
+    {{1, 0, 4, 8, 2, 3, 5, 6, 7}, 5, {0, 1, 2, 4, 3, 5, 6}, {0, 4, 5, 0, 0, 0, 2}, {0, 1, 1, 0, 0, 2, 2}},
+    // 5: as 4, a bending block on warp 12 (scheduler 0) and the mixed block on warp 14
+    {{1, 0, 4, 8, 2, 3, 5, 6, 7}, 5, {0, 1, 2, 5, 3, 4, 6}, {0, 4, 5, 0, 0, 0, 2}, {0, 1, 1, 2, 0, 0, 2}},
+    // 6: as 5, the gradient rounds on warps 9, 10, 12 (two), 15 (two)
+    {{1, 0, 4, 8, 2, 3, 5, 6, 7}, 5, {0, 1, 2, 5, 3, 4, 6}, {5, 4, 0, 0, 0, 0, 2}, {1, 1, 0, 2, 0, 0, 2}},
+    // 7: as 5, one gradient round on warp 12 and three on warp 15
+    {{1, 0, 4, 8, 2, 3, 5, 6, 7}, 5, {0, 1, 2, 5, 3, 4, 6}, {0, 4, 5, 0, 0, 0, 1}, {0, 1, 1, 1, 0, 0, 3}},
+};
 
 // Staged positions: per cp row, the strip's kPosC columns split by column parity ([even | odd] halves of
 // kPosH columns, 3 doubles each), so the lanes of a point set — consecutive knots of one parity, 2 columns
@@ -182,7 +211,7 @@ __device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
                                             const uint32_t (&base1)[4], int o_rc, int o_cr, bool diag,
                                             const double* __restrict__ cst, double* st_lane, bool active,
                                             uint32_t bar, uint32_t parity, double dshift,
-                                            const double* __restrict__ beta, int64_t bs, double mubd) {
+                                            const double* __restrict__ beta, int64_t bs, double mubd, bool tma) {
   double acc[kNB];
 #pragma unroll
   for (int k = 0; k < kNB; ++k) acc[k] = 0.0;
@@ -225,7 +254,7 @@ __device__ __forceinline__ void gather_role(const uint32_t (&base0)[4],
     acc[block_index(0, 0)] += dshift;
   }
   if (!st_lane) return;
-  if (PI == 0 && threadIdx.x == kTma) {   // the previous step's bulk store has read the staging buffer
+  if (PI == 0 && tma) {   // the previous step's bulk store has read the staging buffer
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(bar) : "memory");
   }
@@ -487,20 +516,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
   }
 
   double e_acc = 0.0;
-  // ---- warp roles: warps 0-8 gather block entry (r, c) = (warp / 3, warp % 3) for both parities (warp 0,
-  // entry (0, 0), also waits for the bulk stores); warps 9-15 evaluate the quadrature points of the next step
+  // ---- warp roles: warps 0-8 gather block entry (r, c) = warp_role(warp) for both parities (warp 3, entry
+  // (0, 1), also waits for the bulk stores); warps 9-15 evaluate the quadrature points of the next step
   // (7 x 30 lanes = the 210 points).  (Measured alternative, slower: one warp per entry pair (r,c) + (c,r) and
   // parity, sharing the record loads (A~uu, A~vv symmetric, A~vu[rc] = A~uv[cr]); 46 accumulators per lane and
   // twice the gather code: 705 vs 495 us on C4.  Also slower: a separate diagonal-role variant loading
   // A~uv[rr] once, 562 us, from the register allocation of the extra instantiations.)
   const int warp = tid >> 5, lane = tid & 31;
-  const int role = warp < kGatherWarps ? warp : 0;
+  const CoreLayout& LY = kLayouts[A.layout];
+  const int role = warp < kGatherWarps ? LY.role[warp] : 0;
+  const int tma = 32 * LY.tma_warp;   // the bulk-store issuing thread
   const int rr = role / 3, cc = role - 3 * (role / 3);
   const bool diag = rr == cc;
   const int o_uu = sym3(rr, cc) * kKH;
   const int o_rc = (12 + 3 * rr + cc) * kKH, o_cr = (12 + 3 * cc + rr) * kKH;
   const int h = lane >> 4, m = lane & 15;
-  const int pw = warp - kGatherWarps;   // point warp index
+  const int pw = warp >= kGatherWarps ? LY.pw[warp - kGatherWarps] : -1;   // point item block
 
   CT_MARK(TK1);
   if (ja < jb) {
@@ -549,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
       if (k >= 0) {
         // (b) profiling mode without the gather: the issuing thread releases the staging buffer here (else the
         // gather warp 0 does, right before its staging stores)
-        if (tid == kTma && (A.dbg & 6)) {
+        if (tid == tma && (A.dbg & 6)) {
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(bar) : "memory");
         }
@@ -593,16 +624,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
                                         : nullptr;
             if (PI == 0)
               gather_role<0, CURVED>(base0, base1, orc, ocr, diag, cst, st_lane, active, bar, par, dshift, bsrc, A.cw,
-                                     P.mubd);
+                                     P.mubd, tid == tma);
             else
               gather_role<1, CURVED>(base0, base1, orc, ocr, diag, cst, st_lane, active, bar, par, dshift, bsrc, A.cw,
-                                     P.mubd);
+                                     P.mubd, tid == tma);
           }
         }
       }
-      // (c') gradient rows of step k: six point warps take one (parity, component) round each
-      if (k >= 0 && (gout || IP) && warp >= kGatherWarps && warp < kGatherWarps + 6 && !(A.dbg & 2)) {
-        const int PI = (warp - kGatherWarps) / 3, rg = (warp - kGatherWarps) % 3;
+      // (c') gradient rows of step k: the point warps take the six (parity, component) rounds (layout)
+      const int gr0 = warp >= kGatherWarps ? LY.g0[warp - kGatherWarps] : 0;
+      const int gr1 = warp >= kGatherWarps ? gr0 + LY.gn[warp - kGatherWarps] : 0;
+#pragma unroll 1
+      for (int gw = gr0; gw < gr1; ++gw)
+      if (k >= 0 && (gout || IP) && !(A.dbg & 2)) {
+        const int PI = gw / 3, rg = gw % 3;
         const int jr = j + h;
         const int sigma = (PI + jr + i0) & 1;
         const int i = i0 + 2 * m + sigma;
@@ -661,7 +696,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
       }
 #endif
       // (d) bulk stores of the step's rows (head / tail doubles off the 16-B grid by plain stores)
-      if (k >= 0 && vals && tid >= kTma && tid < kTma + 5) {
+      if (k >= 0 && vals && tid >= tma && tid < tma + 5) {
         for (int hh = 0; hh < kRows; ++hh) {
           const int jr2 = j + hh;
           if (jr2 >= jb) break;
@@ -672,19 +707,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
           const int64_t nd = (int64_t)(i1 - i0) * (kNB * 9);
           const int head = pad;                                  // 1 double if gd is 8 mod 16
           const int tail = (int)((nd - head) & 1);               // 1 double if the end is 8 mod 16
-          if (tid == kTma) {
+          if (tid == tma) {
             const int64_t nb = (A.dbg & 8) ? 0 : nd - head - tail;
             if (nb > 0)
               asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gd + head),
                            "r"(smem_u32(sp + head)), "r"((uint32_t)(nb * 8))
                            : "memory");
-          } else if (tid == kTma + 1 + hh) {
+          } else if (tid == tma + 1 + hh) {
             if (head) gd[0] = sp[0];
-          } else if (tid == kTma + 3 + hh) {
+          } else if (tid == tma + 3 + hh) {
             if (tail) gd[nd - 1] = sp[nd - 1];
           }
         }
-        if (tid == kTma) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (tid == tma) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
 #ifdef BSF_PHASE_TIMERS
       if (k >= 0 && (tid == 0 || tid == 32)) { CT_MARK(T5); CT_ADD(tid ? 14 : 13, T5 - T4); }
@@ -692,7 +727,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
     }
   }
   CT_MARK(TK2);
-  if (tid == kTma) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (tid == tma) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #ifdef BSF_PHASE_TIMERS
   if (tid == 0) { CT_ADD(8, TK1 - TK0); CT_ADD(9, TK2 - TK1); CT_ADD(10, 1); CT_ADD(11, clock64() - TK0); }
 #endif
@@ -1037,6 +1072,8 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
   {   // profiling switches (read once per process): 1 no points, 2 no gather, 4 no stores
     static const int dbg = getenv("BSF_CORE_DEBUG") ? atoi(getenv("BSF_CORE_DEBUG")) : 0;
     A.dbg = dbg;
+    static const int layout = getenv("BSF_CORE_LAYOUT") ? std::min(7, std::max(0, atoi(getenv("BSF_CORE_LAYOUT")))) : 5;
+    A.layout = layout;
   }
   A.G00 = ct.G[0]; A.G01 = ct.G[1]; A.G10 = ct.G[2]; A.G11 = ct.G[3]; A.detJ = ct.detJ;
   A.mu1 = (flags & 2) ? 0.0 : mat.mu_st1;
