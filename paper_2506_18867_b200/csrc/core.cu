@@ -98,7 +98,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 // decides how the per-step work is spread over the four schedulers.  A layout gives the gather warps' block
 // entries (role = 3 r + c), the warp that issues the bulk stores, the point-item block of each point warp
 // (items 30 pw .. 30 pw + 29: pw 0-3 membrane, 4 mixed, 5-6 bending) and its gradient rounds
-// [g0, g0 + gn) (round = 3 parity + component).  Selected with BSF_CORE_LAYOUT (default 5: C4 k_core 451 us with layout 1, 444 with 0, 431 with 4, 429 with 5;
+// [g0, g0 + gn) (round = 3 parity + component).  Selected with BSF_CORE_LAYOUT (default 6: C4 k_core 451 us with layout 1, 444 with 0, 431 with 4, 429 with 5, 428 with 6;
 // the per-warp busy cycles of scripts/core_timers.py --c4 show the gather warps as the limit from layout 4 on).
 struct CoreLayout {
   int8_t role[kGatherWarps];
@@ -119,8 +119,8 @@ __constant__ CoreLayout kLayouts[8] = {
     {{1, 0, 4, 8, 2, 3, 5, 6, 7}, 5, {0, 1, 2, 4, 3, 5, 6}, {0, 4, 5, 0, 0, 0, 2}, {0, 1, 1, 0, 0, 2, 2}},
     // 5: as 4, a bending block on warp 12 (scheduler 0) and the mixed block on warp 14
     {{1, 0, 4, 8, 2, 3, 5, 6, 7}, 5, {0, 1, 2, 5, 3, 4, 6}, {0, 4, 5, 0, 0, 0, 2}, {0, 1, 1, 2, 0, 0, 2}},
-    // 6: as 5, the gradient rounds on warps 9, 10, 12 (two), 15 (two)
-    {{1, 0, 4, 8, 2, 3, 5, 6, 7}, 5, {0, 1, 2, 5, 3, 4, 6}, {5, 4, 0, 0, 0, 0, 2}, {1, 1, 0, 2, 0, 0, 2}},
+    // 6: as 5, no gradient round on scheduler 2 (warps 10, 14): warps 11 (one), 12 (two), 15 (three)
+    {{1, 0, 4, 8, 2, 3, 5, 6, 7}, 5, {0, 1, 2, 5, 3, 4, 6}, {0, 0, 5, 0, 0, 0, 2}, {0, 0, 1, 2, 0, 0, 3}},
     // 7: as 5, one gradient round on warp 12 and three on warp 15
     {{1, 0, 4, 8, 2, 3, 5, 6, 7}, 5, {0, 1, 2, 5, 3, 4, 6}, {0, 4, 5, 0, 0, 0, 1}, {0, 1, 1, 1, 0, 0, 3}},
 };
@@ -1015,6 +1015,9 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
 
 int core_ctas_per_item(const CoreTables& ct, int nchunks) { return ct.nstrips * nchunks; }
 
+constexpr int kOneWaveRows = 192;    // longest row chunk of the one-wave choice
+constexpr double kSideRoundRows = 24;   // one round of band CTAs (2 per SM, ~43 us) in k_core row steps (~1.8 us)
+
 int core_pick_chunks(const CoreTables& ct, int nbatch, int rows_override, int reserved_sms) {
   // row chunks per (strip, item): minimise (waves of 1 CTA per SM) x (rows per chunk + the 6-row prologue
   // of a chunk); chunks of >= 16 rows.  The band / corner kernels run beside k_core and fill a partial
@@ -1037,6 +1040,23 @@ int core_pick_chunks(const CoreTables& ct, int nbatch, int rows_override, int re
   const int per = std::max(1, ct.nstrips * std::max(1, nbatch));
   if (reserved_sms > 0 && per <= 16 && per + reserved_sms < nsm)
     return std::max(1, std::min((nsm - reserved_sms) / per, rows / 6));
+  // One wave when the chunks stay short enough (row slabs of a multi-GPU split): the chunk count minimising
+  // max(chunk rows + prologue, rounds of the band / corner kernels on the SMs k_core leaves free x
+  // kSideRoundRows), with all core CTAs in one wave.  Measured on C4 row slabs against the multi-wave choice
+  // below (whose second wave starts late behind the side kernels): 512 rows 263 -> 251 us, 256 rows
+  // 162 -> 142 us; an N = 8 edge slab (92 core rows, 76 band CTAs) is faster in 3 chunks than in 4 (the band
+  // kernel gets one round); a whole 1024^2 sheet, 256 rows per chunk, is faster in two waves (430 vs 466 us).
+  if (per < nsm) {
+    int best1 = 0;
+    double c1 = 1e300;
+    for (int nch = 1; per * nch < nsm && nch <= std::max(1, rows / 6); ++nch) {
+      const int free_sms = nsm - per * nch;
+      const int rounds = reserved_sms > 0 ? (reserved_sms + free_sms - 1) / free_sms : 0;
+      const double cost = std::max((double)rows / nch + prologue, (double)rounds * kSideRoundRows);
+      if (cost < c1 - 1e-9) { c1 = cost; best1 = nch; }
+    }
+    if (best1 > 0 && rows <= kOneWaveRows * best1) return best1;
+  }
   const int maxch = std::max(1, rows / min_rows);
   int best = 1;
   double bcost = 1e300;
@@ -1072,7 +1092,7 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
   {   // profiling switches (read once per process): 1 no points, 2 no gather, 4 no stores
     static const int dbg = getenv("BSF_CORE_DEBUG") ? atoi(getenv("BSF_CORE_DEBUG")) : 0;
     A.dbg = dbg;
-    static const int layout = getenv("BSF_CORE_LAYOUT") ? std::min(7, std::max(0, atoi(getenv("BSF_CORE_LAYOUT")))) : 5;
+    static const int layout = getenv("BSF_CORE_LAYOUT") ? std::min(7, std::max(0, atoi(getenv("BSF_CORE_LAYOUT")))) : 6;
     A.layout = layout;
   }
   A.G00 = ct.G[0]; A.G01 = ct.G[1]; A.G10 = ct.G[2]; A.G11 = ct.G[3]; A.detJ = ct.detJ;

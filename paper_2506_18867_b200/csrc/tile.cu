@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -908,6 +910,9 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
                                                             (int64_t)ft->ntiles * nbatch);
     const int core_nch = ov ? core_pick_chunks(*ct, nbatch, halo->jb - halo->ja, reserved)
                             : core_pick_chunks(*ct, nbatch, -1, reserved);
+    if (getenv("BSF_DEBUG_CHUNKS"))
+      fprintf(stderr, "chunks: band %d ctas, frame %d tiles, reserved %d, core rows %d strips %d nch %d\n",
+              (int)ft->band.nctas, (int)ft->ntiles, reserved, ct->RJ1 - ct->RJ0, ct->nstrips, core_nch);
     const int64_t nfb = ft->ntiles + ft->band.nctas;   // energy slots: [frame tiles | band CTAs | core CTAs]
     const int64_t nb_lo = (ov && halo->ja > ct->RJ0) ? core_ctas_per_item(*ct, 1) : 0;   // boundary launches
     const int64_t nb_hi = (ov && halo->jb < ct->RJ1) ? core_ctas_per_item(*ct, 1) : 0;
@@ -952,7 +957,11 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     // corners (k_frame) and bands (k_band) run beside the core on side streams.  Small problems (a few core
     // strips: one C2 / C3 sheet) put them on two streams, since the three kernels have similar latencies;
     // large ones queue the corners before the bands on one stream (fewer SMs held back from k_core at its start)
-    const bool small = (int64_t)ct->nstrips * nbatch <= 16;
+    // (row slabs of a multi-GPU split count as small: their corner and band kernels are a large share of the slab;
+    // C4 at N = 8, edge slab of 96 rows: 96 -> 85 us)
+    static const int side_mode = getenv("BSF_SIDE_STREAMS") ? atoi(getenv("BSF_SIDE_STREAMS")) : 0;   // experiment
+    const bool slab = sh.r0 > 0 || sh.r1 < sh.n_v;
+    const bool small = side_mode == 2 || (side_mode != 1 && ((int64_t)ct->nstrips * nbatch <= 16 || slab));
     cudaStream_t fst = small ? tt.side2 : tt.side;
     if (cudaEventRecord(tt.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(tt.side, tt.ev_fork, 0) != cudaSuccess ||
         (small && cudaStreamWaitEvent(tt.side2, tt.ev_fork, 0) != cudaSuccess))

@@ -47,13 +47,14 @@ def slab_bounds(n_v: int, world: int, edge_discount: int = 0):
 
 
 def edge_rows_discount(n_v: int, world: int) -> int:
-    """Rows taken off each edge slab of the fused path.  Model (B200, C4, scripts/slab_compute_bound.py): an
-    edge slab's band and corner kernels delay its interior kernel by ~29 us, ~12 row-steps of each of its 4
-    row chunks, i.e. ~48 rows to shed, spread so that each of the world - 2 middle slabs takes its share:
-    d = 48 (world - 2) / world (N=4: 24, N=8: 36), at most a quarter of the balanced share."""
-    if world < 3:
+    """Rows taken off each edge slab of the fused path.  Measured (B200, C4, scripts/slab_nch_probe.py with the
+    one-wave core chunking and the corner / band kernels on two side streams): at N <= 4 the edge slabs' extra
+    corner and band work hides beside their interior kernel (N = 4 balanced: edge 140 us, middle 142 us), so the
+    split is balanced; at N = 8 an edge slab takes its interior in 3 chunks (its band kernel needs the SMs) and
+    sheds 24 rows (edge 104 rows 86-92 us, middle 136 rows 88-90 us).  At most a quarter of the balanced share."""
+    if world <= 4:
         return 0
-    return min(round(48 * (world - 2) / world), (n_v // world) // 4)
+    return min(24, (n_v // world) // 4)
 
 
 def halo_rows(r0: int, r1: int, n_v: int):

@@ -1,5 +1,6 @@
 """C4 at N = 8 (row slabs with the bench's edge discount): one rank's slab call timed alone for the first (edge)
-and a middle rank, under the current core chunking or BSF_CORE_NCH = n (read once per process)."""
+and a middle rank, under the current core chunking or BSF_CORE_NCH = n (read once per process); SLAB_DISCOUNT overrides the edge
+discount, BSF_SIDE_STREAMS = 2 puts the corner and band kernels on two side streams."""
 import json
 import os
 import sys
@@ -14,8 +15,9 @@ from paper_2506_18867_b200.distributed import edge_rows_discount, slab_bounds  #
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 sh = W.make_c4()
-bounds = slab_bounds(sh.n_v, N, edge_rows_discount(sh.n_v, N))
-out = {"N": N, "nch": os.environ.get("BSF_CORE_NCH")}
+disc = int(os.environ["SLAB_DISCOUNT"]) if os.environ.get("SLAB_DISCOUNT") else edge_rows_discount(sh.n_v, N)
+bounds = slab_bounds(sh.n_v, N, disc)
+out = {"N": N, "nch": os.environ.get("BSF_CORE_NCH"), "side": os.environ.get("BSF_SIDE_STREAMS"), "discount": disc}
 for rank in (0, N // 2):
     r0, r1 = bounds[rank]
     s = B.Sheet.from_sheet(sh, row_begin=r0, row_end=r1)
