@@ -24,6 +24,8 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -121,35 +123,61 @@ __global__ void k_wp_info(const uint64_t* __restrict__ key, const int32_t* __res
 // level 2, one CTA per window pair w, one thread per pair of window entries (ea, eb): the 3x3 block
 // sum over w's vertex pairs of N_ea(alpha) N_eb(beta) H_lin(alpha, beta), in run order, and its key (i, j),
 // emitted when some vertex pair of w has both weights nonzero (the oracle's structural pattern)
+constexpr int kWpChunk = 32;   // vertex pairs of a window pair staged in shared memory at a time
+
 __global__ void __launch_bounds__(96) k_wp_blocks(const int32_t* __restrict__ wps, const uint32_t* __restrict__ wpu,
                                                   const int2* __restrict__ wpo, const int2* __restrict__ ab,
                                                   const double* __restrict__ hlin, const double* __restrict__ vw,
-                                                  int nvert, int n_u, int ncp, double* __restrict__ wblk,
+                                                  int nvert, int n_u, int ncp, int nwp, double* __restrict__ wblk,
                                                   uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
-  const int w = blockIdx.x, e = threadIdx.x;
-  if (e >= 81) return;
+  // the run's weights and H_lin blocks are staged by all threads (independent loads in flight), then every
+  // thread sums its block over them in run order
+  __shared__ double sa[kWpChunk][9], sb[kWpChunk][9], sh[kWpChunk][9], so[729];
+  const int e = threadIdx.x;
   const int ea = e / 9, eb = e - 9 * (e / 9);
+  for (int w = blockIdx.x; w < nwp; w += gridDim.x) {   // grid-stride: the window pairs are many and short
   double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
   bool nz = false;
-  for (int k = wps[w]; k < wps[w + 1]; ++k) {
-    const uint32_t u = wpu[k];
-    const int2 p = ab[u];
-    const double wa = vw[(int64_t)ea * nvert + p.x], wb = vw[(int64_t)eb * nvert + p.y];
-    nz |= wa != 0.0 && wb != 0.0;
-    const double wt = wa * wb;
+  const int k0 = wps[w], k1 = wps[w + 1];
+  for (int c0 = k0; c0 < k1; c0 += kWpChunk) {
+    const int nc = min(kWpChunk, k1 - c0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < 27 * nc; t += blockDim.x) {
+      const int k = t / 27, c = t - 27 * k;
+      const uint32_t u = wpu[c0 + k];
+      const int2 p = ab[u];
+      if (c < 9) sa[k][c] = vw[(int64_t)c * nvert + p.x];
+      else if (c < 18) sb[k][c - 9] = vw[(int64_t)(c - 9) * nvert + p.y];
+      else sh[k][c - 18] = hlin[9 * (int64_t)u + c - 18];
+    }
+    __syncthreads();
+    if (e < 81)
+      for (int k = 0; k < nc; ++k) {
+        const double wa = sa[k][ea], wb = sb[k][eb];
+        nz |= wa != 0.0 && wb != 0.0;
+        const double wt = wa * wb;
 #pragma unroll
-    for (int q = 0; q < 9; ++q) s[q] = fma(wt, hlin[9 * (int64_t)u + q], s[q]);
+        for (int q = 0; q < 9; ++q) s[q] = fma(wt, sh[k][q], s[q]);
+      }
   }
-  const int64_t t = 81 * (int64_t)w + e;
+  // the window pair's 81 blocks are one contiguous 5,832-byte range of wblk: written through shared memory so
+  // that every warp store is coalesced
+  if (e < 81) {
 #pragma unroll
-  for (int q = 0; q < 9; ++q) wblk[9 * t + q] = s[q];
-  const uint64_t m = (uint64_t)ncp;
-  val[t] = (uint32_t)t;
-  if (!nz) { key[t] = m * m; return; }
-  const int2 o = wpo[w];
-  const uint32_t i = (uint32_t)(o.x + (ea / 3) * n_u + ea % 3);
-  const uint32_t j = (uint32_t)(o.y + (eb / 3) * n_u + eb % 3);
-  key[t] = (uint64_t)i * m + j;
+    for (int q = 0; q < 9; ++q) so[9 * e + q] = s[q];
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < 729; q += blockDim.x) wblk[729 * (int64_t)w + q] = so[q];
+  if (e < 81) {
+    const int64_t t = 81 * (int64_t)w + e;
+    const uint64_t m = (uint64_t)ncp;
+    val[t] = (uint32_t)t;
+    const int2 o = wpo[w];
+    const uint32_t i = (uint32_t)(o.x + (ea / 3) * n_u + ea % 3);
+    const uint32_t j = (uint32_t)(o.y + (eb / 3) * n_u + eb % 3);
+    key[t] = nz ? (uint64_t)i * m + j : m * m;
+  }
+  }
 }
 
 // Control-point blocks: sum of the run's window-pair blocks in sorted order; diagonal blocks go into the elastic
@@ -420,7 +448,8 @@ int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const 
     if (!grow(&S.k1, &S.k1_cap, n2) || !grow(&S.v1, &S.v1_cap, n2) || !grow(&S.k2, &S.k2_cap, n2) ||
         !grow(&S.v2, &S.v2_cap, n2)) { err = "allocation"; return -7; }
     if (!grow(&S.wblk, &S.wblk_cap, 9 * n2)) { err = "allocation"; return -7; }
-    k_wp_blocks<<<nwp, 96, 0, st>>>(S.wps, S.wpu, S.wpo, S.ab, S.hlin, S.vw, S.nvert, S.n_u, S.ncp, S.wblk, S.k1, S.v1);
+    k_wp_blocks<<<std::min(nwp, 148 * 16), 96, 0, st>>>(S.wps, S.wpu, S.wpo, S.ab, S.hlin, S.vw, S.nvert, S.n_u, S.ncp,
+                                                        nwp, S.wblk, S.k1, S.v1);
     if ((rc = sort_runs(S, S.k1, S.v1, S.k2, S.v2, n2, (uint64_t)S.ncp * S.ncp, st, &ncpb, err))) return rc;
   }
   if (ncpb > 0) {
@@ -461,6 +490,9 @@ int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const 
     if (nv > 0) k_sum_vert<<<nblk(nv, 128), 128, 0, st>>>(S.start, nv, S.v2, S.k2, d_g, S.gv);
     k_grad_cp<<<nblk(S.ncp, 128), 128, 0, st>>>(S.cp_ptr, S.cp_list, S.vw, S.nvert, S.gv, S.ncp, d_grad_cp);
   }
+  if (getenv("BSF_DEBUG_CONTACT"))
+    fprintf(stderr, "contact: pairs %d, vertex pairs %d, window pairs %d, cp pairs %d, off-diagonal %lld\n", npairs,
+            nlin, nwp, ncpb, (long long)S.nnz);
   if (nnz_off) *nnz_off = S.nnz;
   S.assembled = true;
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
