@@ -20,3 +20,11 @@ for _ in range(5):
 t1.record(); torch.cuda.synchronize()
 ms = t0.elapsed_time(t1) / 5
 print(f"{nst} states: {ms:.3f} ms/call, {ms*1e3/nst:.2f} us/state, launches={h.last_launch_count()}")
+if os.environ.get("PROF_KT"):   # per-kernel live times (bsf_set_kernel_timing): k_core and k_band of the call
+    h.set_kernel_timing(5)
+    for _ in range(5):
+        h.eval_all_batch(X, E, G, V, flags)
+    torch.cuda.synchronize()
+    c, b = h.kernel_timing(5)
+    import statistics
+    print(f"k_core {statistics.median(c):.3f} ms, k_band {statistics.median(b):.3f} ms (live, beside each other)")
