@@ -46,7 +46,8 @@ inline int key_bits(uint64_t sentinel) {
 }
 
 // level 1: (pair, slot a, slot b) -> key (alpha, beta); invalid slots -> the sentinel (sorted to the end)
-__global__ void k_emit_lin(const int32_t* __restrict__ verts, int npairs, int nvert, uint64_t* __restrict__ key,
+template <class K>
+__global__ void k_emit_lin(const int32_t* __restrict__ verts, int npairs, int nvert, K* __restrict__ key,
                            uint32_t* __restrict__ val, int* __restrict__ bad) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)npairs * 16) return;
@@ -56,20 +57,22 @@ __global__ void k_emit_lin(const int32_t* __restrict__ verts, int npairs, int nv
   if (!ok && sb == 0) atomicOr(bad, 1);
   // key a * nvert + b; the sentinel nvert^2 sorts after every valid key within the sorted bit range
   const uint64_t m = (uint64_t)nvert;
-  key[t] = (ok && a >= 0 && b >= 0) ? (uint64_t)a * m + (uint64_t)b : m * m;
+  key[t] = (K)((ok && a >= 0 && b >= 0) ? (uint64_t)a * m + (uint64_t)b : m * m);
   val[t] = (uint32_t)t;
 }
 
 // run heads of a sorted key array (first of each distinct valid key): flag[t] = 1
-__global__ void k_heads(const uint64_t* __restrict__ key, int64_t n, uint64_t nokey, int32_t* __restrict__ flag) {
+template <class K>
+__global__ void k_heads(const K* __restrict__ key, int64_t n, K nokey, int32_t* __restrict__ flag) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   flag[t] = (key[t] != nokey && (t == 0 || key[t] != key[t - 1])) ? 1 : 0;
 }
 
 // run starts: start[id[t] - 1] = t for heads; start[nruns] = end of the valid keys
+template <class K>
 __global__ void k_run_starts(const int32_t* __restrict__ flag, const int32_t* __restrict__ id, int64_t n,
-                             const uint64_t* __restrict__ key, uint64_t nokey, int32_t* __restrict__ start) {
+                             const K* __restrict__ key, K nokey, int32_t* __restrict__ start) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   if (flag[t]) start[id[t] - 1] = (int32_t)t;
@@ -77,8 +80,9 @@ __global__ void k_run_starts(const int32_t* __restrict__ flag, const int32_t* __
 }
 
 // H_lin[u] = sum over the run of the pairs' (alpha, beta) blocks, in sorted (= emission) order
+template <class K>
 __global__ void k_sum_lin(const int32_t* __restrict__ start, int nruns, const uint32_t* __restrict__ val,
-                          const double* __restrict__ H, const uint64_t* __restrict__ key, int nvert,
+                          const double* __restrict__ H, const K* __restrict__ key, int nvert,
                           double* __restrict__ hlin, int2* __restrict__ ab) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= nruns) return;
@@ -100,17 +104,19 @@ __global__ void k_sum_lin(const int32_t* __restrict__ start, int nruns, const ui
 
 // level 1b: the vertex-pair blocks grouped by their pair of control-point windows (all vertices inside one knot
 // span share a window), so that level 2 emits 81 control-point pairs per window pair, not per vertex pair
+template <class K>
 __global__ void k_emit_wp(const int2* __restrict__ ab, int nlin, const int2* __restrict__ vwin, int n_u, int ncp,
-                          uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+                          K* __restrict__ key, uint32_t* __restrict__ val) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= nlin) return;
   const int2 p = ab[u], oa = vwin[p.x], ob = vwin[p.y];
-  key[u] = (uint64_t)(oa.y * n_u + oa.x) * (uint64_t)ncp + (uint64_t)(ob.y * n_u + ob.x);
+  key[u] = (K)((uint64_t)(oa.y * n_u + oa.x) * (uint64_t)ncp + (uint64_t)(ob.y * n_u + ob.x));
   val[u] = (uint32_t)u;
 }
 
 // window pair w: its run of vertex pairs [wps[w], wps[w+1]) in wpu, and its two window origins (linear cp index)
-__global__ void k_wp_info(const uint64_t* __restrict__ key, const int32_t* __restrict__ start, int nwp, int ncp,
+template <class K>
+__global__ void k_wp_info(const K* __restrict__ key, const int32_t* __restrict__ start, int nwp, int ncp,
                           int32_t* __restrict__ wps, int2* __restrict__ wpo) {
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
   if (w >= nwp) return;
@@ -125,11 +131,12 @@ __global__ void k_wp_info(const uint64_t* __restrict__ key, const int32_t* __res
 // emitted when some vertex pair of w has both weights nonzero (the oracle's structural pattern)
 constexpr int kWpChunk = 32;   // vertex pairs of a window pair staged in shared memory at a time
 
+template <class K>
 __global__ void __launch_bounds__(96) k_wp_blocks(const int32_t* __restrict__ wps, const uint32_t* __restrict__ wpu,
                                                   const int2* __restrict__ wpo, const int2* __restrict__ ab,
                                                   const double* __restrict__ hlin, const double* __restrict__ vw,
                                                   int nvert, int n_u, int ncp, int nwp, double* __restrict__ wblk,
-                                                  uint64_t* __restrict__ key, uint32_t* __restrict__ val) {
+                                                  K* __restrict__ key, uint32_t* __restrict__ val) {
   // the run's weights and H_lin blocks are staged by all threads (independent loads in flight), then every
   // thread sums its block over them in run order
   __shared__ double sa[kWpChunk][9], sb[kWpChunk][9], sh[kWpChunk][9], so[729];
@@ -175,42 +182,59 @@ __global__ void __launch_bounds__(96) k_wp_blocks(const int32_t* __restrict__ wp
     const int2 o = wpo[w];
     const uint32_t i = (uint32_t)(o.x + (ea / 3) * n_u + ea % 3);
     const uint32_t j = (uint32_t)(o.y + (eb / 3) * n_u + eb % 3);
-    key[t] = nz ? (uint64_t)i * m + j : m * m;
+    key[t] = (K)(nz ? (uint64_t)i * m + j : m * m);
   }
   }
 }
 
 // Control-point blocks: sum of the run's window-pair blocks in sorted order; diagonal blocks go into the elastic
 // matrix's diagonal (vals_d, nullable), off-diagonal ones into the contact BSR at their rank.
-__global__ void k_sum_cp(const int32_t* __restrict__ start, int nruns, const uint32_t* __restrict__ val,
-                         const uint64_t* __restrict__ key, const double* __restrict__ wblk, int ncp,
-                         const int32_t* __restrict__ offd_rank, double* __restrict__ bvals, int32_t* __restrict__ bcol,
-                         double* __restrict__ vals_d, const int32_t* __restrict__ diag_pos) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= nruns) return;
-  double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-  for (int k = start[r]; k < start[r + 1]; ++k) {
-    const double* b = wblk + 9 * (int64_t)val[k];
+constexpr int kSumThreads = 128;
+
+template <class K>
+__global__ void __launch_bounds__(kSumThreads) k_sum_cp(const int32_t* __restrict__ start, int nruns,
+                                                         const uint32_t* __restrict__ val, const K* __restrict__ key,
+                                                         const double* __restrict__ wblk, int ncp,
+                                                         const int32_t* __restrict__ offd_rank,
+                                                         double* __restrict__ bvals, int32_t* __restrict__ bcol,
+                                                         double* __restrict__ vals_d,
+                                                         const int32_t* __restrict__ diag_pos) {
+  // the CTA's off-diagonal blocks are consecutive in the output: staged in shared memory, then written coalesced
+  __shared__ double so[9 * kSumThreads];
+  const int r0 = blockIdx.x * kSumThreads, r = r0 + threadIdx.x;
+  const int rl = min(nruns, r0 + kSumThreads) - 1;
+  const int o0 = offd_rank[r0];
+  if (r < nruns) {
+    double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int k = start[r]; k < start[r + 1]; ++k) {
+      const double* b = wblk + 9 * (int64_t)val[k];
 #pragma unroll
-    for (int q = 0; q < 9; ++q) s[q] += b[q];
-  }
-  const uint64_t kk = key[start[r]];
-  const int i = (int)(kk / (uint64_t)ncp), j = (int)(kk % (uint64_t)ncp);
-  if (i == j) {
-    if (vals_d) {
-      double* d = vals_d + 9 * (int64_t)diag_pos[i];
-#pragma unroll
-      for (int q = 0; q < 9; ++q) d[q] += s[q];
+      for (int q = 0; q < 9; ++q) s[q] += b[q];
     }
-    return;
-  }
-  const int32_t o = offd_rank[r];
-  bcol[o] = j;
+    const uint64_t kk = key[start[r]];
+    const int i = (int)(kk / (uint64_t)ncp), j = (int)(kk % (uint64_t)ncp);
+    if (i == j) {
+      if (vals_d) {
+        double* d = vals_d + 9 * (int64_t)diag_pos[i];
 #pragma unroll
-  for (int q = 0; q < 9; ++q) bvals[9 * (int64_t)o + q] = s[q];
+        for (int q = 0; q < 9; ++q) d[q] += s[q];
+      }
+    } else {
+      const int32_t o = offd_rank[r];
+      bcol[o] = j;
+#pragma unroll
+      for (int q = 0; q < 9; ++q) so[9 * (o - o0) + q] = s[q];
+    }
+  }
+  __syncthreads();
+  // off-diagonal blocks of this CTA: ranks [o0, o1)
+  const uint64_t kl = key[start[rl]];
+  const int o1 = offd_rank[rl] + ((kl / (uint64_t)ncp) != (kl % (uint64_t)ncp) ? 1 : 0);
+  for (int t = threadIdx.x; t < 9 * (o1 - o0); t += kSumThreads) bvals[9 * (int64_t)o0 + t] = so[t];
 }
 
-__global__ void k_offd_flags(const uint64_t* __restrict__ key, const int32_t* __restrict__ start, int nruns, int ncp,
+template <class K>
+__global__ void k_offd_flags(const K* __restrict__ key, const int32_t* __restrict__ start, int nruns, int ncp,
                              int32_t* __restrict__ flag) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nruns) return;
@@ -220,7 +244,8 @@ __global__ void k_offd_flags(const uint64_t* __restrict__ key, const int32_t* __
 
 // row_ptr of the off-diagonal contact BSR from the sorted unique keys (rows ascending): one thread per row
 // finds its first entry by binary search over the off-diagonal ranks
-__global__ void k_row_ptr(const uint64_t* __restrict__ key, const int32_t* __restrict__ start,
+template <class K>
+__global__ void k_row_ptr(const K* __restrict__ key, const int32_t* __restrict__ start,
                           const int32_t* __restrict__ flag, const int32_t* __restrict__ rank, int nruns, int nrows,
                           int ncp, int32_t* __restrict__ row_ptr) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
@@ -237,17 +262,19 @@ __global__ void k_row_ptr(const uint64_t* __restrict__ key, const int32_t* __res
 
 // gradient: per-vertex sums (k_sum_vert over runs of the sorted (alpha, slot) keys), scattered into a dense
 // per-vertex array, then gathered per control point through the static cp -> (vertex, entry) lists
-__global__ void k_emit_vert(const int32_t* __restrict__ verts, int npairs, int nvert, uint64_t* __restrict__ key,
+template <class K>
+__global__ void k_emit_vert(const int32_t* __restrict__ verts, int npairs, int nvert, K* __restrict__ key,
                             uint32_t* __restrict__ val) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)npairs * 4) return;
   const int32_t a = verts[t];
-  key[t] = (a >= 0 && a < nvert) ? (uint64_t)a : (uint64_t)nvert;
+  key[t] = (K)((a >= 0 && a < nvert) ? (uint64_t)a : (uint64_t)nvert);
   val[t] = (uint32_t)t;
 }
 
+template <class K>
 __global__ void k_sum_vert(const int32_t* __restrict__ start, int nruns, const uint32_t* __restrict__ val,
-                           const uint64_t* __restrict__ key, const double* __restrict__ g, double* __restrict__ gv) {
+                           const K* __restrict__ key, const double* __restrict__ g, double* __restrict__ gv) {
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   if (u >= nruns) return;
   double s[3] = {0, 0, 0};
@@ -367,9 +394,11 @@ int contact_positions(const ContactState& S, const double* d_x, double* d_xv, cu
 
 // sorts (key, val) of n entries with CUB (stable LSD radix sort), then marks the runs of equal valid keys:
 // returns the number of runs (host), run starts in S.start[0 .. nruns] (device)
-static int sort_runs(ContactState& S, uint64_t* k_in, uint32_t* v_in, uint64_t* k_out, uint32_t* v_out, int64_t n,
-                     uint64_t nokey, cudaStream_t st, int* nruns, std::string& err) {
-  const int nbits = key_bits(nokey);
+template <class K>
+static int sort_runs(ContactState& S, K* k_in, uint32_t* v_in, K* k_out, uint32_t* v_out, int64_t n, uint64_t nokey64,
+                     cudaStream_t st, int* nruns, std::string& err) {
+  const int nbits = key_bits(nokey64);
+  const K nokey = (K)nokey64;
   size_t tb = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tb, k_in, k_out, v_in, v_out, (int)n, 0, nbits, st);
   size_t tb2 = 0;
@@ -398,9 +427,14 @@ static int sort_runs(ContactState& S, uint64_t* k_in, uint32_t* v_in, uint64_t* 
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
 }
 
-int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const double* d_H, const double* d_g,
-                     double* d_grad_cp, double* d_vals, const int32_t* d_diag_pos, int64_t* nnz_off, cudaStream_t st,
-                     std::string& err) {
+// K1: key type of the vertex keys (level 1, gradient), K2: of the control-point keys (levels 1b, 2); 32-bit when
+// the sentinel fits (fewer radix passes and half the key traffic)
+template <class K1, class K2>
+static int assemble_impl(ContactState& S, int npairs, const int32_t* d_verts, const double* d_H, const double* d_g,
+                         double* d_grad_cp, double* d_vals, const int32_t* d_diag_pos, int64_t* nnz_off,
+                         cudaStream_t st, std::string& err) {
+  const auto K1p = [](uint64_t* p) { return reinterpret_cast<K1*>(p); };
+  const auto K2p = [](uint64_t* p) { return reinterpret_cast<K2*>(p); };
   S.nnz = 0;
   S.nrows = S.ncp;
   if (!grow(&S.row_ptr, &S.row_cap, S.ncp + 1)) { err = "allocation"; return -7; }
@@ -415,8 +449,8 @@ int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const 
       err = "allocation";
       return -7;
     }
-    k_emit_lin<<<nblk(n1, 256), 256, 0, st>>>(d_verts, npairs, S.nvert, S.k1, S.v1, S.bad);
-    if ((rc = sort_runs(S, S.k1, S.v1, S.k2, S.v2, n1, (uint64_t)S.nvert * S.nvert, st, &nlin, err))) return rc;
+    k_emit_lin<<<nblk(n1, 256), 256, 0, st>>>(d_verts, npairs, S.nvert, K1p(S.k1), S.v1, S.bad);
+    if ((rc = sort_runs(S, K1p(S.k1), S.v1, K1p(S.k2), S.v2, n1, (uint64_t)S.nvert * S.nvert, st, &nlin, err))) return rc;
     int bad = 0;
     if (cudaMemcpy(&bad, S.bad, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) { err = "copy"; return -6; }
     if (bad) { err = "contact pair vertex index >= n_vert"; return -1; }
@@ -424,18 +458,18 @@ int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const 
   }
   if (nlin > 0) {
     if (!grow(&S.hlin, &S.hlin_cap, 9 * (int64_t)nlin) || !grow(&S.ab, &S.ab_cap, nlin)) { err = "allocation"; return -7; }
-    k_sum_lin<<<nblk(nlin, 128), 128, 0, st>>>(S.start, nlin, S.v2, d_H, S.k2, S.nvert, S.hlin, S.ab);
+    k_sum_lin<<<nblk(nlin, 128), 128, 0, st>>>(S.start, nlin, S.v2, d_H, K1p(S.k2), S.nvert, S.hlin, S.ab);
   }
   // ---- level 1b: window pairs
   int nwp = 0;
   if (nlin > 0) {
-    k_emit_wp<<<nblk(nlin, 256), 256, 0, st>>>(S.ab, nlin, S.vwin, S.n_u, S.ncp, S.k1, S.v1);
-    if ((rc = sort_runs(S, S.k1, S.v1, S.k2, S.v2, nlin, (uint64_t)S.ncp * S.ncp, st, &nwp, err))) return rc;
+    k_emit_wp<<<nblk(nlin, 256), 256, 0, st>>>(S.ab, nlin, S.vwin, S.n_u, S.ncp, K2p(S.k1), S.v1);
+    if ((rc = sort_runs(S, K2p(S.k1), S.v1, K2p(S.k2), S.v2, nlin, (uint64_t)S.ncp * S.ncp, st, &nwp, err))) return rc;
     if (!grow(&S.wps, &S.wps_cap, nwp + 1) || !grow(&S.wpo, &S.wpo_cap, nwp) || !grow(&S.wpu, &S.wpu_cap, nlin)) {
       err = "allocation";
       return -7;
     }
-    k_wp_info<<<nblk(nwp, 256), 256, 0, st>>>(S.k2, S.start, nwp, S.ncp, S.wps, S.wpo);
+    k_wp_info<<<nblk(nwp, 256), 256, 0, st>>>(K2p(S.k2), S.start, nwp, S.ncp, S.wps, S.wpo);
     if (cudaMemcpyAsync(S.wpu, S.v2, sizeof(uint32_t) * nlin, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
       err = "copy";
       return -6;
@@ -449,14 +483,14 @@ int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const 
         !grow(&S.v2, &S.v2_cap, n2)) { err = "allocation"; return -7; }
     if (!grow(&S.wblk, &S.wblk_cap, 9 * n2)) { err = "allocation"; return -7; }
     k_wp_blocks<<<std::min(nwp, 148 * 16), 96, 0, st>>>(S.wps, S.wpu, S.wpo, S.ab, S.hlin, S.vw, S.nvert, S.n_u, S.ncp,
-                                                        nwp, S.wblk, S.k1, S.v1);
-    if ((rc = sort_runs(S, S.k1, S.v1, S.k2, S.v2, n2, (uint64_t)S.ncp * S.ncp, st, &ncpb, err))) return rc;
+                                                        nwp, S.wblk, K2p(S.k1), S.v1);
+    if ((rc = sort_runs(S, K2p(S.k1), S.v1, K2p(S.k2), S.v2, n2, (uint64_t)S.ncp * S.ncp, st, &ncpb, err))) return rc;
   }
   if (ncpb > 0) {
     // off-diagonal ranks (exclusive scan of the off-diagonal flags of the runs), pattern, values
     if (!grow(&S.rank, &S.rank_cap, ncpb + 1)) { err = "allocation"; return -7; }
     int32_t* offflag = S.flag;   // reuse: the run flags of the level-2 sort are no longer needed
-    k_offd_flags<<<nblk(ncpb, 256), 256, 0, st>>>(S.k2, S.start, ncpb, S.ncp, offflag);
+    k_offd_flags<<<nblk(ncpb, 256), 256, 0, st>>>(K2p(S.k2), S.start, ncpb, S.ncp, offflag);
     size_t tb = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tb, offflag, S.rank, ncpb, st);
     if (!grow(&S.tmp, &S.tmp_cap, (int64_t)tb)) { err = "allocation"; return -7; }
@@ -471,9 +505,9 @@ int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const 
       err = "allocation";
       return -7;
     }
-    k_sum_cp<<<nblk(ncpb, 128), 128, 0, st>>>(S.start, ncpb, S.v2, S.k2, S.wblk, S.ncp, S.rank, S.vals, S.col,
+    k_sum_cp<<<nblk(ncpb, kSumThreads), kSumThreads, 0, st>>>(S.start, ncpb, S.v2, K2p(S.k2), S.wblk, S.ncp, S.rank, S.vals, S.col,
                                               d_vals, d_diag_pos);
-    k_row_ptr<<<nblk(S.ncp + 1, 256), 256, 0, st>>>(S.k2, S.start, offflag, S.rank, ncpb, S.ncp, S.ncp, S.row_ptr);
+    k_row_ptr<<<nblk(S.ncp + 1, 256), 256, 0, st>>>(K2p(S.k2), S.start, offflag, S.rank, ncpb, S.ncp, S.ncp, S.row_ptr);
   } else if (cudaMemsetAsync(S.row_ptr, 0, sizeof(int32_t) * (S.ncp + 1), st) != cudaSuccess) {
     err = "memset";
     return -6;
@@ -484,10 +518,10 @@ int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const 
     if (!grow(&S.k1, &S.k1_cap, n3) || !grow(&S.v1, &S.v1_cap, n3) || !grow(&S.k2, &S.k2_cap, n3) ||
         !grow(&S.v2, &S.v2_cap, n3) || !grow(&S.gv, &S.gv_cap, 3 * (int64_t)S.nvert)) { err = "allocation"; return -7; }
     if (cudaMemsetAsync(S.gv, 0, sizeof(double) * 3 * (size_t)S.nvert, st) != cudaSuccess) { err = "memset"; return -6; }
-    k_emit_vert<<<nblk(n3, 256), 256, 0, st>>>(d_verts, npairs, S.nvert, S.k1, S.v1);
+    k_emit_vert<<<nblk(n3, 256), 256, 0, st>>>(d_verts, npairs, S.nvert, K1p(S.k1), S.v1);
     int nv = 0;
-    if ((rc = sort_runs(S, S.k1, S.v1, S.k2, S.v2, n3, (uint64_t)S.nvert, st, &nv, err))) return rc;
-    if (nv > 0) k_sum_vert<<<nblk(nv, 128), 128, 0, st>>>(S.start, nv, S.v2, S.k2, d_g, S.gv);
+    if ((rc = sort_runs(S, K1p(S.k1), S.v1, K1p(S.k2), S.v2, n3, (uint64_t)S.nvert, st, &nv, err))) return rc;
+    if (nv > 0) k_sum_vert<<<nblk(nv, 128), 128, 0, st>>>(S.start, nv, S.v2, K1p(S.k2), d_g, S.gv);
     k_grad_cp<<<nblk(S.ncp, 128), 128, 0, st>>>(S.cp_ptr, S.cp_list, S.vw, S.nvert, S.gv, S.ncp, d_grad_cp);
   }
   if (getenv("BSF_DEBUG_CONTACT"))
@@ -496,6 +530,21 @@ int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const 
   if (nnz_off) *nnz_off = S.nnz;
   S.assembled = true;
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
+}
+
+int contact_assemble(ContactState& S, int npairs, const int32_t* d_verts, const double* d_H, const double* d_g,
+                     double* d_grad_cp, double* d_vals, const int32_t* d_diag_pos, int64_t* nnz_off, cudaStream_t st,
+                     std::string& err) {
+  static const bool force64 = getenv("BSF_CONTACT_KEYS64") && atoi(getenv("BSF_CONTACT_KEYS64")) != 0;   // test switch
+  const bool v32 = !force64 && (uint64_t)S.nvert * S.nvert <= 0xffffffffull;
+  const bool c32 = !force64 && (uint64_t)S.ncp * S.ncp <= 0xffffffffull;
+  if (v32 && c32)
+    return assemble_impl<uint32_t, uint32_t>(S, npairs, d_verts, d_H, d_g, d_grad_cp, d_vals, d_diag_pos, nnz_off, st, err);
+  if (v32)
+    return assemble_impl<uint32_t, uint64_t>(S, npairs, d_verts, d_H, d_g, d_grad_cp, d_vals, d_diag_pos, nnz_off, st, err);
+  if (c32)
+    return assemble_impl<uint64_t, uint32_t>(S, npairs, d_verts, d_H, d_g, d_grad_cp, d_vals, d_diag_pos, nnz_off, st, err);
+  return assemble_impl<uint64_t, uint64_t>(S, npairs, d_verts, d_H, d_g, d_grad_cp, d_vals, d_diag_pos, nnz_off, st, err);
 }
 
 }  // namespace bsf

@@ -255,3 +255,43 @@ def test_contact_edge_cases():
     slab = B.Sheet.from_sheet(sh, row_begin=2, row_end=5)
     with pytest.raises(B.BsfError):
         slab.contact_mesh(np.array([[0.5, 0.5]]))
+
+
+_KEYS64 = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle as O, workloads as W, paper_2506_18867_b200 as B
+import scipy.sparse as sp
+sh = W.make_sheet(12, 1.0, 4, n_modes=2, amp=5e-3)
+cs = W.make_contact(sh, 2, 400, seed=2, obstacle_frac=0.2)
+Hcp, gcp = O.Oracle.from_sheet(sh).contact_pullback(cs.uv, cs.verts, cs.H, cs.g)
+s = B.Sheet.from_sheet(sh)
+s.contact_mesh(cs.uv)
+V = torch.zeros((s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+G = torch.zeros((sh.n_v, sh.n_u, 3), dtype=torch.float64, device="cuda")
+s.contact_assemble(torch.from_numpy(cs.verts).cuda(), torch.from_numpy(cs.H).cuda(), torch.from_numpy(cs.g).cuda(), G, V)
+torch.cuda.synchronize()
+n = sh.n_u * sh.n_v
+rp, ci, va = (t.cpu().numpy() for t in s.contact_get())
+Hg = sp.bsr_matrix((va, ci, rp), shape=(3 * n, 3 * n)).toarray()
+rpe, cie = s.pattern()
+Vn = V.cpu().numpy()
+for a in range(n):
+    Hg[3 * a:3 * a + 3, 3 * a:3 * a + 3] += Vn[rpe[a] + int(np.searchsorted(cie[rpe[a]:rpe[a + 1]], a))]
+print("ERR", np.max(np.abs(Hg - Hcp)) / np.abs(Hcp).max(), np.max(np.abs(G.cpu().numpy() - gcp)) / np.abs(gcp).max())
+"""
+
+
+def test_64bit_sort_keys():
+    """The sort keys are 32-bit when their sentinel fits (every test sheet here), else 64-bit (C4-size sheets,
+    meshes of > 65535 vertices); BSF_CONTACT_KEYS64=1 forces the 64-bit path (read once per process: run in a
+    subprocess) against the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BSF_REBUILD="0", BSF_CONTACT_KEYS64="1")
+    r = subprocess.run([sys.executable, "-c", _KEYS64 % root], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    err, gerr = map(float, r.stdout.split("ERR")[1].split())
+    assert err <= 1e-13 and gerr <= 1e-13, (err, gerr)
