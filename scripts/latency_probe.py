@@ -55,5 +55,8 @@ def probe(sh, n=50, tag=""):
 
 
 env = {k: os.environ.get(k) for k in ("BSF_CORE_MINROWS", "BSF_CORE_PROLOGUE", "PROBE_TILE")}
-for name, sh in (("C2", W.make_c2(state=0)), ("C3", W.make_c3())):
-    print(json.dumps({"env": env, **probe(sh, tag=name)}), flush=True)
+cases = [("C2", W.make_c2(state=0)), ("C3", W.make_c3())]
+if "--c4" in sys.argv:
+    cases.append(("C4", W.make_c4()))
+for name, sh in cases:
+    print(json.dumps({"env": env, **probe(sh, n=20 if name == "C4" else 50, tag=name)}), flush=True)
