@@ -561,8 +561,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
     if (nst >= 2) load_pos_async(posb + kPosStep, x, A, i0, ja + 2, 5, tid);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    // the 3 pairs' 420 membrane items first, then their 210 bending items: the second round over the 512 threads
+    // holds only the cheap bending items (one membrane round instead of two)
     for (int it = tid; it < 3 * 6 * kKC; it += kThreads) {
-      const int pr = it / (6 * kKC), item = it - pr * (6 * kKC);
+      const bool mem = it < 3 * 4 * kKC;
+      const int b = it - 3 * 4 * kKC;
+      const int pr = mem ? it / (4 * kKC) : b / (2 * kKC);
+      const int item = mem ? it - pr * (4 * kKC) : 4 * kKC + b - pr * (2 * kKC);
       e_acc += eval_item<CURVED>(ring, ppos + 2 * pr * (kPosC * 3), ja - 4 + 2 * pr, cst, P, ja - 3 + 2 * pr, item);
     }
     __syncthreads();
