@@ -263,7 +263,10 @@ bsf_status bsf_gershgorin(bsf_handle h, const double* d_vals, double* lo, double
 bsf_status bsf_pcg(bsf_handle h, const double* d_vals, const double* d_b, double* d_x, int max_iter, double rtol,
                    int* iters, double* relres, bsf_stream stream);
 
-/* Energy only (the line-search call). d_energy: device, 1 double (overwritten). */
+/* Energy only (the line-search call). d_energy: device, 1 double (overwritten).  Calls without
+ * Hessian values (this one, bsf_eval_gradient, any call with d_vals = NULL) skip the per-point A entries, their
+ * projection and the Hessian gather (C4: 0.15 ms energy, 0.21 ms gradient against 0.45 ms for all three) and give
+ * the same bits as the full call. */
 bsf_status bsf_eval_energy(bsf_handle h, const double* d_x, double* d_energy, int flags,
                            bsf_stream stream);
 

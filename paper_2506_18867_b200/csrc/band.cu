@@ -284,6 +284,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
     const int wt = D.wtask[warp][kt];
     if (wt == 255) break;
     const int td = wt / 6, pi = (wt / 3) & 1, grp = wt % 3;
+    // groups 0, 1 are Hessian entries only; group 2 holds entry (2, 2) and the gradient lanes (and the IP energy)
+    if (!A.vals && (grp < 2 || (!A.g && !A.xhat))) continue;
     const int lc = grp * kLC + k4;                   // 0..8: block entry (r, c); 9..11: gradient component
     const int s = S0 + pi + 2 * l, t = t0 + td;
     const bool valid = s >= sa0 && s < sa1;

@@ -333,7 +333,7 @@ struct PointCtx {
 // each set ordered by its knot index k = lp >> 1 (conflict-free record writes; membrane items first so
 // that warps do not diverge between the two kinds).  pos holds cp rows from prow0.
 // Returns the point's owned energy.
-template <bool CURVED>
+template <bool CURVED, bool HESS>
 __device__ __forceinline__ double eval_item(double* ring, const double* pos, int prow0, const double* cst,
                                          const PointCtx& P, int q0, int it) {
   const int nmem = 2 * kKC;
@@ -363,7 +363,7 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
     rec[2 * kKH] = lap[2];
     if (p >= P.i0 && p < P.i1 && q >= P.ja && q < P.jb)
       return 0.5 * (CURVED ? __ldg(bt + 9 * P.kp) : cst[kCstP + 9]) * cst[kCstP + 8] *
-             (lap[0] * lap[0] + lap[1] * lap[1] + lap[2] * lap[2]);
+             fma(lap[0], lap[0], fma(lap[1], lap[1], lap[2] * lap[2]));
     return 0.0;
   }
   const int r = it >= nmem, mi = it - r * nmem, q = q0 + r;
@@ -404,17 +404,20 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
     for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * G00; f2[c] = Fv[c] * G11; }
   } else {
 #pragma unroll
-    for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * G00 + Fv[c] * G10; f2[c] = Fu[c] * G01 + Fv[c] * G11; }
+    for (int c = 0; c < 3; ++c) { f1[c] = fma(Fu[c], G00, Fv[c] * G10); f2[c] = fma(Fu[c], G01, Fv[c] * G11); }
   }
   double* rec = row + set * kSetD + k;
   double psi, i5 = 1.0;
   // P~_mu = w sum_beta G_mu,beta P_beta;  A~_mu,nu = w sum_{beta,gamma} G_mu,beta G_nu,gamma A_beta,gamma,
   // streamed into the record as fbw_emit forms each F-space entry
-  const auto emit_p = [&](int c, double P1c, double P2c) {
-    rec[(21 + c) * kKH] = wq * (G00 * P1c + G01 * P2c);
-    rec[(24 + c) * kKH] = wq * (G10 * P1c + G11 * P2c);
+  const auto emit_p = [&](int c, double P1c, double P2c) {   // explicit FMAs (see fbw_emit)
+    rec[(21 + c) * kKH] = wq * fma(G00, P1c, G01 * P2c);
+    rec[(24 + c) * kKH] = wq * fma(G10, P1c, G11 * P2c);
   };
-  if (!CURVED && P.diagG) {   // A~uu = w G00^2 A11, A~vv = w G11^2 A22, A~uv = w G00 G11 A12
+  if constexpr (!HESS) {   // no Hessian requested: Psi and P only (the A entries and the projection are dead code)
+    psi = fbw_emit(f1, f2, cst[kCstP + 5], cst[kCstP + 6], cst[kCstP + 7], false, emit_p,
+                   [](int, int, double, double, double, double) {}, &i5);
+  } else if (!CURVED && P.diagG) {   // A~uu = w G00^2 A11, A~vv = w G11^2 A22, A~uv = w G00 G11 A12
     const double auu = wq * G00 * G00, avv = wq * G11 * G11;
     const double auv = wq * G00 * G11;
     psi = fbw_emit(f1, f2, cst[kCstP + 5], cst[kCstP + 6], cst[kCstP + 7], P.project, emit_p,
@@ -446,7 +449,7 @@ __device__ __forceinline__ double eval_item(double* ring, const double* pos, int
 
 // IP: the incremental-potential terms (compiled out of the elastic kernel); CURVED: a non-affine rest map (per-point
 // G, w and Laplacian coefficients and per-cp bending blocks from the CoreTables device tables)
-template <bool IP, bool CURVED>
+template <bool IP, bool CURVED, bool HESS>
 __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);   // [kRing][kRowD]
@@ -568,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
       const int b = it - 3 * 4 * kKC;
       const int pr = mem ? it / (4 * kKC) : b / (2 * kKC);
       const int item = mem ? it - pr * (4 * kKC) : 4 * kKC + b - pr * (2 * kKC);
-      e_acc += eval_item<CURVED>(ring, ppos + 2 * pr * (kPosC * 3), ja - 4 + 2 * pr, cst, P, ja - 3 + 2 * pr, item);
+      e_acc += eval_item<CURVED, HESS>(ring, ppos + 2 * pr * (kPosC * 3), ja - 4 + 2 * pr, cst, P, ja - 3 + 2 * pr, item);
     }
     __syncthreads();
     for (int mi = 3; mi <= nst + 2; ++mi) {
@@ -580,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
       // (a) positions of the next pair (async) and the quadrature points of this pair
       if (mi + 1 <= nst + 1) load_pos_step(pos_s + ((mi + 1) & 1) * (kPosStep * 8), x, A, pm, i0, q0 + 1);
       if (mi <= nst + 1 && pw >= 0 && lane < 30 && !((A.dbg & 1) && k >= 0))
-        e_acc += eval_item<CURVED>(ring, posb + (mi & 1) * kPosStep, q0 - 1, cst, P, q0, pw * 30 + lane);
+        e_acc += eval_item<CURVED, HESS>(ring, posb + (mi & 1) * kPosStep, q0 - 1, cst, P, q0, pw * 30 + lane);
       CT_MARK(T1);
       if (k >= 0) {
         // (b) profiling mode without the gather: the issuing thread releases the staging buffer here (else the
@@ -590,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
           asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(bar) : "memory");
         }
         // (c) gather of rows j, j+1: lanes = 16 control points of parity PI in each of the two rows
-        if (warp < kGatherWarps && !(A.dbg & 2)) {
+        if (HESS && warp < kGatherWarps && !(A.dbg & 2)) {
           // ring rows of knot rows jr-2 .. jr+1 of this lane's row jr = j + h (parity independent)
           const double* rowp[4];
           {
@@ -998,18 +1001,20 @@ int build_core(const Sheet& sh, const int32_t* d_row_ptr, CoreTables& ct, std::s
   }
   ct.smem = sizeof(double) * ((size_t)kRing * kRowD + 2 * kStageRow + kPosD + kCstN) + 16;
   if (ct.smem > 227 * 1024) { err = "core: shared memory budget"; return -1; }
-  if (cudaFuncSetAttribute(k_core<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_core<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_core<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess ||
-      cudaFuncSetAttribute(k_core<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) != cudaSuccess) {
+  const auto attr = [&](auto fn) {
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ct.smem) == cudaSuccess;
+  };
+  if (!attr(k_core<false, false, true>) || !attr(k_core<true, false, true>) || !attr(k_core<false, true, true>) ||
+      !attr(k_core<true, true, true>) || !attr(k_core<false, false, false>) || !attr(k_core<true, false, false>) ||
+      !attr(k_core<false, true, false>) || !attr(k_core<true, true, false>)) {
     cudaGetLastError();
     { if (getenv("BSF_CORE_DEBUG")) fprintf(stderr, "build_core: no core (line %d)\n", __LINE__); return 1; }
   }
   if (getenv("BSF_CORE_DEBUG")) {
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k_core<false, false>);
+    cudaFuncGetAttributes(&fa, k_core<false, false, true>);
     int nb = -1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_core<false, false>, kThreads, ct.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_core<false, false, true>, kThreads, ct.smem);
     fprintf(stderr, "k_core: regs %d maxthreads %d local %zu static smem %zu dyn %zu maxdyn %d occ %d\n", fa.numRegs,
             fa.maxThreadsPerBlock, fa.localSizeBytes, fa.sharedSizeBytes, ct.smem, fa.maxDynamicSharedSizeBytes, nb);
   }
@@ -1112,11 +1117,21 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
   A.mtab = ct.mtab; A.btab = ct.btab; A.beta = ct.beta; A.gw = ct.gw; A.kp = ct.kp; A.cw = ct.cw;
   A.Su = sh.Su; A.Sv = sh.Sv;
   if (ct.curved) {
-    if (A.xhat) k_core<true, true><<<grid, kThreads, ct.smem, st>>>(A);
-    else k_core<false, true><<<grid, kThreads, ct.smem, st>>>(A);
+    if (A.vals) {
+      if (A.xhat) k_core<true, true, true><<<grid, kThreads, ct.smem, st>>>(A);
+      else k_core<false, true, true><<<grid, kThreads, ct.smem, st>>>(A);
+    } else {
+      if (A.xhat) k_core<true, true, false><<<grid, kThreads, ct.smem, st>>>(A);
+      else k_core<false, true, false><<<grid, kThreads, ct.smem, st>>>(A);
+    }
   } else {
-    if (A.xhat) k_core<true, false><<<grid, kThreads, ct.smem, st>>>(A);
-    else k_core<false, false><<<grid, kThreads, ct.smem, st>>>(A);
+    if (A.vals) {
+      if (A.xhat) k_core<true, false, true><<<grid, kThreads, ct.smem, st>>>(A);
+      else k_core<false, false, true><<<grid, kThreads, ct.smem, st>>>(A);
+    } else {   // energy / gradient calls: no Hessian gather, no A entries
+      if (A.xhat) k_core<true, false, false><<<grid, kThreads, ct.smem, st>>>(A);
+      else k_core<false, false, false><<<grid, kThreads, ct.smem, st>>>(A);
+    }
   }
   return cudaPeekAtLastError() == cudaSuccess ? 0 : -6;
 }
