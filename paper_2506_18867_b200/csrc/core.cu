@@ -752,6 +752,105 @@ __global__ void __launch_bounds__(kThreads, 1) k_core(const CoreArgs A) {
   energy_final_fused(A.ef, A.epart, item);
 }
 
+// Energy-only calls on affine sheets (the line search): the quadrature points whose anchor lies in the
+// CTA's [i0, i1) x [ja, jb) (k_core's ownership), one thread per anchor (s, t): its 2 membrane points (V+ and H-
+// when s + t is even, V- and H+ when odd; Q1) and its bending point, straight from the positions in
+// global memory (no ring, no staging, no gather), plus the incremental-potential terms of the control point
+// (s, t).  Same per-point arithmetic as eval_item; the per-CTA sum is in another order than k_core's.
+constexpr int kEThreads = 256;
+
+template <bool IP>
+__global__ void __launch_bounds__(kEThreads) k_core_energy(const CoreArgs A) {
+  __shared__ double c[kCstN];
+  __shared__ double red[kEThreads / 32];
+  const int tid = threadIdx.x;
+  const int strip = blockIdx.x, chunk = blockIdx.y, item = blockIdx.z;
+  const int i0 = A.CI0 + strip * kW, i1 = min(i0 + kW, A.CI1);
+  const int nsteps = (A.JB - A.JA + kRows - 1) / kRows;
+  const int sa = chunk * nsteps / A.nchunks, sb = (chunk + 1) * nsteps / A.nchunks;
+  const int ja = A.JA + kRows * sa, jb = min(A.JA + kRows * sb, A.JB);
+  const double* __restrict__ x = A.x + item * A.xs;
+  double G00 = A.G00, G01 = A.G01, G10 = A.G10, G11 = A.G11, det = A.detJ;
+  double mu1 = A.mu1, mu2 = A.mu2, mush = A.mush, mubd = A.mubd;
+  if (A.params) {
+    const double* pp = A.params + 9 * (int64_t)item;
+    G00 = pp[0]; G01 = pp[1]; G10 = pp[2]; G11 = pp[3]; det = pp[4];
+    mu1 = (A.flags & 2) ? 0.0 : pp[5];
+    mu2 = (A.flags & 2) ? 0.0 : pp[6];
+    mush = (A.flags & 2) ? 0.0 : pp[7];
+    mubd = (A.flags & 4) ? 0.0 : pp[8];
+  }
+  const bool diagG = (G01 == 0.0 && G10 == 0.0);
+  const double cuu = G00 * G00 + G01 * G01, cvv = G10 * G10 + G11 * G11, cuv = 2.0 * (G00 * G10 + G01 * G11);
+  const double wb = A.what[4] * det;
+  if (tid < 9) c[kCstL + tid] = (tid == 8) ? 0.0 : cuu * A.tabs[72 + tid] + cvv * A.tabs[81 + tid] + cuv * A.tabs[90 + tid];
+  if (tid < 72) c[kCstS + tid] = A.tabs[tid];
+  if (tid < 5) c[kCstW + tid] = A.tabs[99 + tid];
+  __syncthreads();
+  const double msc = (IP && A.ipar) ? A.ipar[9 * (int64_t)item + 4] / A.ip_detJ : 1.0;
+  double e_acc = 0.0;
+  const int nw = i1 - i0, na = nw * max(0, jb - ja);
+  for (int a = tid; a < na; a += kEThreads) {
+    const int t = ja + a / nw, s = i0 + a - (a / nw) * nw;
+    const double* xw = x + ((int64_t)(t - A.xlo) * A.n_u + s) * 3;   // window origin (s, t)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int set = ((s + t) & 1) ? (h ? 3 : 0) : (h ? 2 : 1);
+      const bool vset = set < 2;
+      const double* Sset = c + kCstS + set * 18;
+      double Fu[3] = {0, 0, 0}, Fv[3] = {0, 0, 0};
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const int iu = vset ? (q & 1) : (q % 3), jv = vset ? (q >> 1) : (q / 3);
+        const int e = 3 * jv + iu;
+        const double du = Sset[2 * e], dv = Sset[2 * e + 1];
+        const double* C = xw + ((int64_t)jv * A.n_u + iu) * 3;
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) { Fu[cc] = fma(__ldg(C + cc), du, Fu[cc]); Fv[cc] = fma(__ldg(C + cc), dv, Fv[cc]); }
+      }
+      double f1[3], f2[3];
+      if (diagG) {
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) { f1[cc] = Fu[cc] * G00; f2[cc] = Fv[cc] * G11; }
+      } else {
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) { f1[cc] = fma(Fu[cc], G00, Fv[cc] * G10); f2[cc] = fma(Fu[cc], G01, Fv[cc] * G11); }
+      }
+      double i5 = 1.0;
+      const double psi = fbw_emit(f1, f2, mu1, mu2, mush, false, [](int, double, double) {},
+                                  [](int, int, double, double, double, double) {}, &i5);
+      e_acc += c[kCstW + set] * det * psi;
+      fbw_flag_singular(A.sflag, i5, item, s, t);
+    }
+    double lap[3] = {0, 0, 0};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const double L = c[kCstL + e];
+      const double* C = xw + ((int64_t)(e / 3) * A.n_u + e % 3) * 3;
+      lap[0] = fma(L, __ldg(C), lap[0]); lap[1] = fma(L, __ldg(C + 1), lap[1]); lap[2] = fma(L, __ldg(C + 2), lap[2]);
+    }
+    e_acc += 0.5 * wb * mubd * fma(lap[0], lap[0], fma(lap[1], lap[1], lap[2] * lap[2]));
+    if constexpr (IP) {
+      const int64_t al = (int64_t)(t - A.r0) * A.n_u + s;
+      const double mm = A.mass[al] * msc;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const double xa = xw[r], d = xa - A.xhat[item * A.xhs + al * 3 + r];
+        e_acc += 0.5 * A.ipk * mm * d * d - mm * A.grav[r] * xa;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) e_acc += __shfl_xor_sync(0xffffffffu, e_acc, o);
+  if ((tid & 31) == 0) red[tid >> 5] = e_acc;
+  __syncthreads();
+  if (tid == 0) {
+    double sum = 0.0;
+    for (int w = 0; w < kEThreads / 32; ++w) sum += red[w];
+    A.epart[item * A.e_stride + A.e_off + (int64_t)chunk * A.nstrips + strip] = sum;
+  }
+  energy_final_fused(A.ef, A.epart, item);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------------------------------ host
@@ -1125,9 +1224,13 @@ int core_eval(const CoreTables& ct, const Sheet& sh, const double* d_x, int64_t 
       else k_core<false, true, false><<<grid, kThreads, ct.smem, st>>>(A);
     }
   } else {
+    static const bool no_ekernel = getenv("BSF_CORE_NO_EKERNEL") != nullptr;   // test switch
     if (A.vals) {
       if (A.xhat) k_core<true, false, true><<<grid, kThreads, ct.smem, st>>>(A);
       else k_core<false, false, true><<<grid, kThreads, ct.smem, st>>>(A);
+    } else if (!A.g && !no_ekernel) {   // energy only: no ring, no gather (k_core_energy)
+      if (A.xhat) k_core_energy<true><<<grid, kEThreads, 0, st>>>(A);
+      else k_core_energy<false><<<grid, kEThreads, 0, st>>>(A);
     } else {   // energy / gradient calls: no Hessian gather, no A entries
       if (A.xhat) k_core<true, false, false><<<grid, kThreads, ct.smem, st>>>(A);
       else k_core<false, false, false><<<grid, kThreads, ct.smem, st>>>(A);

@@ -133,8 +133,53 @@ def test_deterministic_and_partial_outputs():
         s.eval_gradient(xd, g3, B.PROJECT_PSD | path)
         v3 = torch.zeros_like(v1)
         s.assemble_hessian(xd, v3, B.PROJECT_PSD | path)
-        assert torch.equal(E1, E3) and torch.equal(g1, g3) and torch.equal(v1, v3)
+        # gradient and Hessian: the same bits; the energy-only call sums the same point energies in another order
+        # (k_core_energy: one thread per anchor instead of the point warps), so to rounding
+        assert torch.equal(g1, g3) and torch.equal(v1, v3)
+        assert abs(E1.item() - E3.item()) <= 1e-14 * abs(E1.item())
         assert s.last_launch_count() > 0
+
+
+def test_energy_only_calls_match_full_calls():
+    """Energy-only calls (the line search) through k_core_energy: plain, batched with per-item parameters, and the
+    incremental potential; each against the full call's energy (1e-13) and the oracle's (the parity floor)."""
+    sh = W.make_c2(state=3)
+    s = B.Sheet.from_sheet(sh)
+    xd = torch.from_numpy(sh.x).cuda()
+    E1, _, _ = s(xd, B.PROJECT_PSD)
+    E2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    s.eval_energy(xd, E2, B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    Er, _, _ = O.Oracle.from_sheet(sh).eval(sh.x, flags=O.FLAG_PROJECT)
+    assert abs(E2.item() - E1.item()) <= 1e-13 * abs(E1.item())
+    assert abs(E2.item() - Er) <= 1e-11 * abs(Er)
+    # batched, per-item parameters (C5 style), energy only vs the full batch
+    sheets = W.make_c5(count=3, n=64)
+    h = B.Sheet.from_sheet(sheets[0])
+    X = torch.stack([torch.from_numpy(q.x) for q in sheets]).cuda()
+    P = torch.from_numpy(np.stack([B.affine_params(q.rest_xy, B.material_from_young(q.E, q.nu, q.h))
+                                   for q in sheets])).cuda()
+    Ef = torch.zeros(3, dtype=torch.float64, device="cuda")
+    G = torch.zeros_like(X)
+    V = torch.zeros((3, h.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    h.eval_all_batch_params(X, P, Ef, G, V, B.PROJECT_PSD)
+    Ee = torch.zeros(3, dtype=torch.float64, device="cuda")
+    h.eval_all_batch_params(X, P, Ee, None, None, B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    assert torch.max(torch.abs(Ee - Ef)).item() <= 1e-13 * torch.max(torch.abs(Ef)).item()
+    # incremental potential, energy only
+    s.set_inertia(0.15, 2e-3, gravity=np.array([0.0, 0.0, -9.81]))
+    rng = np.random.default_rng(5)
+    xh = torch.from_numpy(sh.x + rng.normal(0, 1e-3, sh.x.shape)).cuda().unsqueeze(0).contiguous()
+    X1 = xd.unsqueeze(0).contiguous()
+    Ei = torch.zeros(1, dtype=torch.float64, device="cuda")
+    Gi = torch.zeros_like(X1)
+    Vi = torch.zeros((1, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    s.eval_ip_batch(X1, xh, Ei, Gi, Vi, B.PROJECT_PSD)
+    Eo = torch.zeros(1, dtype=torch.float64, device="cuda")
+    s.eval_ip_batch(X1, xh, Eo, None, None, B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    assert abs(Eo.item() - Ei.item()) <= 1e-13 * abs(Ei.item())
 
 
 def test_c4_full_size():
