@@ -237,18 +237,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_band(const BandArgs A) {
       const double wq = A.mwhat[D.cls0 + cls] * kc[4];
       double f1[3], f2[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * kc[0] + Fv[c] * kc[2]; f2[c] = Fu[c] * kc[1] + Fv[c] * kc[3]; }
+      for (int c = 0; c < 3; ++c) { f1[c] = fma(Fu[c], kc[0], Fv[c] * kc[2]); f2[c] = fma(Fu[c], kc[1], Fv[c] * kc[3]); }
       double* r = rec + kRecC * cls + kRecP * m;
       const auto emit_p = [&](int c, double P1c, double P2c) {   // P~_mu = w sum_beta G_mu,beta P_beta
-        r[rec_pos(21 + c)] = wq * (kc[0] * P1c + kc[1] * P2c);
-        r[rec_pos(24 + c)] = wq * (kc[2] * P1c + kc[3] * P2c);
+        r[rec_pos(21 + c)] = wq * fma(kc[0], P1c, kc[1] * P2c);
+        r[rec_pos(24 + c)] = wq * fma(kc[2], P1c, kc[3] * P2c);
       };
       const double wG00 = wq * kc[0], wG01 = wq * kc[1], wG10 = wq * kc[2], wG11 = wq * kc[3];
       const double a11 = wG00 * kc[0], a12 = wG00 * kc[1], a22 = wG01 * kc[1];
       const double b11 = wG10 * kc[2], b12 = wG10 * kc[3], b22 = wG11 * kc[3];
       const double c11 = wG00 * kc[2], c12 = wG00 * kc[3], c21 = wG01 * kc[2], c22 = wG01 * kc[3];
       double i5 = 1.0;
-      const double psi = fbw_emit(f1, f2, kc[5], kc[6], kc[7], A.project != 0, emit_p,
+      const double psi = !A.vals   // no Hessian values requested: Psi and P only (explicit FMAs: the same bits)
+          ? fbw_emit(f1, f2, kc[5], kc[6], kc[7], false, emit_p, [](int, int, double, double, double, double) {}, &i5)
+          : fbw_emit(f1, f2, kc[5], kc[6], kc[7], A.project != 0, emit_p,
                                   [&](int r3, int c3, double A11, double A22, double A12rc, double A12cr) {
         const int e6 = sym3(r3, c3);
         r[rec_pos(e6)] = a11 * A11 + a12 * (A12rc + A12cr) + a22 * A22;

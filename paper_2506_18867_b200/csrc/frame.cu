@@ -155,13 +155,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_frame(const FrameArgs A) {
       const double wq = A.m_what[p] * kc[4];
       double f1[3], f2[3];
 #pragma unroll
-      for (int c = 0; c < 3; ++c) { f1[c] = Fu[c] * kc[0] + Fv[c] * kc[2]; f2[c] = Fu[c] * kc[1] + Fv[c] * kc[3]; }
+      for (int c = 0; c < 3; ++c) { f1[c] = fma(Fu[c], kc[0], Fv[c] * kc[2]); f2[c] = fma(Fu[c], kc[1], Fv[c] * kc[3]); }
       double psi, i5 = 1.0;
       const auto emit_p = [&](int c, double P1c, double P2c) {   // P~_mu = w sum_beta G_mu,beta P_beta
-        rec[21 + c] = wq * (kc[0] * P1c + kc[1] * P2c);
-        rec[24 + c] = wq * (kc[2] * P1c + kc[3] * P2c);
+        rec[21 + c] = wq * fma(kc[0], P1c, kc[1] * P2c);
+        rec[24 + c] = wq * fma(kc[2], P1c, kc[3] * P2c);
       };
-      if (kc[1] == 0.0 && kc[2] == 0.0) {   // axis-aligned rest map: A~ by entrywise scaling
+      if (!A.vals) {   // no Hessian values requested: Psi and P only (explicit FMAs: the same bits as below)
+        psi = fbw_emit(f1, f2, kc[5], kc[6], kc[7], false, emit_p, [](int, int, double, double, double, double) {},
+                       &i5);
+      } else if (kc[1] == 0.0 && kc[2] == 0.0) {   // axis-aligned rest map: A~ by entrywise scaling
         const double auu = wq * kc[0] * kc[0], avv = wq * kc[3] * kc[3], auv = wq * kc[0] * kc[3];
         psi = fbw_emit(f1, f2, kc[5], kc[6], kc[7], A.project != 0, emit_p,
                        [&](int r3, int c3, double A11, double A22, double A12rc, double A12cr) {
@@ -217,6 +220,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_frame(const FrameArgs A) {
   const uint4 task = A.lst[tile * kTasks + tk];
   const int first = task.x & 0xFFFFF, cnt = task.x >> 20;
   const int out = (int)task.y, outT = (int)task.z;
+  if (out >= 0 && !A.vals) continue;   // a Hessian block task of a call without Hessian values
   if (cnt > 0 && out >= 0) {
     double h[9];
 #pragma unroll
