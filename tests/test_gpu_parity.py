@@ -180,6 +180,14 @@ def test_energy_only_calls_match_full_calls():
     s.eval_ip_batch(X1, xh, Eo, None, None, B.PROJECT_PSD)
     torch.cuda.synchronize()
     assert abs(Eo.item() - Ei.item()) <= 1e-13 * abs(Ei.item())
+    # a row slab (its core rows only, its own energy share)
+    sl = B.Sheet.from_sheet(sh, row_begin=40, row_end=90)
+    xs = torch.from_numpy(np.ascontiguousarray(sh.x[sl.x_row_begin:sl.x_row_end])).cuda()
+    Es, _, _ = sl(xs, B.PROJECT_PSD)
+    Ese = torch.zeros(1, dtype=torch.float64, device="cuda")
+    sl.eval_energy(xs, Ese, B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    assert abs(Ese.item() - Es.item()) <= 1e-13 * abs(Es.item())
 
 
 def test_c4_full_size():

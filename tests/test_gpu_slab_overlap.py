@@ -28,6 +28,13 @@ for r0, r1 in [(0, 128), (40, 90), (0, 64), (64, 128)]:
     assert s.last_launch_count() >= 3, s.last_launch_count()
     assert torch.equal(g1, g2) and torch.equal(v1, v2), (r0, r1)
     assert abs(E1.item() - E2.item()) <= 1e-13 * abs(E1.item())
+    # partial outputs on the split schedule: energy only (k_core_energy per row range), gradient only
+    E3 = torch.zeros_like(E1); g3 = torch.zeros_like(g1)
+    s.eval_all_slab(x, E3, None, None, flags=B.PROJECT_PSD)
+    s.eval_all_slab(x, None, g3, None, flags=B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    assert abs(E3.item() - E1.item()) <= 1e-13 * abs(E1.item()), (r0, r1, E3.item(), E1.item())
+    assert torch.equal(g3, g1), (r0, r1)
     o = O.Oracle.from_sheet(sh, r0=r0, r1=r1)
     Er, gr, vr = o.eval(sh.x, flags=O.FLAG_PROJECT)
     rp, ci = o.pattern()
