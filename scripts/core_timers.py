@@ -2,8 +2,8 @@
 import sys, os, ctypes as C
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, numpy as np, workloads as W, paper_2506_18867_b200 as B
-sh = W.make_c4() if "--c4" in sys.argv else W.make_c2(0)
-nst = 1 if ("--c4" in sys.argv or "--single" in sys.argv) else 100
+sh = W.make_c4() if "--c4" in sys.argv else W.make_c3() if "--c3" in sys.argv else W.make_c2(0)
+nst = 1 if ("--c4" in sys.argv or "--c3" in sys.argv or "--single" in sys.argv) else 100
 h = B.Sheet.from_sheet(sh)
 X = torch.from_numpy(sh.x).cuda().unsqueeze(0).repeat(nst, 1, 1, 1).contiguous()
 E = torch.zeros(nst, dtype=torch.float64, device="cuda")
