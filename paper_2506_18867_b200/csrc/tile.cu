@@ -966,20 +966,34 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
     if (cudaEventRecord(tt.ev_fork, st) != cudaSuccess || cudaStreamWaitEvent(tt.side, tt.ev_fork, 0) != cudaSuccess ||
         (small && cudaStreamWaitEvent(tt.side2, tt.ev_fork, 0) != cudaSuccess))
       return -6;
-    rc = frame_eval(*ft, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
-                        tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, fst, ip);
-    if (rc) return rc;
+    // Small problems whose core, band and corner CTAs together exceed the SMs (one C3 sheet: 112 + 56 + 4): launch
+    // k_core first.  The CTA scheduler spreads a kernel's CTAs over idle SMs before doubling up, so band CTAs that
+    // start first hold one SM each and push the last core CTAs into a second wave (C3 graph replays 63 -> 46 us;
+    // direct calls, where the memset in front already lines the three up, are unchanged).
+    const bool cf = !ov && small &&
+                    (int64_t)core_ctas_per_item(*ct, core_nch) * nbatch + (int64_t)ft->band.nctas * nbatch +
+                            (int64_t)ft->ntiles * nbatch > 148;
     cudaEvent_t* tv = nullptr;   // [core start, core end, band start, band end] of this call
     if (tt.tev_n > 0) {
       tv = tt.tev.data() + 4 * tt.tev_next;
       tt.tev_next = (tt.tev_next + 1) % tt.tev_n;
       tt.tev_count = std::min(tt.tev_count + 1, tt.tev_n);
-      if (cudaEventRecord(tv[2], tt.side) != cudaSuccess) return -6;
     }
+    if (cf) {
+      if (tv && cudaEventRecord(tv[0], st) != cudaSuccess) return -6;
+      rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
+                     nfb, core_nch, d_params, tt.detJ_ref, st, ip);
+      if (rc) return rc;
+    }
+    rc = frame_eval(*ft, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
+                        tt.e_part, e_stride, 0, d_params, ct->G, ct->detJ, fst, ip);
+    if (rc) return rc;
+    if (tv && cudaEventRecord(tv[2], tt.side) != cudaSuccess) return -6;
     rc = band_eval(ft->band, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.row_ptr,
                    tt.e_part, e_stride, ft->ntiles, d_params, ct->G, ct->detJ, tt.side, ip);
     if (rc) return rc;
-    if (tv && (cudaEventRecord(tv[3], tt.side) != cudaSuccess || cudaEventRecord(tv[0], st) != cudaSuccess)) return -6;
+    if (tv && (cudaEventRecord(tv[3], tt.side) != cudaSuccess || (!cf && cudaEventRecord(tv[0], st) != cudaSuccess)))
+      return -6;
     if (ov) {
       const int64_t o1 = nfb + core_ctas_per_item(*ct, core_nch), o2 = o1 + nb_lo;
       rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
@@ -987,7 +1001,7 @@ int tile_eval(TileTables& tt, const Sheet& sh, const double* d_x, int64_t x_stri
       if (rc) return rc;
       rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
                      o2, 1, d_params, tt.detJ_ref, st, ip, halo->jb, ct->RJ1);
-    } else {
+    } else if (!cf) {
       rc = core_eval(*ct, sh, d_x, x_stride, mat, flags, nbatch, d_g, g_stride, d_vals, v_stride, tt.e_part, e_stride,
                      nfb, core_nch, d_params, tt.detJ_ref, st, ip);
     }
