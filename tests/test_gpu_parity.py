@@ -600,3 +600,37 @@ def test_incremental_potential_curved_rest():
     va = o.eval_ip(sh.x, xh, m, dt, grav, flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
     assert_parity(E.item(), G[0].cpu().numpy(), V[0].cpu().numpy(), Er, gr, vr, what="IP curved rest",
                   hdiag=diag_block_norms(vr, rp, ci, 0, 20), cmax=np.abs(sh.x).max(), vabs=va)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_random_sizes_slabs_and_batches(seed):
+    """Randomised coverage of the launch shapes the chunking and stream logic pick (one-wave slabs, side streams,
+    k_core-first ordering, ragged strips, batches): random grid sizes, slab bounds and batch sizes, the full call
+    and the energy-only call, against the oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    n_u, n_v = int(rng.integers(12, 96)), int(rng.integers(12, 96))
+    ku, kv = W.open_uniform_knots(n_u), W.open_uniform_knots(n_v)
+    rest = W.greville_grid(n_u, n_v, float(rng.uniform(0.5, 2.0)), float(rng.uniform(0.5, 2.0)))
+    nb = int(rng.integers(1, 4))
+    xs = [np.concatenate([rest, np.zeros((n_v, n_u, 1))], -1) + rng.normal(0, 1e-2, (n_v, n_u, 3)) for _ in range(nb)]
+    sh = W.Sheet(n_u, n_v, ku, kv, rest, xs[0], 1e5, 0.3, 3e-4)
+    r0 = int(rng.integers(0, n_v // 3)) if rng.uniform() < 0.5 else 0
+    r1 = int(rng.integers(r0 + 2 + (n_v - r0 - 2) // 2, n_v + 1)) if r0 > 0 else n_v
+    o = O.Oracle.from_sheet(sh, r0=r0, r1=r1)
+    s = B.Sheet.from_sheet(sh, row_begin=r0, row_end=r1)
+    X = torch.stack([torch.from_numpy(np.ascontiguousarray(x[s.x_row_begin:s.x_row_end])) for x in xs]).cuda()
+    E = torch.zeros(nb, dtype=torch.float64, device="cuda")
+    G = torch.zeros((nb, r1 - r0, n_u, 3), dtype=torch.float64, device="cuda")
+    V = torch.zeros((nb, s.nnzb, 3, 3), dtype=torch.float64, device="cuda")
+    s.eval_all_batch(X, E, G, V, B.PROJECT_PSD)
+    Ee = torch.zeros(nb, dtype=torch.float64, device="cuda")
+    s.eval_all_batch(X, Ee, None, None, B.PROJECT_PSD)
+    torch.cuda.synchronize()
+    rp, ci = o.pattern()
+    for k in range(nb):
+        Er, gr, vr = o.eval(xs[k], flags=O.FLAG_PROJECT)
+        va = o.eval(xs[k], flags=O.FLAG_PROJECT | O.FLAG_ABS_SUM, energy=False, gradient=False)[2]
+        assert_parity(E[k].item(), G[k].cpu().numpy(), V[k].cpu().numpy(), Er, gr, vr,
+                      what=f"n={n_u}x{n_v} rows [{r0},{r1}) item {k}/{nb}",
+                      hdiag=diag_block_norms(vr, rp, ci, r0, n_u), cmax=np.abs(xs[k]).max(), vabs=va)
+        assert abs(Ee[k].item() - E[k].item()) <= 1e-13 * max(abs(E[k].item()), 1e-300)
