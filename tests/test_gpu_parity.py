@@ -602,13 +602,14 @@ def test_incremental_potential_curved_rest():
                   hdiag=diag_block_norms(vr, rp, ci, 0, 20), cmax=np.abs(sh.x).max(), vabs=va)
 
 
-@pytest.mark.parametrize("seed", range(16))
+@pytest.mark.parametrize("seed", list(range(16)) + [100, 101, 102])
 def test_random_sizes_slabs_and_batches(seed):
     """Randomised coverage of the launch shapes the chunking and stream logic pick (one-wave slabs, side streams,
     k_core-first ordering, ragged strips, batches): random grid sizes, slab bounds and batch sizes, the full call
     and the energy-only call, against the oracle."""
     rng = np.random.default_rng(1000 + seed)
-    n_u, n_v = int(rng.integers(12, 96)), int(rng.integers(12, 96))
+    lo, hi = (12, 96) if seed < 100 else (200, 420)   # seeds >= 100: grids with many core strips (multi-wave paths)
+    n_u, n_v = int(rng.integers(lo, hi)), int(rng.integers(lo, hi))
     ku, kv = W.open_uniform_knots(n_u), W.open_uniform_knots(n_v)
     rest = W.greville_grid(n_u, n_v, float(rng.uniform(0.5, 2.0)), float(rng.uniform(0.5, 2.0)))
     nb = int(rng.integers(1, 4))
