@@ -116,6 +116,19 @@ def test_host_only_handle_refuses_every_compute_entry_point():
     it, rr = C.c_int(), C.c_double()
     assert L.bsf_pcg(s._h, p, p, p, 10, 1e-8, C.byref(it), C.byref(rr), None) == no_dev
     assert L.bsf_set_kernel_timing(s._h, 4) == no_dev
+    # round-2 entry points: device work refused (NO_DEVICE); calls that need an earlier device result
+    # (a factorisation, a contact mesh / assembly) refuse with INVALID_ARG, pointers untouched
+    assert L.bsf_chol_factor(s._h, p, None) == no_dev
+    assert L.bsf_chol_solve(s._h, p, p, None) == -1
+    g, t = C.c_double(), C.c_int()
+    assert L.bsf_neumann_solve(s._h, p, p, p, 10, 1e-10, C.byref(g), C.byref(t), None) == -1
+    uv = np.array([[0.5, 0.5]])
+    assert L.bsf_contact_mesh(s._h, 1, uv.ctypes.data_as(C.POINTER(C.c_double))) == no_dev
+    assert L.bsf_contact_positions(s._h, p, p, None) == -1
+    n = C.c_int64()
+    assert L.bsf_contact_assemble(s._h, 1, p, p, p, p, p, C.byref(n), None) == -1
+    assert L.bsf_contact_get(s._h, p, p, p, None) == -1
+    assert L.bsf_contact_neumann_solve(s._h, p, p, 10, 1e-10, C.byref(g), C.byref(t), None) == -1
     s.set_inertia(0.2, 1e-3, gravity=(0, 0, -9.81))
     assert s.lumped_mass().shape == (sh.n_v, sh.n_u)
     assert L.bsf_eval_ip_batch(s._h, 1, p, 0, p, 0, None, p, p, 0, p, 0, 0, None) == no_dev
