@@ -31,3 +31,15 @@ def test_algorithmic_model_matches_survey():
     assert abs(bench.algorithmic_bytes(128 * 128, bench.reduced_nnzb(128)) / 1e6 - 27.51) < 0.01
     # SURVEY §8(d) flop table: C4 4.37 GFLOP (symmetric model) from the point counts 2,109,394 and 1,046,525
     assert abs(bench.algorithmic_flops(2109394, 1046525) / 1e9 - 4.32) < 0.06
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    """--gpus 2 without a torchrun environment re-launches bench.py under torch.distributed.run (127.0.0.1); in the
+    reference arm rank 0 alone runs and prints one JSON line, rank 1 exits 0 without work."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0
