@@ -72,6 +72,9 @@ def reduced_nnzb(n):
     return 23 * S * S + 48 * S + 8
 
 
+THROTTLE = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
 class Clocks:
     """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
 
@@ -383,6 +386,15 @@ def bench_c4(args, rank, world, local_rank):
         torch.distributed.barrier()
     with Clocks(local_rank) as clk:
         ms, _ = _timed(torch, step, args.steps, stream)   # no per-call events: each costs ~2.5 us of the step
+    remeasured = False
+    if set(clk.summary()["reasons"]) & THROTTLE:   # a throttled run is re-measured once (the contract's rule)
+        if core_timed:
+            slab.h.set_kernel_timing(args.steps)
+        if world > 1:
+            torch.distributed.barrier()
+        with Clocks(local_rank) as clk:
+            ms, _ = _timed(torch, step, args.steps, stream)
+        remeasured = True
     core_ms, band_ms = slab.h.kernel_timing(args.steps) if core_timed else ([], [])
     if core_timed:
         slab.h.set_kernel_timing(0)
@@ -485,7 +497,7 @@ def bench_c4(args, rank, world, local_rank):
                         "energy is read back; gradient and Hessian stay on the device (their consumer, the Newton "
                         "solve, runs on the device)"},
         "gpu_launches": launches * args.steps,
-        "clocks": clk.summary(),
+        "clocks": dict(clk.summary(), remeasured=remeasured),
     }
     if world == 1 and not args.no_secondary:
         torch.cuda.empty_cache()
