@@ -433,11 +433,13 @@ def test_async_stage_pipelined_host_calls():
         assert torch.equal(Eh, E.cpu())
 
 
-@pytest.mark.parametrize("case", ["c1", "c2_pinned", "slab"])
+@pytest.mark.parametrize("case", ["c1", "c2_pinned", "slab", "c3_size"])
 def test_incremental_potential_matches_oracle(case):
     """bsf_eval_ip_batch (elastic assembly + lumped-mass inertia, gravity, pinned elimination) against the
-    oracle's eval_ip, every path, a batch of 2 items with different predicted positions."""
-    sh = W.make_c1() if case == "c1" else W.make_c2(state=4)
+    oracle's eval_ip, every path, a batch of 2 items with different predicted positions.  c3_size: a 200^2 sheet,
+    whose core, band and corner CTAs overfill the SMs (k_core launched first)."""
+    sh = (W.make_c1() if case == "c1" else
+          W.make_sheet(200, 1.5, 5, n_modes=4, amp=5e-3, lam=0.2) if case == "c3_size" else W.make_c2(state=4))
     r0, r1 = (40, 90) if case == "slab" else (0, sh.n_v)
     R0, dt, grav = 0.15, 4e-3, np.array([0.0, -9.81, 0.5])
     pinned = None
@@ -454,7 +456,9 @@ def test_incremental_potential_matches_oracle(case):
     rng = np.random.default_rng(17)
     s = B.Sheet.from_sheet(sh, row_begin=r0, row_end=r1)
     s.set_inertia(R0, dt, gravity=grav, pinned=pinned)
-    assert np.max(np.abs(s.lumped_mass() - m)) < 1e-14 * m.max()
+    # the library integrates m_a = int R0 N_a directly, the oracle sums the consistent mass rows: the same number
+    # up to summation order (1.2e-14 of max m on the 200^2 sheet)
+    assert np.max(np.abs(s.lumped_mass() - m)) < 1e-13 * m.max()
     xs = [sh.x, sh.x + rng.normal(0, 1e-3, sh.x.shape)]
     xh = [x[r0:r1] + rng.normal(0, 2e-3, x[r0:r1].shape) for x in xs]
     X = torch.stack([torch.from_numpy(np.ascontiguousarray(x[s.x_row_begin:s.x_row_end])) for x in xs]).cuda()
